@@ -1,0 +1,159 @@
+/*
+ * compass_moe.h — C ABI of the B200-native (sm_100a) MoE-layer hot path.
+ *
+ * Drop-in for the MoE-layer operations the reference specifies and composes from its tensor
+ * primitives:
+ *   route_tokens(hidden, router_weights) -> RouterDecision
+ *   moe_forward(hidden, decision, experts) -> out
+ *   aux_loss(decision) / z_loss(logits)
+ *                                (proj/src/tensor.cpp:980-1040 ops::moe_aux_loss / ops::z_loss)
+ *   fp8_qdq / quantize_model (expert-aware E4M3 W8A8 scheme)
+ * and keeps the conventions of the reference C API proj/include/compass_lab.h:20-50 /
+ * proj/src/capi.cpp:13-68: an opaque handle, cl_status return codes (same values as
+ * compass_lab.h:23-27), per-handle last-error string owned by the handle ("" if none), configuration
+ * errors -> CL_ERR_CONFIG, every other failure (CUDA error, non-finite output, bad runtime input)
+ * -> CL_ERR_RUN.
+ *
+ * Memory: unless a function says "host", tensor pointers are DEVICE pointers on the handle's GPU
+ * and `stream` is a cudaStream_t (NULL = legacy default stream). Calls are asynchronous on
+ * `stream` except where noted; the handle owns its weights and workspaces. One handle per
+ * (process, GPU); callers serialise calls on a handle (as with cl_lab).
+ *
+ * Layouts (row-major, reference orientation):
+ *   hidden / out        [T x d]        bf16 (the device path's storage type)
+ *   w_router            [d x N]        fp32 (router gating stays fp32, PAPER §2.3.4)
+ *   w_in  (expert e)    [d x 2f]       columns [0,f) = gate, [f,2f) = up
+ *   w_out (expert e)    [f x d]
+ *   topk_idx            [T x K] int32, descending probability, ties -> lowest expert index
+ *   combine_weights     [T x K] fp32  (top-K probabilities renormalised to sum 1)
+ */
+#ifndef COMPASS_MOE_H
+#define COMPASS_MOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef COMPASS_LAB_H
+/* Identical to compass_lab.h:23-27 so both headers can be included together. */
+typedef enum cl_status {
+  CL_OK = 0,        /* success */
+  CL_ERR_RUN = 1,   /* validation or runtime failure */
+  CL_ERR_CONFIG = 2 /* bad config or bad arguments */
+} cl_status;
+#endif
+
+typedef struct cl_moe cl_moe;
+
+typedef enum cl_moe_precision {
+  CL_MOE_BF16 = 0,    /* bf16 operands, fp32 accumulate */
+  CL_MOE_FP8_E4M3 = 1 /* expert-aware W8A8: e4m3 operands, per-expert act scale, per-channel W scale */
+} cl_moe_precision;
+
+typedef enum cl_moe_io_dtype { CL_MOE_IO_BF16 = 0, CL_MOE_IO_F32 = 1 } cl_moe_io_dtype;
+
+typedef struct cl_moe_config {
+  int64_t d_model;    /* d  (multiple of 256) */
+  int64_t n_experts;  /* N  (global expert count, 1..128) */
+  int64_t top_k;      /* K  (1..min(N,8)) */
+  int64_t d_ff;       /* f  (multiple of 128) */
+  int64_t max_tokens; /* capacity: tokens per call on this rank */
+  int32_t device;     /* CUDA device ordinal */
+  int32_t gemm_ctas;  /* 0 = auto, 1 = cta_group::1 (M=128), 2 = cta_group::2 (M=256) */
+  int32_t ep_size;    /* expert-parallel ranks (1 = single GPU) */
+  int32_t ep_rank;    /* this rank; owns experts [rank*N/ep_size, (rank+1)*N/ep_size) */
+} cl_moe_config;
+
+/* Routing result (SPEC RouterDecision). Device pointers; NULL fields skipped. */
+typedef struct cl_moe_decision {
+  float* logits;          /* [T x N] */
+  float* probs;           /* [T x N] */
+  int32_t* topk_idx;      /* [T x K] */
+  float* combine_weights; /* [T x K] */
+  int64_t* counts;        /* [N]   c_i, sums to T*K exactly */
+  float* agg_prob;        /* [N]   p_i = sum_j probs[j][i] */
+  float* aux_loss;        /* [1]   N * sum_i (p_i/B)(c_i/(B K))  (ops::moe_aux_loss) */
+  float* z_loss;          /* [1]   (1/B) sum_j lse_j^2            (ops::z_loss) */
+} cl_moe_decision;
+
+/* Internal per-call workspaces, exposed read-only for stage-level parity checks. */
+typedef struct cl_moe_stage_view {
+  const int32_t* offsets;  /* [N_local+1] expert segment starts in the permuted row space */
+  const int32_t* perm;     /* [T*K] permuted row r -> slot j*K+k */
+  const int32_t* inv;      /* [T*K] slot j*K+k -> permuted row r */
+  const float* row_weight; /* [T*K] combine weight of permuted row r */
+  const void* x_perm;      /* [T*K x d] GEMM1 operand (bf16, or e4m3 in FP8 mode) */
+  const void* act;         /* [T*K x f] SwiGLU output / GEMM2 operand (bf16, or e4m3) */
+  const void* y;           /* [T*K x d] bf16 weighted expert outputs */
+  int64_t rows;            /* T*K of the last call */
+} cl_moe_stage_view;
+
+const char* cl_moe_version(void);
+
+/* Creates a layer from reference-layout fp32 HOST weights: w_router [d x N], w_in [N][d][2f],
+ * w_out [N][f][d]. The handle keeps bf16 copies repacked K-major for the tensor cores. With
+ * ep_size > 1, w_in / w_out hold only this rank's N/ep_size experts. */
+cl_status cl_moe_create(const cl_moe_config* cfg, const float* w_router, const float* w_in,
+                        const float* w_out, cl_moe** out);
+
+/* Creates a layer whose weights are generated on the device from the reference counter PRNG
+ * (proj/include/compasslab/prng.hpp) exactly as SURVEY.md §8(d) prescribes (root seed `seed`). */
+cl_status cl_moe_create_synthetic(const cl_moe_config* cfg, uint64_t seed, cl_moe** out);
+
+void cl_moe_destroy(cl_moe* h);
+
+/* Message of the most recent failing call on this handle ("" if none); owned by the handle. */
+const char* cl_moe_last_error(const cl_moe* h);
+
+/* Synthetic tokens x = split(1) N(0,1) of root seed `seed`, rounded to bf16: [T x d] device. */
+cl_status cl_moe_synthetic_tokens(cl_moe* h, uint64_t seed, int64_t T, void* x, void* stream);
+
+/* route_tokens. */
+cl_status cl_moe_route_tokens(cl_moe* h, const void* hidden, int64_t T, const cl_moe_decision* out,
+                              void* stream);
+
+/* moe_forward with a caller-supplied decision. */
+cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int32_t* topk_idx,
+                             const float* combine_weights, void* out, void* stream);
+
+/* The fused layer: route_tokens + dispatch + expert FFN + combine. `out` bf16 [T x d].
+ * `decision` may be NULL. */
+cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
+                         const cl_moe_decision* decision, void* stream);
+
+/* Same layer through HOST buffers (the reference-facing call): copies hidden in, runs the
+ * layer and copies the output back; synchronous. io_dtype selects bf16 or fp32 host tensors. */
+cl_status cl_moe_forward_host(cl_moe* h, const void* hidden_host, int64_t T, void* out_host,
+                              int32_t io_dtype);
+
+/* Waits for `stream` and reports device-side failures: any non-finite router logit or layer
+ * output (the reference's check_finite, proj/src/tensor.cpp:35-41) -> CL_ERR_RUN. */
+cl_status cl_moe_sync(cl_moe* h, void* stream);
+
+/* Stage buffers of the last call (valid until the next call on the handle). */
+cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* view);
+
+/* Copies stage buffer `which` (0 offsets, 1 perm, 2 inv, 3 row_weight, 4 x_perm, 5 act, 6 y)
+ * into the device buffer `dst` (`bytes` bytes), stream-ordered after the last call. */
+cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, void* stream);
+
+/* Expert-aware FP8. Calibration (collect_calibration) runs
+ * the bf16 layer on `hidden` and accumulates per-expert activation maxima of the GEMM1 input and
+ * the SwiGLU output; quantize then sets per-expert activation scales = max/448 and per-(expert,
+ * output channel) weight scales = channel absmax/448 and switches the
+ * handle's precision. act_scale_* may be given explicitly (host arrays [N_local]) instead. */
+cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream);
+cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float* act_scale_mid);
+cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
+/* Host copies of the FP8 scales in use: [N_local], [N_local], [N_local x 2f], [N_local x d]. */
+cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,
+                                float* w_out_scale);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COMPASS_MOE_H */

@@ -1,0 +1,163 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY.
+//
+// The reference's MoE layer, composed from the reference's OWN primitives. The reference
+// (compass-lab) implements every building block (compasslab::ops in proj/src/tensor.cpp) but
+// not the layer itself, which exists only in SPEC.md:147-182. This file is the thinnest possible
+// composition of those ops per SPEC; it is compiled TOGETHER WITH the reference sources, straight
+// from /root/reference/proj/src (see oracle/Makefile, target `ref`), into oracle/_ref/. Nothing
+// from the reference is copied into this repository.
+//
+// Used (a) to validate the restatement oracle/moe_oracle.cpp bit-for-bit, (b) to generate the
+// golden vectors in tests/golden/, and (c) as the "reference" CPU arm of bench.py.
+
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "compasslab/common.hpp"
+#include "compasslab/gradcheck.hpp"
+#include "compasslab/tensor.hpp"
+
+using compasslab::Tape;
+using compasslab::Tensor;
+namespace ops = compasslab::ops;
+
+namespace {
+thread_local std::string g_err;
+
+std::vector<float> vec(const float* p, std::int64_t n) { return std::vector<float>(p, p + n); }
+
+template <typename Fn>
+int guarded(Fn fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const compasslab::ConfigError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// route_tokens from ops::matmul, ops::softmax_rows, ops::top_k, ops::col_sums.
+int ref_route(const float* x, const float* wr, std::int64_t T, std::int64_t d, std::int64_t N,
+              std::int64_t K, float* logits, float* probs, std::int64_t* idx, float* w,
+              std::int64_t* counts, float* agg_prob) {
+  return guarded([&] {
+    Tensor xt = Tensor::from_values({T, d}, vec(x, T * d));
+    Tensor wt = Tensor::from_values({d, N}, vec(wr, d * N));
+    Tensor z = ops::matmul(xt, wt);
+    Tensor p = ops::softmax_rows(z);
+    std::memcpy(logits, z.values().data(), sizeof(float) * T * N);
+    std::memcpy(probs, p.values().data(), sizeof(float) * T * N);
+    std::vector<float> val(static_cast<std::size_t>(K));
+    for (std::int64_t i = 0; i < N; ++i) counts[i] = 0;
+    for (std::int64_t j = 0; j < T; ++j) {
+      ops::top_k(p.values().data() + j * N, N, K, idx + j * K, val.data());
+      double s = 0.0;
+      for (std::int64_t k = 0; k < K; ++k) s += static_cast<double>(val[static_cast<std::size_t>(k)]);
+      for (std::int64_t k = 0; k < K; ++k) {
+        w[j * K + k] = static_cast<float>(static_cast<double>(val[static_cast<std::size_t>(k)]) / s);
+        counts[idx[j * K + k]] += 1;
+      }
+    }
+    Tensor cs = ops::col_sums(p);
+    std::memcpy(agg_prob, cs.values().data(), sizeof(float) * N);
+  });
+}
+
+int ref_aux_loss(const float* probs, const std::int64_t* counts, std::int64_t B, std::int64_t N,
+                 std::int64_t K, float* out) {
+  return guarded([&] {
+    Tensor p = Tensor::from_values({B, N}, vec(probs, B * N));
+    std::vector<std::int64_t> c(counts, counts + N);
+    *out = ops::moe_aux_loss(p, c, K).scalar();
+  });
+}
+
+int ref_z_loss(const float* logits, std::int64_t B, std::int64_t N, float* out) {
+  return guarded([&] { *out = ops::z_loss(Tensor::from_values({B, N}, vec(logits, B * N))).scalar(); });
+}
+
+int ref_top_k(const float* x, std::int64_t n, std::int64_t k, std::int64_t* idx, float* val) {
+  return guarded([&] { ops::top_k(x, n, k, idx, val); });
+}
+
+// moe_forward: per expert gather_rows -> matmul -> slice_cols x2 -> silu -> mul
+// -> matmul -> mul_rowwise -> scatter_add_rows; experts fanned out with the reference's own
+// parallel_for (common.cpp:141-168); outputs summed with ops::add in expert order.
+int ref_moe_forward(const float* x, std::int64_t T, std::int64_t d, std::int64_t N, std::int64_t K,
+                    std::int64_t f, const float* w_in, const float* w_out, const std::int64_t* idx,
+                    const float* w, float* out, int jobs) {
+  return guarded([&] {
+    Tensor xt = Tensor::from_values({T, d}, vec(x, T * d));
+    std::vector<std::vector<std::int64_t>> rows(static_cast<std::size_t>(N));
+    std::vector<std::vector<float>> wcol(static_cast<std::size_t>(N));
+    for (std::int64_t j = 0; j < T; ++j)
+      for (std::int64_t k = 0; k < K; ++k) {
+        rows[static_cast<std::size_t>(idx[j * K + k])].push_back(j);
+        wcol[static_cast<std::size_t>(idx[j * K + k])].push_back(w[j * K + k]);
+      }
+    std::vector<Tensor> contrib(static_cast<std::size_t>(N));
+    compasslab::parallel_for(static_cast<std::size_t>(N), jobs, [&](std::size_t e) {
+      if (rows[e].empty()) return;
+      const auto m = static_cast<std::int64_t>(rows[e].size());
+      Tensor win = Tensor::from_values({d, 2 * f}, vec(w_in + static_cast<std::int64_t>(e) * d * 2 * f, d * 2 * f));
+      Tensor wout = Tensor::from_values({f, d}, vec(w_out + static_cast<std::int64_t>(e) * f * d, f * d));
+      Tensor xe = ops::gather_rows(xt, rows[e]);
+      Tensor h = ops::matmul(xe, win);
+      Tensor a = ops::mul(ops::silu(ops::slice_cols(h, 0, f)), ops::slice_cols(h, f, 2 * f));
+      Tensor y = ops::matmul(a, wout);
+      Tensor yw = ops::mul_rowwise(y, Tensor::from_values({m, 1}, wcol[e]));
+      contrib[e] = ops::scatter_add_rows(T, yw, rows[e]);
+    });
+    Tensor acc = Tensor::zeros({T, d});
+    for (std::int64_t e = 0; e < N; ++e)
+      if (contrib[static_cast<std::size_t>(e)].defined()) acc = ops::add(acc, contrib[static_cast<std::size_t>(e)]);
+    std::memcpy(out, acc.values().data(), sizeof(float) * T * d);
+  });
+}
+
+// Expert-FFN backward through the reference Tape (tensor.cpp:133-150): loss = sum(Y * stop(dY))
+// seeds dL/dY = dY exactly; the Tape then replays matmul/mul/silu/slice_cols backward closures.
+int ref_expert_ffn_backward(const float* xe, std::int64_t m, std::int64_t d, std::int64_t f,
+                            const float* w_in, const float* w_out, const float* dy, float* dx,
+                            float* dw_in, float* dw_out) {
+  return guarded([&] {
+    Tensor x = Tensor::param({m, d}, vec(xe, m * d));
+    Tensor win = Tensor::param({d, 2 * f}, vec(w_in, d * 2 * f));
+    Tensor wout = Tensor::param({f, d}, vec(w_out, f * d));
+    Tensor g = Tensor::from_values({m, d}, vec(dy, m * d));
+    Tape tape;
+    Tape::Scope scope(tape);
+    Tensor h = ops::matmul(x, win);
+    Tensor a = ops::mul(ops::silu(ops::slice_cols(h, 0, f)), ops::slice_cols(h, f, 2 * f));
+    Tensor y = ops::matmul(a, wout);
+    Tensor loss = ops::sum_all(ops::mul(y, ops::stop_grad(g)));
+    tape.backward(loss);
+    std::memcpy(dx, x.grad().data(), sizeof(float) * m * d);
+    std::memcpy(dw_in, win.grad().data(), sizeof(float) * d * 2 * f);
+    std::memcpy(dw_out, wout.grad().data(), sizeof(float) * f * d);
+  });
+}
+
+// The reference's own finite-difference gradient suite (gradcheck.cpp:610-656); returns the
+// number of failing ops (0 = all pass) and the number of ops checked in *n_ops.
+int ref_gradcheck(std::uint64_t seed, int cases, double tol, int* n_ops) {
+  const auto res = compasslab::run_gradcheck(seed, cases, tol);
+  int fails = 0;
+  for (const auto& r : res) fails += r.pass ? 0 : 1;
+  *n_ops = static_cast<int>(res.size());
+  return fails;
+}
+
+}  // extern "C"

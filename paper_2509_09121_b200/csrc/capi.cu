@@ -1,0 +1,680 @@
+// Host orchestration of the MoE layer behind the C ABI of include/compass_moe.h.
+//
+// Error convention follows the reference C API (proj/src/capi.cpp:44-68): configuration errors
+// -> CL_ERR_CONFIG, anything else (CUDA error, non-finite output, invalid runtime input)
+// -> CL_ERR_RUN, message kept on the handle. No CPU fallback exists: without a usable sm_100
+// device every entry point fails with CL_ERR_RUN.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "compass_moe.h"
+#include "grouped_gemm.cuh"
+#include "moe_kernels.cuh"
+#include "synth_pack.cuh"
+
+using namespace cmoe;
+
+namespace {
+
+struct ConfigErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RunErr : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+std::string fmt(const char* f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof(buf), f, ap);
+  va_end(ap);
+  return buf;
+}
+
+#define CK(x)                                                                                \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) throw RunErr(fmt("%s failed: %s", #x, cudaGetErrorString(e_)));  \
+  } while (0)
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !p) throw RunErr("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2D row-major tensor [rows][inner] with a 128-byte-swizzled box of [box_rows][128 bytes].
+CUtensorMap make_map(const void* base, bool fp8, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+  CUtensorMap m;
+  const uint32_t esz = fp8 ? 1 : 2;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * esz};
+  cuuint32_t box[2] = {128u / esz, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                           const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw RunErr(fmt("cuTensorMapEncodeTiled failed (%d)", (int)r));
+  return m;
+}
+
+template <typename T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  return static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
+}
+
+}  // namespace
+
+struct cl_moe {
+  cl_moe_config cfg{};
+  int64_t d = 0, N = 0, K = 0, f = 0, cap = 0;
+  int n_local = 0, e0 = 0;
+  int gemm_ctas = 2;
+  int num_sms = 148;
+  int precision = CL_MOE_BF16;
+  std::string last_error;
+
+  // weights
+  float* wr = nullptr;                 // [d][N] fp32
+  __nv_bfloat16* win = nullptr;        // [n_local][2f][d] packed
+  __nv_bfloat16* wout = nullptr;       // [n_local][d][f] packed
+  uint8_t* win8 = nullptr;             // e4m3 copies
+  uint8_t* wout8 = nullptr;
+  float* ws_in = nullptr;              // [n_local][2f]
+  float* ws_out = nullptr;             // [n_local][d]
+  float* sx_in = nullptr;              // [n_local]
+  float* sx_mid = nullptr;             // [n_local]
+  float* calib = nullptr;              // [2][n_local] running maxima
+  bool fp8_ready = false;
+
+  // workspaces
+  RouteBufs rb{};
+  int n_tiles_cap = 0;
+  void* xperm = nullptr;               // [cap*K][d] (bf16 or e4m3)
+  void* act = nullptr;                 // [cap*K][f]
+  __nv_bfloat16* y = nullptr;          // [cap*K][d]
+  int32_t* perm = nullptr;
+  int32_t* inv = nullptr;
+  float* row_w = nullptr;
+  void* io_in = nullptr;               // staging for the host-buffer entry point
+  void* io_out = nullptr;
+  float* io_f32 = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int64_t last_rows = 0;
+
+  CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
+  CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
+  bool maps_q = false;
+
+  ~cl_moe() {
+    void* ptrs[] = {wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
+                    sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
+                    inv,    row_w,   io_in,   io_out,    io_f32,       rb.logits,    rb.probs,
+                    rb.topk_idx, rb.combine_w, rb.local_rank, rb.tile_cnt, rb.tile_psum, rb.tile_lse2,
+                    rb.counts, rb.offsets, rb.agg_prob, rb.losses, rb.finite_flag};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace {
+
+template <typename Fn>
+cl_status guarded(cl_moe* h, Fn fn) {
+  if (!h) return CL_ERR_CONFIG;
+  try {
+    h->last_error.clear();
+    fn();
+    return CL_OK;
+  } catch (const ConfigErr& e) {
+    h->last_error = e.what();
+    return CL_ERR_CONFIG;
+  } catch (const std::exception& e) {
+    h->last_error = e.what();
+    return CL_ERR_RUN;
+  }
+}
+
+void validate(const cl_moe_config* c) {
+  if (!c) throw ConfigErr("config is null");
+  if (c->d_model <= 0 || c->d_model % 256) throw ConfigErr(fmt("d_model=%lld must be a positive multiple of 256", (long long)c->d_model));
+  if (c->d_ff <= 0 || c->d_ff % 128) throw ConfigErr(fmt("d_ff=%lld must be a positive multiple of 128", (long long)c->d_ff));
+  if (c->n_experts < 1 || c->n_experts > 128) throw ConfigErr(fmt("n_experts=%lld outside [1, 128]", (long long)c->n_experts));
+  if (c->top_k < 1 || c->top_k > c->n_experts || c->top_k > 8)
+    throw ConfigErr(fmt("top_k=%lld outside [1, min(N, 8)]", (long long)c->top_k));
+  if (c->max_tokens < 1 || c->max_tokens * c->top_k > (int64_t(1) << 30)) throw ConfigErr("max_tokens out of range");
+  const int ep = c->ep_size <= 0 ? 1 : c->ep_size;
+  if (c->n_experts % ep) throw ConfigErr("n_experts must be divisible by ep_size");
+  if (c->ep_rank < 0 || c->ep_rank >= ep) throw ConfigErr("ep_rank out of range");
+  if (c->gemm_ctas < 0 || c->gemm_ctas > 2) throw ConfigErr("gemm_ctas must be 0, 1 or 2");
+}
+
+void build_maps(cl_moe* h, bool fp8) {
+  const uint64_t rows = static_cast<uint64_t>(h->cap * h->K);
+  for (int v = 0; v < 2; ++v) {
+    const uint32_t brow = v == 0 ? 256 : 128;
+    if (!fp8) {
+      h->mA1[v] = make_map(h->xperm, false, h->d, rows, 128);
+      h->mB1[v] = make_map(h->win, false, h->d, (uint64_t)h->n_local * 2 * h->f, brow);
+      h->mA2[v] = make_map(h->act, false, h->f, rows, 128);
+      h->mB2[v] = make_map(h->wout, false, h->f, (uint64_t)h->n_local * h->d, brow);
+    } else {
+      h->mA1q[v] = make_map(h->xperm, true, h->d, rows, 128);
+      h->mB1q[v] = make_map(h->win8, true, h->d, (uint64_t)h->n_local * 2 * h->f, brow);
+      h->mA2q[v] = make_map(h->act, true, h->f, rows, 128);
+      h->mB2q[v] = make_map(h->wout8, true, h->f, (uint64_t)h->n_local * h->d, brow);
+    }
+  }
+}
+
+void init_handle(cl_moe* h, const cl_moe_config* c) {
+  validate(c);
+  h->cfg = *c;
+  h->d = c->d_model;
+  h->N = c->n_experts;
+  h->K = c->top_k;
+  h->f = c->d_ff;
+  h->cap = c->max_tokens;
+  const int ep = c->ep_size <= 0 ? 1 : c->ep_size;
+  h->n_local = static_cast<int>(h->N / ep);
+  h->e0 = c->ep_rank * h->n_local;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RunErr("no CUDA device available (the MoE path has no CPU fallback)");
+  CK(cudaSetDevice(c->device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, c->device));
+  if (prop.major != 10) throw RunErr(fmt("device %d is sm_%d%d; this library is built for sm_100a only", c->device, prop.major, prop.minor));
+  h->num_sms = prop.multiProcessorCount;
+  h->gemm_ctas = c->gemm_ctas == 0 ? 2 : c->gemm_ctas;
+  CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+
+  const int64_t rows = h->cap * h->K;
+  const int tpc = router_tokens_per_cta(static_cast<int>(h->N));
+  h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
+  RouteBufs& rb = h->rb;
+  rb.logits = dalloc<float>(h->cap * h->N);
+  rb.probs = dalloc<float>(h->cap * h->N);
+  rb.topk_idx = dalloc<int32_t>(rows);
+  rb.combine_w = dalloc<float>(rows);
+  rb.local_rank = dalloc<int32_t>(rows);
+  rb.tile_cnt = dalloc<int32_t>((size_t)h->n_tiles_cap * h->N);
+  rb.tile_psum = dalloc<double>((size_t)h->n_tiles_cap * h->N);
+  rb.tile_lse2 = dalloc<double>(h->n_tiles_cap);
+  rb.counts = dalloc<int32_t>(h->N);
+  rb.offsets = dalloc<int32_t>(h->N + 1);
+  rb.agg_prob = dalloc<float>(h->N);
+  rb.losses = dalloc<float>(2);
+  rb.finite_flag = dalloc<int32_t>(1);
+  CK(cudaMemset(rb.finite_flag, 0, sizeof(int32_t)));
+  CK(cudaMemset(rb.offsets, 0, sizeof(int32_t) * (h->N + 1)));
+
+  h->xperm = dalloc<__nv_bfloat16>(rows * h->d);
+  h->act = dalloc<__nv_bfloat16>(rows * h->f);
+  h->y = dalloc<__nv_bfloat16>(rows * h->d);
+  h->perm = dalloc<int32_t>(rows);
+  h->inv = dalloc<int32_t>(rows);
+  h->row_w = dalloc<float>(rows);
+
+  h->wr = dalloc<float>(h->d * h->N);
+  h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
+  h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
+  h->sx_in = dalloc<float>(h->n_local);
+  h->sx_mid = dalloc<float>(h->n_local);
+  h->calib = dalloc<float>(2 * h->n_local);
+  CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
+
+  using namespace cmoe;
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+}
+
+template <int G, int EPI, bool F8, bool OF8>
+void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((h->num_sms / G) * G);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = GemmCfg<G>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8>, a, b, args));
+}
+
+// route_tokens on device: K1 + K2.
+void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
+  if (T < 1) throw RunErr("route_tokens: B must be >= 1");
+  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
+  const int N = static_cast<int>(h->N);
+  const int tpc = router_tokens_per_cta(N);
+  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
+  const int N4 = (N + 3) / 4 * 4;
+  const size_t smem = sizeof(float) * (tpc * (kRouterChunk + 1) + kRouterChunk * N4 + tpc * N4);
+  router_kernel<<<n_tiles, kRouterThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), h->wr, (int)T,
+                                                       (int)h->d, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+}
+
+void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T, cudaStream_t st) {
+  if (T < 1) throw RunErr("moe_forward: B must be >= 1");
+  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
+  const int N = static_cast<int>(h->N);
+  const int tpc = router_tokens_per_cta(N);
+  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
+  CK(cudaMemcpyAsync(h->rb.topk_idx, idx, sizeof(int32_t) * T * h->K, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h->rb.combine_w, w, sizeof(float) * T * h->K, cudaMemcpyDeviceToDevice, st));
+  decision_tiles_kernel<<<n_tiles, 128, 0, st>>>(h->rb.topk_idx, (int)T, N, (int)h->K, tpc, h->rb);
+  CK(cudaGetLastError());
+  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+}
+
+// dispatch + expert FFN + combine (local experts; ep_size == 1).
+void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  if (h->cfg.ep_size > 1) throw ConfigErr("expert-parallel forward goes through the EP entry points");
+  const int N = static_cast<int>(h->N);
+  const int tpc = router_tokens_per_cta(N);
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  const int blocks = static_cast<int>((T + 7) / 8);
+  if (fp8)
+    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
+                                                  h->inv, h->row_w, h->sx_in);
+  else
+    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
+                                                   h->perm, h->inv, h->row_w, nullptr);
+  CK(cudaGetLastError());
+
+  GemmArgs g1{};
+  g1.offsets = h->rb.offsets;
+  g1.n_experts = h->n_local;
+  g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
+  g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
+  g1.b_rows_per_expert = static_cast<int>(2 * h->f);
+  g1.out = h->act;
+  g1.ldo = static_cast<int>(h->f);
+  g1.act_scale = h->sx_in;
+  g1.w_scale = h->ws_in;
+  g1.out_scale = h->sx_mid;
+  GemmArgs g2{};
+  g2.offsets = h->rb.offsets;
+  g2.n_experts = h->n_local;
+  g2.n_tiles_n = static_cast<int>(h->d / kBN);
+  g2.num_kb = static_cast<int>(h->f * (fp8 ? 1 : 2) / kBKBytes);
+  g2.b_rows_per_expert = static_cast<int>(h->d);
+  g2.out = h->y;
+  g2.ldo = static_cast<int>(h->d);
+  g2.row_scale = h->row_w;
+  g2.act_scale = h->sx_mid;
+  g2.w_scale = h->ws_out;
+  const int v = h->gemm_ctas == 2 ? 1 : 0;
+  if (!fp8) {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
+      launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
+      launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
+    }
+  } else {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
+      launch_gemm<2, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
+      launch_gemm<1, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
+    }
+  }
+  if (out_f32)
+    combine_kernel<float><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out),
+                                                  h->rb.finite_flag);
+  else
+    combine_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K,
+                                                          static_cast<__nv_bfloat16*>(out), h->rb.finite_flag);
+  CK(cudaGetLastError());
+  h->last_rows = T * h->K;
+}
+
+void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_t st) {
+  if (!o) return;
+  const int64_t N = h->N, K = h->K;
+  if (o->logits) CK(cudaMemcpyAsync(o->logits, h->rb.logits, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
+  if (o->probs) CK(cudaMemcpyAsync(o->probs, h->rb.probs, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
+  if (o->topk_idx) CK(cudaMemcpyAsync(o->topk_idx, h->rb.topk_idx, sizeof(int32_t) * T * K, cudaMemcpyDeviceToDevice, st));
+  if (o->combine_weights)
+    CK(cudaMemcpyAsync(o->combine_weights, h->rb.combine_w, sizeof(float) * T * K, cudaMemcpyDeviceToDevice, st));
+  if (o->counts) {
+    i32_to_i64_kernel<<<(int)((N + 127) / 128), 128, 0, st>>>(h->rb.counts, (int)N, o->counts);
+    CK(cudaGetLastError());
+  }
+  if (o->agg_prob) CK(cudaMemcpyAsync(o->agg_prob, h->rb.agg_prob, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+  if (o->aux_loss) CK(cudaMemcpyAsync(o->aux_loss, h->rb.losses, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (o->z_loss) CK(cudaMemcpyAsync(o->z_loss, h->rb.losses + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
+}
+
+void ensure_fp8_storage(cl_moe* h) {
+  if (h->win8) return;
+  h->win8 = dalloc<uint8_t>((size_t)h->n_local * 2 * h->f * h->d);
+  h->wout8 = dalloc<uint8_t>((size_t)h->n_local * h->d * h->f);
+  h->ws_in = dalloc<float>((size_t)h->n_local * 2 * h->f);
+  h->ws_out = dalloc<float>((size_t)h->n_local * h->d);
+  build_maps(h, true);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cl_moe_version(void) { return "0.1.0-sm100a"; }
+
+const char* cl_moe_last_error(const cl_moe* h) { return h == nullptr ? "" : h->last_error.c_str(); }
+
+static cl_status create_common(const cl_moe_config* cfg, cl_moe** out, const float* w_router, const float* w_in,
+                               const float* w_out, bool synthetic, uint64_t seed) {
+  if (out == nullptr) return CL_ERR_CONFIG;
+  *out = nullptr;
+  cl_moe* h = new cl_moe();
+  const cl_status st = guarded(h, [&] {
+    init_handle(h, cfg);
+    const int64_t d = h->d, f = h->f, N = h->N;
+    const float sd = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+    const float sf = static_cast<float>(1.0 / std::sqrt(static_cast<double>(f)));
+    if (synthetic) {
+      synth_f32_kernel<<<grid_for(d * N), 256>>>(split_seed(seed, 2), d * N, sd, h->wr);
+      for (int el = 0; el < h->n_local; ++el) {
+        const int e = h->e0 + el;
+        synth_pack_win_kernel<<<grid_for(2 * f * d), 256>>>(split_seed(seed, 16 + e), (int)d, (int)f, sd,
+                                                            h->win + (size_t)el * 2 * f * d);
+        synth_pack_wout_kernel<<<grid_for(d * f), 256>>>(split_seed(seed, 16 + N + e), (int)d, (int)f, sf,
+                                                         h->wout + (size_t)el * d * f);
+      }
+      CK(cudaGetLastError());
+    } else {
+      if (!w_router || !w_in || !w_out) throw ConfigErr("weights are null");
+      CK(cudaMemcpy(h->wr, w_router, sizeof(float) * d * N, cudaMemcpyHostToDevice));
+      float* tmp = dalloc<float>(2 * f * d);
+      for (int el = 0; el < h->n_local; ++el) {
+        CK(cudaMemcpy(tmp, w_in + (size_t)el * d * 2 * f, sizeof(float) * d * 2 * f, cudaMemcpyHostToDevice));
+        pack_transpose_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)((d + 31) / 32)), dim3(32, 8)>>>(
+            tmp, (int)d, (int)(2 * f), (int)f, h->win + (size_t)el * 2 * f * d);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(tmp, w_out + (size_t)el * f * d, sizeof(float) * f * d, cudaMemcpyHostToDevice));
+        pack_transpose_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)((f + 31) / 32)), dim3(32, 8)>>>(
+            tmp, (int)f, (int)d, (int)f, h->wout + (size_t)el * d * f);
+        CK(cudaGetLastError());
+      }
+      CK(cudaDeviceSynchronize());
+      cudaFree(tmp);
+    }
+    CK(cudaDeviceSynchronize());
+    build_maps(h, false);
+  });
+  if (st != CL_OK) {
+    std::fprintf(stderr, "cl_moe_create: %s\n", h->last_error.c_str());
+    delete h;
+    return st;
+  }
+  *out = h;
+  return CL_OK;
+}
+
+cl_status cl_moe_create(const cl_moe_config* cfg, const float* w_router, const float* w_in, const float* w_out,
+                        cl_moe** out) {
+  return create_common(cfg, out, w_router, w_in, w_out, false, 0);
+}
+
+cl_status cl_moe_create_synthetic(const cl_moe_config* cfg, uint64_t seed, cl_moe** out) {
+  return create_common(cfg, out, nullptr, nullptr, nullptr, true, seed);
+}
+
+void cl_moe_destroy(cl_moe* h) {
+  if (h) {
+    cudaSetDevice(h->cfg.device);
+    cudaDeviceSynchronize();
+  }
+  delete h;
+}
+
+cl_status cl_moe_synthetic_tokens(cl_moe* h, uint64_t seed, int64_t T, void* x, void* stream) {
+  return guarded(h, [&] {
+    if (!x || T < 1) throw ConfigErr("bad arguments");
+    CK(cudaSetDevice(h->cfg.device));
+    synth_bf16_kernel<<<grid_for(T * h->d), 256, 0, (cudaStream_t)stream>>>(split_seed(seed, 1), T * h->d, 1.0f,
+                                                                             static_cast<__nv_bfloat16*>(x));
+    CK(cudaGetLastError());
+  });
+}
+
+cl_status cl_moe_route_tokens(cl_moe* h, const void* hidden, int64_t T, const cl_moe_decision* out, void* stream) {
+  return guarded(h, [&] {
+    if (!hidden) throw ConfigErr("hidden is null");
+    CK(cudaSetDevice(h->cfg.device));
+    run_router(h, hidden, T, (cudaStream_t)stream);
+    export_decision(h, T, out, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int32_t* topk_idx,
+                             const float* combine_weights, void* out, void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !topk_idx || !combine_weights || !out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    plan_from_decision(h, topk_idx, combine_weights, T, (cudaStream_t)stream);
+    run_experts(h, hidden, T, out, false, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
+                         void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    run_router(h, hidden, T, (cudaStream_t)stream);
+    run_experts(h, hidden, T, out, false, (cudaStream_t)stream);
+    export_decision(h, T, decision, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_forward_host(cl_moe* h, const void* hidden_host, int64_t T, void* out_host, int32_t io_dtype) {
+  return guarded(h, [&] {
+    if (!hidden_host || !out_host) throw ConfigErr("null argument");
+    if (io_dtype != CL_MOE_IO_BF16 && io_dtype != CL_MOE_IO_F32) throw ConfigErr("io_dtype must be BF16 or F32");
+    if (T < 1) throw RunErr("moe_forward: B must be >= 1");
+    if (T > h->cap) throw ConfigErr("T exceeds max_tokens");
+    CK(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = h->own_stream;
+    if (!h->io_in) {
+      h->io_in = dalloc<__nv_bfloat16>(h->cap * h->d);
+      h->io_f32 = dalloc<float>(h->cap * h->d);
+    }
+    const int64_t n = T * h->d;
+    if (io_dtype == CL_MOE_IO_BF16) {
+      CK(cudaMemcpyAsync(h->io_in, hidden_host, n * 2, cudaMemcpyHostToDevice, st));
+    } else {
+      CK(cudaMemcpyAsync(h->io_f32, hidden_host, n * 4, cudaMemcpyHostToDevice, st));
+      f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(h->io_f32, n, static_cast<__nv_bfloat16*>(h->io_in));
+      CK(cudaGetLastError());
+    }
+    run_router(h, h->io_in, T, st);
+    const bool f32 = io_dtype == CL_MOE_IO_F32;
+    // fp32 output reuses the fp32 input staging buffer (already converted to bf16 above)
+    void* dout = h->io_f32;
+    if (!f32) {
+      if (!h->io_out) h->io_out = dalloc<__nv_bfloat16>(h->cap * h->d);
+      dout = h->io_out;
+    }
+    run_experts(h, h->io_in, T, dout, f32, st);
+    CK(cudaMemcpyAsync(out_host, dout, n * (f32 ? 4 : 2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int flag = 0;
+    CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
+      throw RunErr("non-finite value produced by op 'moe_forward'");
+    }
+  });
+}
+
+cl_status cl_moe_sync(cl_moe* h, void* stream) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    int flag = 0;
+    CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    if (flag) {
+      CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
+      throw RunErr("non-finite value produced by op 'moe_forward'");
+    }
+  });
+}
+
+cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* v) {
+  return guarded(h, [&] {
+    if (!v) throw ConfigErr("view is null");
+    v->offsets = h->rb.offsets;
+    v->perm = h->perm;
+    v->inv = h->inv;
+    v->row_weight = h->row_w;
+    v->x_perm = h->xperm;
+    v->act = h->act;
+    v->y = h->y;
+    v->rows = h->last_rows;
+  });
+}
+
+cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, void* stream) {
+  return guarded(h, [&] {
+    const void* src = nullptr;
+    switch (which) {
+      case 0: src = h->rb.offsets; break;
+      case 1: src = h->perm; break;
+      case 2: src = h->inv; break;
+      case 3: src = h->row_w; break;
+      case 4: src = h->xperm; break;
+      case 5: src = h->act; break;
+      case 6: src = h->y; break;
+      default: throw ConfigErr("unknown stage buffer");
+    }
+    if (!dst || bytes < 0) throw ConfigErr("bad destination");
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  });
+}
+
+cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream) {
+  return guarded(h, [&] {
+    if (!hidden) throw ConfigErr("hidden is null");
+    CK(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (reset) CK(cudaMemsetAsync(h->calib, 0, sizeof(float) * 2 * h->n_local, st));
+    const int saved = h->precision;
+    h->precision = CL_MOE_BF16;
+    run_router(h, hidden, T, st);
+    if (!h->io_out) h->io_out = dalloc<__nv_bfloat16>(h->cap * h->d);
+    run_experts(h, hidden, T, h->io_out, false, st);
+    h->precision = saved;
+    const int64_t rows = T * h->K;
+    segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)h->d,
+                                                                 h->rb.offsets, h->n_local, h->calib);
+    segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)h->f,
+                                                                 h->rb.offsets, h->n_local, h->calib + h->n_local);
+    CK(cudaGetLastError());
+  });
+}
+
+cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float* act_scale_mid) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    ensure_fp8_storage(h);
+    std::vector<float> sin(h->n_local), smid(h->n_local);
+    if (act_scale_in && act_scale_mid) {
+      std::copy(act_scale_in, act_scale_in + h->n_local, sin.begin());
+      std::copy(act_scale_mid, act_scale_mid + h->n_local, smid.begin());
+    } else {
+      std::vector<float> c(2 * h->n_local);
+      CK(cudaDeviceSynchronize());
+      CK(cudaMemcpy(c.data(), h->calib, sizeof(float) * 2 * h->n_local, cudaMemcpyDeviceToHost));
+      for (int e = 0; e < h->n_local; ++e) {
+        if (!(c[e] > 0.0f) || !(c[h->n_local + e] > 0.0f))
+          throw RunErr(fmt("quantize_model: missing calibration for expert %d", h->e0 + e));
+        sin[e] = c[e] / 448.0f;
+        smid[e] = c[h->n_local + e] / 448.0f;
+      }
+    }
+    for (int e = 0; e < h->n_local; ++e)
+      if (!(sin[e] > 0.0f) || !(smid[e] > 0.0f)) throw ConfigErr("activation scales must be > 0");
+    CK(cudaMemcpy(h->sx_in, sin.data(), sizeof(float) * h->n_local, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sx_mid, smid.data(), sizeof(float) * h->n_local, cudaMemcpyHostToDevice));
+    const int64_t r1 = (int64_t)h->n_local * 2 * h->f, r2 = (int64_t)h->n_local * h->d;
+    quantize_rows_e4m3_kernel<<<(int)((r1 + 7) / 8), 256>>>(h->win, r1, (int)h->d, h->win8, h->ws_in);
+    quantize_rows_e4m3_kernel<<<(int)((r2 + 7) / 8), 256>>>(h->wout, r2, (int)h->f, h->wout8, h->ws_out);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    h->fp8_ready = true;
+    h->precision = CL_MOE_FP8_E4M3;
+  });
+}
+
+cl_status cl_moe_set_precision(cl_moe* h, int32_t precision) {
+  return guarded(h, [&] {
+    if (precision != CL_MOE_BF16 && precision != CL_MOE_FP8_E4M3) throw ConfigErr("unknown precision");
+    if (precision == CL_MOE_FP8_E4M3 && !h->fp8_ready) throw ConfigErr("FP8 scheme not quantized yet");
+    h->precision = precision;
+  });
+}
+
+cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale, float* w_out_scale) {
+  return guarded(h, [&] {
+    if (!h->fp8_ready) throw ConfigErr("FP8 scheme not quantized yet");
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaDeviceSynchronize());
+    if (act_in) CK(cudaMemcpy(act_in, h->sx_in, sizeof(float) * h->n_local, cudaMemcpyDeviceToHost));
+    if (act_mid) CK(cudaMemcpy(act_mid, h->sx_mid, sizeof(float) * h->n_local, cudaMemcpyDeviceToHost));
+    if (w_in_scale) CK(cudaMemcpy(w_in_scale, h->ws_in, sizeof(float) * h->n_local * 2 * h->f, cudaMemcpyDeviceToHost));
+    if (w_out_scale) CK(cudaMemcpy(w_out_scale, h->ws_out, sizeof(float) * h->n_local * h->d, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,313 @@
+// Grouped (per-expert) GEMM on the 5th-generation tensor cores for the MoE expert FFN.
+//
+//   GEMM1 (EPI_SWIGLU):   A_act[r, :] = silu(X[r,:] W_gate[e]) * (X[r,:] W_up[e])      (bf16 or e4m3 out)
+//   GEMM2 (EPI_ROWSCALE): Y[r, :]     = w[r] * (A_act[r,:] W_out[e])                    (bf16 out)
+//
+// Rows r of the permuted activation matrix are grouped by expert (offsets[e] .. offsets[e+1]);
+// expert e multiplies against its own weight block. Replaces the per-expert ops::matmul +
+// slice_cols + silu + mul (+ mul_rowwise) chain of the reference composition
+// (proj/src/tensor.cpp:350-375, :398-420, :315-322, :283-303, :572-610).
+//
+// Design (sm_100a):
+//  * persistent kernel, one CTA (or CTA pair) per SM, static round-robin over output tiles in
+//    (expert, n-block, m-block) order so CTAs running together share the weight n-block in L2;
+//  * warp-specialised: warp 0 = TMA producer, warp 1 = tcgen05.mma issuer (one elected thread),
+//    warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM -> registers -> global);
+//  * operands staged by TMA into 128-byte-swizzled K-major tiles, kStages-deep mbarrier ring;
+//  * FP32 accumulators in TMEM, double-buffered (2 x 256 columns) so the epilogue of tile i
+//    overlaps the main loop of tile i+1;
+//  * kCtaGroup == 2: cta_group::2 MMA with M=256 over a CTA pair (each CTA stages 128 rows of A
+//    and half of the 256-wide B tile), halving per-SM operand traffic.
+#pragma once
+#include <cuda_fp8.h>
+
+#include "ptx.cuh"
+
+namespace cmoe {
+
+enum GemmEpi : int { EPI_SWIGLU = 0, EPI_ROWSCALE = 1 };
+
+struct GemmArgs {
+  const int32_t* offsets;   // [n_experts+1] first permuted row of each expert (device)
+  int32_t n_experts;        // experts on this rank
+  int32_t n_tiles_n;        // 256-wide n-blocks per expert
+  int32_t num_kb;           // 128-byte k-blocks
+  int32_t b_rows_per_expert;
+  void* out;                // output rows (bf16 or e4m3)
+  int32_t ldo;              // output row stride (elements)
+  const float* row_scale;   // EPI_ROWSCALE: per permuted row combine weight
+  const float* act_scale;   // FP8: per-expert activation scale of the A operand [n_experts]
+  const float* w_scale;     // FP8: per-(expert, B row) weight scale [n_experts][b_rows_per_expert]
+  const float* out_scale;   // FP8 EPI_SWIGLU: per-expert scale of the e4m3 output [n_experts]
+};
+
+constexpr int kGemmThreads = 256;
+constexpr int kBN = 256;                 // MMA N (output columns of one tile, pre-SwiGLU)
+constexpr int kBKBytes = 128;            // one swizzle atom along K
+constexpr int kMaxExperts = 256;
+
+template <int kCtaGroup>
+struct GemmCfg {
+  static constexpr int kRowsPerCta = 128;
+  static constexpr int kBM = 128 * kCtaGroup;
+  static constexpr int kBRowsPerCta = kBN / kCtaGroup;
+  static constexpr int kStageA = kRowsPerCta * kBKBytes;
+  static constexpr int kStageB = kBRowsPerCta * kBKBytes;
+  static constexpr int kStageBytes = kStageA + kStageB;
+  static constexpr int kStages = kCtaGroup == 1 ? 4 : 6;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
+                               (kMaxExperts + 1) * 4;
+};
+
+struct TileInfo {
+  int e, mt, nt, row0, row_end;
+};
+
+__device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, int n_experts, int n_tiles_n,
+                                            const int32_t* offsets, int bm, TileInfo& ti) {
+  if (tile >= mt_prefix[n_experts] * n_tiles_n) return false;
+  int e = 0;
+  while (tile >= mt_prefix[e + 1] * n_tiles_n) ++e;
+  const int local = tile - mt_prefix[e] * n_tiles_n;
+  const int mtiles = mt_prefix[e + 1] - mt_prefix[e];
+  ti.e = e;
+  ti.nt = local / mtiles;
+  ti.mt = local - ti.nt * mtiles;
+  ti.row0 = offsets[e] + ti.mt * bm;
+  ti.row_end = offsets[e + 1];
+  return true;
+}
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const GemmArgs args) {
+  using Cfg = GemmCfg<kCtaGroup>;
+  constexpr int S = Cfg::kStages;
+  constexpr int kUmmaKBytes = 32;                    // 16 bf16 or 32 e4m3 per MMA
+  constexpr int kMmaPerKb = kBKBytes / kUmmaKBytes;  // 4
+  constexpr uint32_t kIdesc = idesc_f32acc<kFp8>(Cfg::kBM, kBN);
+  constexpr int kElemBytes = kFp8 ? 1 : 2;
+  constexpr int kBKElems = kBKBytes / kElemBytes;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kStageA;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* mt_prefix = reinterpret_cast<int*>(smem + S * Cfg::kStageBytes + 256);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const uint32_t cta_rank = kCtaGroup == 1 ? 0 : cluster_ctarank();
+  const int cluster = kCtaGroup == 1 ? blockIdx.x : cluster_id_x();
+  const int nclusters = kCtaGroup == 1 ? gridDim.x : nclusters_x();
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    mt_prefix[0] = 0;
+    for (int e = 0; e < args.n_experts; ++e) {
+      const int cnt = args.offsets[e + 1] - args.offsets[e];
+      acc += (cnt + Cfg::kBM - 1) / Cfg::kBM;
+      mt_prefix[e + 1] = acc;
+    }
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4 * kCtaGroup);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, 512);
+  tc_fence_before();
+  if constexpr (kCtaGroup == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      TileInfo ti;
+      for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
+                                           Cfg::kBM, ti);
+           tile += nclusters) {
+        const int a_row = ti.row0 + cta_rank * Cfg::kRowsPerCta;
+        const int b_row = ti.e * args.b_rows_per_expert + ti.nt * kBN + cta_rank * Cfg::kBRowsPerCta;
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if constexpr (kCtaGroup == 1) {
+            mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+            tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kEvictNormal);
+            tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
+          } else {
+            if (cta_rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
+            tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kEvictNormal);
+            tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
+          }
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA) =====================
+    if ((kCtaGroup == 1 || cta_rank == 0) && elect_one()) {
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      TileInfo ti;
+      for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
+                                           Cfg::kBM, ti);
+           tile += nclusters) {
+        mbar_wait(&tempty[acc], aph ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kBN;
+        for (int kb = 0; kb < args.num_kb; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t adesc = sdesc_k_sw128(smem_u32(sA + s * Cfg::kStageA));
+          const uint64_t bdesc = sdesc_k_sw128(smem_u32(sB + s * Cfg::kStageB));
+#pragma unroll
+          for (int k = 0; k < kMmaPerKb; ++k) {
+            const uint64_t koff = static_cast<uint64_t>((k * kUmmaKBytes) >> 4);
+            mma_ss<kCtaGroup, kFp8>(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+          }
+          mma_commit<kCtaGroup>(&empty[s]);
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        mma_commit<kCtaGroup>(&tfull[acc]);
+        if (++acc == 2) { acc = 0; aph ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ===================== epilogue: TMEM -> registers -> global =====================
+    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row_in_cta = q * 32 + lane;
+    int acc = 0;
+    uint32_t aph = 0;
+    TileInfo ti;
+    for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
+                                         Cfg::kBM, ti);
+         tile += nclusters) {
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const int row = ti.row0 + cta_rank * Cfg::kRowsPerCta + row_in_cta;
+      const bool valid = row < ti.row_end;
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kBN;
+      if constexpr (kEpi == EPI_SWIGLU) {
+        float sg = 1.0f, su = 1.0f, so = 1.0f;
+        const float* wsg = nullptr;
+        const float* wsu = nullptr;
+        if constexpr (kFp8) {
+          const float sx = args.act_scale[ti.e];
+          sg = sx;
+          su = sx;
+          wsg = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
+          wsu = wsg + kBN / 2;
+        }
+        if constexpr (kOutFp8) so = 1.0f / args.out_scale[ti.e];
+#pragma unroll 1
+        for (int c = 0; c < kBN / 2 / 32; ++c) {
+          uint32_t g[32], u[32];
+          tmem_ld32(t_row + c * 32, g);
+          tmem_ld32(t_row + kBN / 2 + c * 32, u);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            float gv = __uint_as_float(g[i]) * sg;
+            float uv = __uint_as_float(u[i]) * su;
+            if constexpr (kFp8) {
+              gv *= wsg[c * 32 + i];
+              uv *= wsu[c * 32 + i];
+            }
+            v[i] = silu_f(gv) * uv;
+          }
+          if (valid) {
+            const int col = ti.nt * (kBN / 2) + c * 32;
+            if constexpr (kOutFp8) {
+              uint32_t p[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const __nv_fp8x2_storage_t lo =
+                    __nv_cvt_float2_to_fp8x2(make_float2(v[4 * i] * so, v[4 * i + 1] * so), __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                    make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
+                p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+              }
+              uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;
+              st_global_v4(dst, p[0], p[1], p[2], p[3]);
+              st_global_v4(dst + 16, p[4], p[5], p[6], p[7]);
+            } else {
+              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                             pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            }
+          }
+        }
+      } else {
+        float rs = valid ? args.row_scale[row] : 0.0f;
+        const float* ws = nullptr;
+        if constexpr (kFp8) {
+          rs *= args.act_scale[ti.e];
+          ws = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
+        }
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t a[32];
+          tmem_ld32(t_row + c * 32, a);
+          tmem_ld_wait();
+          if (valid) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              v[i] = __uint_as_float(a[i]) * rs;
+              if constexpr (kFp8) v[i] *= ws[c * 32 + i];
+            }
+            __nv_bfloat16* dst =
+                reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                           pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (kCtaGroup == 1) mbar_arrive(&tempty[acc]);
+        else mbar_arrive_cluster(&tempty[acc], 0);
+      }
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  if constexpr (kCtaGroup == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<kCtaGroup>(tmem_base, 512);
+}
+
+}  // namespace cmoe

@@ -1,0 +1,137 @@
+// Weight preparation kernels: device-side synthetic generation with the reference counter PRNG
+// (proj/include/compasslab/prng.hpp:15-70) and repacking of reference-layout fp32 weights into
+// the K-major bf16 / e4m3 operand layouts of the grouped GEMMs.
+//
+// Packed layouts (per expert e):
+//   W_in  [2f][d]  row p: block b = p/256, i = p%256; i < 128 -> gate column b*128+i,
+//                  else up column f + b*128 + (i-128). A 256-row n-block therefore holds the gate
+//                  and up columns of the same 128 FFN channels, so the SwiGLU runs in the GEMM1
+//                  epilogue straight from TMEM (no slice_cols copies, tensor.cpp:398-420).
+//   W_out [d][f]   transpose of the reference [f][d].
+#pragma once
+#include <cuda_fp8.h>
+
+#include "ptx.cuh"
+
+namespace cmoe {
+
+__host__ __device__ inline uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ull;
+__host__ __device__ inline uint64_t split_seed(uint64_t root, uint64_t stream) {
+  return mix64(root ^ mix64(stream * kGolden + 0x632be59bd9b4e019ull));
+}
+// Value i of Prng(seed).next_normal_f(0, stddev): Box-Muller over draws 2i+1, 2i+2.
+__device__ __forceinline__ float prng_normal_f(uint64_t seed, uint64_t i, float stddev) {
+  const uint64_t c = 2 * i;
+  const double u1 = 1.0 - static_cast<double>(mix64(seed + (c + 1) * kGolden) >> 11) * 0x1.0p-53;
+  const double u2 = static_cast<double>(mix64(seed + (c + 2) * kGolden) >> 11) * 0x1.0p-53;
+  const double z = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+  return 0.0f + stddev * static_cast<float>(z);
+}
+
+__device__ __forceinline__ int win_col_of_packed_row(int p, int f) {
+  const int b = p >> 8, i = p & 255;
+  return i < 128 ? b * 128 + i : f + b * 128 + (i - 128);
+}
+
+__global__ void synth_bf16_kernel(uint64_t seed, int64_t n, float stddev, __nv_bfloat16* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(prng_normal_f(seed, i, stddev));
+}
+__global__ void synth_f32_kernel(uint64_t seed, int64_t n, float stddev, float* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = prng_normal_f(seed, i, stddev);
+}
+// Packed W_in[e] element (p, l) is reference element (l, c(p)) = draw l*2f + c of stream seed.
+__global__ void synth_pack_win_kernel(uint64_t seed, int d, int f, float stddev, __nv_bfloat16* out) {
+  const int64_t n = (int64_t)2 * f * d;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = static_cast<int>(i / d), l = static_cast<int>(i % d);
+    const int c = win_col_of_packed_row(p, f);
+    out[i] = __float2bfloat16_rn(prng_normal_f(seed, (uint64_t)l * 2 * f + c, stddev));
+  }
+}
+// Packed W_out[e] element (n, l) is reference element (l, n) = draw l*d + n.
+__global__ void synth_pack_wout_kernel(uint64_t seed, int d, int f, float stddev, __nv_bfloat16* out) {
+  const int64_t total = (int64_t)d * f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int nrow = static_cast<int>(i / f), l = static_cast<int>(i % f);
+    out[i] = __float2bfloat16_rn(prng_normal_f(seed, (uint64_t)l * d + nrow, stddev));
+  }
+}
+
+// Transpose-and-convert of one expert's reference-layout fp32 matrix src[rows][cols] into
+// dst[cols'][rows] bf16, where dst row q takes source column map(q). 32x32 smem tiles.
+template <bool kWin>
+__global__ void pack_transpose_kernel(const float* __restrict__ src, int rows, int cols, int f,
+                                      __nv_bfloat16* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int q0 = blockIdx.x * 32;  // dst row block (source column space)
+  const int r0 = blockIdx.y * 32;  // source row block (= dst column)
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i;
+    const int q = q0 + threadIdx.x;
+    float v = 0.0f;
+    if (r < rows && q < cols) {
+      const int c = kWin ? win_col_of_packed_row(q, f) : q;
+      v = src[(size_t)r * cols + c];
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int q = q0 + i;
+    const int r = r0 + threadIdx.x;
+    if (q < cols && r < rows) dst[(size_t)q * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+  }
+}
+
+// Per-output-channel FP8 weight quantisation: scale = absmax/448 over the
+// packed row (a K-major row is one output channel), q = e4m3_satfinite(w / scale). One warp/row.
+__global__ void quantize_rows_e4m3_kernel(const __nv_bfloat16* __restrict__ w, int64_t rows, int kdim,
+                                          uint8_t* __restrict__ q, float* __restrict__ scale) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const __nv_bfloat16* src = w + r * kdim;
+  float m = 0.0f;
+  for (int i = lane; i < kdim; i += 32) m = fmaxf(m, fabsf(__bfloat162float(src[i])));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const float s = m > 0.0f ? m / 448.0f : 1.0f;
+  if (lane == 0) scale[r] = s;
+  uint8_t* dst = q + r * kdim;
+  for (int i = lane; i < kdim; i += 32)
+    dst[i] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__bfloat162float(src[i]) / s, __NV_SATFINITE, __NV_E4M3));
+}
+
+// Calibration (collect_calibration): per-expert max |value| over the rows of
+// each expert segment. Non-negative floats order like their bit patterns -> atomicMax on ints.
+__global__ void segment_absmax_kernel(const __nv_bfloat16* __restrict__ m, int cols, const int32_t* __restrict__ offsets,
+                                      int n_experts, float* __restrict__ out) {
+  const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= offsets[n_experts]) return;
+  int e = 0;
+  while (r >= offsets[e + 1]) ++e;
+  float mx = 0.0f;
+  const __nv_bfloat16* src = m + r * cols;
+  for (int i = lane; i < cols; i += 32) mx = fmaxf(mx, fabsf(__bfloat162float(src[i])));
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) atomicMax(reinterpret_cast<int*>(out) + e, __float_as_int(mx));
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, int64_t n, __nv_bfloat16* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+__global__ void i32_to_i64_kernel(const int32_t* __restrict__ in, int n, int64_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+
+}  // namespace cmoe

@@ -1,0 +1,235 @@
+"""Host-side mirror of the reference's MoE-layer operator interface.
+
+Same operation names, argument meaning and error behaviour as the SPEC ops, backed by the
+sm_100a kernels through the C ABI (include/compass_moe.h):
+
+* ``route_tokens(hidden) -> RouterDecision``
+* ``moe_forward(hidden, decision) -> Tensor[B x d]``
+* ``aux_loss(decision)`` / ``z_loss(decision)``        SPEC.md:165-182 (computed on device)
+* ``calibrate`` / ``quantize_fp8``                     SPEC.md:532-570 (expert-aware FP8)
+
+Device tensors are torch CUDA tensors (torch is used for device memory and streams only).
+Errors: ``MoEConfigError`` for CL_ERR_CONFIG, ``MoEError`` for CL_ERR_RUN (ValidationError).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import MoEConfigError, MoEError  # noqa: F401  (re-exported)
+
+
+@dataclass
+class MoEConfig:
+    d_model: int
+    n_experts: int
+    top_k: int
+    d_ff: int
+    max_tokens: int
+    device: int = 0
+    gemm_ctas: int = 0  # 0 auto (2-CTA), 1 or 2
+    ep_size: int = 1
+    ep_rank: int = 0
+
+    def to_c(self) -> _lib.Config:
+        return _lib.Config(self.d_model, self.n_experts, self.top_k, self.d_ff, self.max_tokens, self.device,
+                           self.gemm_ctas, self.ep_size, self.ep_rank)
+
+
+@dataclass
+class RouterDecision:
+    """logits z, probs, topk_idx, combine_weights, counts c, agg_prob p, B, K."""
+    logits: torch.Tensor
+    probs: torch.Tensor
+    topk_idx: torch.Tensor
+    combine_weights: torch.Tensor
+    counts: torch.Tensor
+    agg_prob: torch.Tensor
+    aux: torch.Tensor
+    z: torch.Tensor
+    B: int
+    K: int
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> C.c_void_p:
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class MoELayer:
+    """One MoE layer (router + N gated experts) resident on one B200."""
+
+    def __init__(self, cfg: MoEConfig, w_router=None, w_in=None, w_out=None, seed: int | None = None):
+        self.cfg = cfg
+        self.L = _lib.lib()
+        self.h = C.c_void_p()
+        self.device = torch.device("cuda", cfg.device)
+        c = cfg.to_c()
+        if seed is not None:
+            rc = self.L.cl_moe_create_synthetic(C.byref(c), seed, C.byref(self.h))
+        else:
+            wr = np.ascontiguousarray(w_router, np.float32)
+            wi = np.ascontiguousarray(w_in, np.float32)
+            wo = np.ascontiguousarray(w_out, np.float32)
+            rc = self.L.cl_moe_create(C.byref(c), wr.ctypes.data, wi.ctypes.data, wo.ctypes.data, C.byref(self.h))
+        if rc != _lib.CL_OK:
+            cls = MoEConfigError if rc == _lib.CL_ERR_CONFIG else MoEError
+            raise cls(f"cl_moe_create failed with status {rc}")
+
+    def close(self):
+        if self.h:
+            self.L.cl_moe_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc, what):
+        _lib.check(rc, self.h, what)
+
+    # ---------------------------------------------------------------- SPEC ops
+    def route_tokens(self, hidden: torch.Tensor) -> RouterDecision:
+        t = hidden.shape[0]
+        n, k = self.cfg.n_experts, self.cfg.top_k
+        dev = self.device
+        dec = RouterDecision(
+            logits=torch.empty(t, n, dtype=torch.float32, device=dev),
+            probs=torch.empty(t, n, dtype=torch.float32, device=dev),
+            topk_idx=torch.empty(t, k, dtype=torch.int32, device=dev),
+            combine_weights=torch.empty(t, k, dtype=torch.float32, device=dev),
+            counts=torch.empty(n, dtype=torch.int64, device=dev),
+            agg_prob=torch.empty(n, dtype=torch.float32, device=dev),
+            aux=torch.empty(1, dtype=torch.float32, device=dev),
+            z=torch.empty(1, dtype=torch.float32, device=dev), B=t, K=k)
+        cd = self._decision_struct(dec)
+        self._check(self.L.cl_moe_route_tokens(self.h, _ptr(self._bf16(hidden)), t, C.byref(cd), _stream(dev)),
+                    "route_tokens")
+        return dec
+
+    def moe_forward(self, hidden: torch.Tensor, decision: RouterDecision) -> torch.Tensor:
+        hidden = self._bf16(hidden)
+        out = torch.empty_like(hidden)
+        idx = decision.topk_idx.to(torch.int32).contiguous()
+        w = decision.combine_weights.to(torch.float32).contiguous()
+        self._check(self.L.cl_moe_moe_forward(self.h, _ptr(hidden), hidden.shape[0], _ptr(idx), _ptr(w), _ptr(out),
+                                              _stream(self.device)), "moe_forward")
+        return out
+
+    def forward(self, hidden: torch.Tensor, want_decision: bool = False):
+        """route_tokens + moe_forward fused on device. Returns out (and the decision)."""
+        hidden = self._bf16(hidden)
+        out = torch.empty_like(hidden)
+        dec = None
+        cd = None
+        if want_decision:
+            t, n, k, dev = hidden.shape[0], self.cfg.n_experts, self.cfg.top_k, self.device
+            dec = RouterDecision(
+                logits=torch.empty(t, n, dtype=torch.float32, device=dev),
+                probs=torch.empty(t, n, dtype=torch.float32, device=dev),
+                topk_idx=torch.empty(t, k, dtype=torch.int32, device=dev),
+                combine_weights=torch.empty(t, k, dtype=torch.float32, device=dev),
+                counts=torch.empty(n, dtype=torch.int64, device=dev),
+                agg_prob=torch.empty(n, dtype=torch.float32, device=dev),
+                aux=torch.empty(1, dtype=torch.float32, device=dev),
+                z=torch.empty(1, dtype=torch.float32, device=dev), B=t, K=k)
+            cd = C.byref(self._decision_struct(dec))
+        self._check(self.L.cl_moe_forward(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), cd, _stream(self.device)),
+                    "forward")
+        return (out, dec) if want_decision else out
+
+    def forward_host(self, x: np.ndarray, io_dtype: str = "bf16") -> np.ndarray:
+        """Reference-facing call on HOST buffers (H2D + layer + D2H, synchronous).
+
+        ``x`` is float32 [T x d] (io_dtype "f32") or a uint16 array of bf16 bits ("bf16")."""
+        t = x.shape[0]
+        if io_dtype == "f32":
+            x = np.ascontiguousarray(x, np.float32)
+            out = np.empty_like(x)
+            code = _lib.CL_MOE_IO_F32
+        else:
+            x = np.ascontiguousarray(x, np.uint16)
+            out = np.empty_like(x)
+            code = _lib.CL_MOE_IO_BF16
+        self._check(self.L.cl_moe_forward_host(self.h, x.ctypes.data, t, out.ctypes.data, code), "forward_host")
+        return out
+
+    def forward_host_ptr(self, x_ptr: int, t: int, out_ptr: int, io_dtype: int = _lib.CL_MOE_IO_BF16) -> None:
+        self._check(self.L.cl_moe_forward_host(self.h, C.c_void_p(x_ptr), t, C.c_void_p(out_ptr), io_dtype),
+                    "forward_host")
+
+    @staticmethod
+    def aux_loss(decision: RouterDecision) -> float:
+        return float(decision.aux.item())
+
+    @staticmethod
+    def z_loss(decision: RouterDecision) -> float:
+        return float(decision.z.item())
+
+    def sync(self):
+        self._check(self.L.cl_moe_sync(self.h, _stream(self.device)), "sync")
+
+    # ---------------------------------------------------------------- FP8 (SPEC expert-quantizer)
+    def calibrate(self, hidden: torch.Tensor, reset: bool = True):
+        self._check(self.L.cl_moe_calibrate(self.h, _ptr(self._bf16(hidden)), hidden.shape[0], int(reset),
+                                            _stream(self.device)), "calibrate")
+
+    def quantize_fp8(self, act_scale_in=None, act_scale_mid=None):
+        if act_scale_in is None:
+            rc = self.L.cl_moe_quantize_fp8(self.h, None, None)
+        else:
+            a = np.ascontiguousarray(act_scale_in, np.float32)
+            b = np.ascontiguousarray(act_scale_mid, np.float32)
+            rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
+        self._check(rc, "quantize_fp8")
+
+    def set_precision(self, precision: str):
+        code = _lib.CL_MOE_FP8_E4M3 if precision == "fp8" else _lib.CL_MOE_BF16
+        self._check(self.L.cl_moe_set_precision(self.h, code), "set_precision")
+
+    def fp8_scales(self):
+        nl = self.cfg.n_experts // self.cfg.ep_size
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        a = np.empty(nl, np.float32)
+        b = np.empty(nl, np.float32)
+        wi = np.empty((nl, 2 * f), np.float32)
+        wo = np.empty((nl, d), np.float32)
+        self._check(self.L.cl_moe_get_fp8_scales(self.h, a.ctypes.data, b.ctypes.data, wi.ctypes.data, wo.ctypes.data),
+                    "fp8_scales")
+        return a, b, wi, wo
+
+    # ---------------------------------------------------------------- stage access (tests)
+    def stage(self, name: str, shape, dtype) -> torch.Tensor:
+        out = torch.empty(shape, dtype=dtype, device=self.device)
+        nbytes = out.numel() * out.element_size()
+        self._check(self.L.cl_moe_copy_stage(self.h, _lib.STAGE[name], _ptr(out), nbytes, _stream(self.device)),
+                    "copy_stage")
+        return out
+
+    def synthetic_tokens(self, t: int, seed: int) -> torch.Tensor:
+        x = torch.empty(t, self.cfg.d_model, dtype=torch.bfloat16, device=self.device)
+        self._check(self.L.cl_moe_synthetic_tokens(self.h, seed, t, _ptr(x), _stream(self.device)), "synthetic_tokens")
+        return x
+
+    # ---------------------------------------------------------------- helpers
+    def _bf16(self, x: torch.Tensor) -> torch.Tensor:
+        if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous():
+            raise MoEConfigError("hidden must be a contiguous bf16 CUDA tensor [B x d]")
+        if x.shape[1] != self.cfg.d_model:
+            raise MoEConfigError(f"hidden has {x.shape[1]} columns, expected d_model={self.cfg.d_model}")
+        return x
+
+    @staticmethod
+    def _decision_struct(dec: RouterDecision) -> _lib.Decision:
+        return _lib.Decision(dec.logits.data_ptr(), dec.probs.data_ptr(), dec.topk_idx.data_ptr(),
+                             dec.combine_weights.data_ptr(), dec.counts.data_ptr(), dec.agg_prob.data_ptr(),
+                             dec.aux.data_ptr(), dec.z.data_ptr())

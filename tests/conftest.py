@@ -1,0 +1,27 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "slow: long-running CPU oracle case")
+
+
+@pytest.fixture(scope="session")
+def oracle_port():
+    from oracle.oracle import Oracle
+    return Oracle("port")
+
+
+@pytest.fixture(scope="session")
+def oracle_ref():
+    from oracle.oracle import Oracle, available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    return Oracle("reference")
