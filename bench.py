@@ -1,0 +1,319 @@
+#!/usr/bin/env python3
+"""Benchmark of the MoE-layer hot path (BASELINE.json metric) on B200.
+
+Default workload = BASELINE.json configs[1] ("C2"): one bf16 MoE layer, T=16384 tokens, d=4096,
+N=16 experts, top-2, SwiGLU FFN 14336, synthetic tokens and random-init weights drawn on the
+device with the reference counter PRNG (root seed 20261018).
+
+A step = one full layer forward (router -> plan -> dispatch -> GEMM1+SwiGLU -> GEMM2+weight ->
+combine) over one batch of T tokens, inputs resident in HBM (x = 134 MB and 5.6 GB of weights:
+every input is larger than the 126 MB L2, so no flush is needed between steps).
+
+Prints ONE JSON line (rank 0). ``--impl reference`` times the reference CPU implementation
+(oracle/_ref: the reference's own tensor.cpp compiled from /root/reference, composed per SPEC)
+on a bounded token sample of the same layer on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]
+    "c2": dict(workload="single-B200 MoE layer bf16 (BASELINE configs[1])", T=16384, d=4096, N=16, K=2, f=14336),
+    # BASELINE.json configs[0] shape on the GPU
+    "c1": dict(workload="small MoE layer (BASELINE configs[0] shape) bf16 on GPU", T=4096, d=1024, N=8, K=2, f=2816),
+    # BASELINE.json configs[3] decode-size batch at the C2 layer shape (bf16 path)
+    "c4": dict(workload="decode-size batch at the C2 layer shape (BASELINE configs[3])", T=256, d=4096, N=16, K=2,
+               f=14336),
+}
+SEED = 20261018
+METRIC = "MoE-layer tokens/sec at 1/2/4/8 B200; % tcgen05 peak (GEMM), % HBM BW (dispatch)"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            j = json.load(fh)
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50", "-i", self.gpu_id],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"], samples=0)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=max(mx) if mx else None,
+                    power_w_max=max(pw) if pw else None, reasons=sorted(reasons), samples=len(sm))
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+# ------------------------------------------------------------------------------------------
+# CPU baseline: the reference implementation (or the oracle port) on a bounded token sample
+def cpu_sample(cfg, t_sample: int, kind_pref: str = "reference"):
+    """Prepare a bounded sample of the configured layer for the CPU oracle. Weights are random
+    uniform values (the reference arithmetic is data-independent: dense fp64-accumulated loops),
+    tokens and router weights are the §8(d) PRNG streams so routing is realistic."""
+    from oracle.oracle import Oracle, available, make_inputs
+    kind = "reference" if (kind_pref == "reference" and available("reference")) else "port"
+    o = Oracle(kind)
+    d, n, k, f = cfg["d"], cfg["N"], cfg["K"], cfg["f"]
+    inp = make_inputs(t_sample, d, n, f, experts=False)
+    rng = np.random.default_rng(0)
+    a = np.float32(1.0 / np.sqrt(d))
+    w_in = (rng.random((n, d, 2 * f), dtype=np.float32) - np.float32(0.5)) * a
+    w_out = (rng.random((n, f, d), dtype=np.float32) - np.float32(0.5)) * a
+    return o, kind, inp, w_in, w_out
+
+
+def cpu_step(o, inp, w_in, w_out, k, jobs):
+    r = o.route(inp["x"], inp["w_router"], k)
+    return o.moe_forward(inp["x"], w_in, w_out, r["topk_idx"], r["combine_weights"], jobs=jobs)
+
+
+def pick_cpu_tokens(cfg):
+    # ~45 GFLOP per 64 tokens at the C2 shape; aim for ~5-20 s of CPU work per sample.
+    flop_per_tok = 2 * cfg["K"] * 3 * cfg["d"] * cfg["f"]
+    return int(max(8, min(cfg["T"], round(60e9 / flop_per_tok / 8) * 8)))
+
+
+def run_reference(args, cfg):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    t_s = pick_cpu_tokens(cfg)
+    jobs = os.cpu_count() or 1
+    o, kind, inp, w_in, w_out = cpu_sample(cfg, t_s)
+    cores = min(jobs, cfg["N"])
+    for _ in range(args.warmup):
+        cpu_step(o, inp, w_in, w_out, cfg["K"], jobs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_step(o, inp, w_in, w_out, cfg["K"], jobs)
+    dt = time.perf_counter() - t0
+    val = t_s * args.steps / dt
+    sample = (f"{t_s} of {cfg['T']} tokens per step at the layer shape d={cfg['d']} N={cfg['N']} K={cfg['K']} "
+              f"f={cfg['f']} (fp32, expert fan-out over {cores} threads via the reference parallel_for)")
+    line = dict(metric=METRIC, value=val, unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+                ms_per_step=dt / args.steps * 1e3, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f32", data="synthetic", impl="reference",
+                config=dict(workload=cfg["workload"], T=cfg["T"], d=cfg["d"], n_experts=cfg["N"], top_k=cfg["K"],
+                            d_ff=cfg["f"], parallelism="cpu", sample_tokens=t_s),
+                cpu_baseline=dict(value=val, unit="tokens/s", cores=cores, kind=kind, sample=sample),
+                e2e=dict(value=val, unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+
+    T, d, N, K, f = cfg["T"], cfg["d"], cfg["N"], cfg["K"], cfg["f"]
+    layer = MoELayer(MoEConfig(d_model=d, n_experts=N, top_k=K, d_ff=f, max_tokens=T, device=local_rank,
+                               gemm_ctas=args.gemm_ctas), seed=SEED)
+    x = layer.synthetic_tokens(T, SEED + rank)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        layer._check(layer.L.cl_moe_forward(layer.h, x.data_ptr(), T, out.data_ptr(), None, stream.cuda_stream),
+                     "forward")
+
+    for _ in range(args.warmup):
+        step()
+    layer.sync()
+
+    props = torch.cuda.get_device_properties(local_rank)
+    sampler = ClockSampler("GPU-" + str(props.uuid) if getattr(props, "uuid", None) else str(local_rank))
+    layer.profile(True)
+    sampler.start()
+    time.sleep(0.3)  # let the sampler attach
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    layer.sync()
+    ms = ev0.elapsed_time(ev1)
+    stage_ms, calls = layer.profile_read()
+    layer.profile(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_step = ms / args.steps
+    value = world * T * args.steps / (ms / 1e3)
+
+    # ---- end to end through the host-buffer C-ABI call (pinned host bf16 in/out) ----
+    xh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+    xh.copy_(x)
+    oh = torch.empty_like(xh, pin_memory=True)
+    for _ in range(2):
+        layer.forward_host_ptr(xh.data_ptr(), T, oh.data_ptr())
+    e2e_steps = max(3, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        layer.forward_host_ptr(xh.data_ptr(), T, oh.data_ptr())
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = world * T * e2e_steps / e2e_s
+
+    # ---- roofline of the dominant kernel (GEMM1 + SwiGLU) and of dispatch ----
+    peaks = load_peaks()
+    per = {k: v / max(calls, 1) for k, v in stage_ms.items()}
+    g1_flop = 2.0 * T * K * d * (2 * f)
+    g2_flop = 2.0 * T * K * f * d
+    g1_tf = g1_flop / (per["gemm1"] * 1e-3) / 1e12
+    g2_tf = g2_flop / (per["gemm2"] * 1e-3) / 1e12
+    disp_bytes = T * d * 2 + T * K * d * 2 + 8 * T * K
+    comb_bytes = T * K * d * 2 + T * d * 2 + 8 * T * K
+    disp_gbs = disp_bytes / (per["dispatch"] * 1e-3) / 1e9
+    comb_gbs = comb_bytes / (per["combine"] * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(f"{T}x{d}x{N}x{K}x{f}")
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+            data="synthetic (device-generated reference-PRNG tokens and random-init weights)",
+            config=dict(workload=cfg["workload"], T=T, d=d, n_experts=N, top_k=K, d_ff=f,
+                        global_batch=T * world, parallelism=("dp%d (replicas)" % world) if world > 1 else "single",
+                        gemm_ctas=args.gemm_ctas or 2, l2="inputs larger than L2 (x 134 MB, weights 5.6 GB); no flush"),
+            roofline=dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
+                          peak=peaks["bf16_sus"], unit="TFLOP/s", frac=g1_tf / peaks["bf16_sus"],
+                          frac_of_burst=g1_tf / peaks["bf16"], peak_kind=f"sustained ({peaks['src']})",
+                          traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"]),
+            stages=dict(
+                ms=per,
+                gemm2=dict(achieved=g2_tf, unit="TFLOP/s", frac=g2_tf / peaks["bf16_sus"]),
+                dispatch=dict(achieved=disp_gbs, unit="GB/s", frac=disp_gbs / peaks["hbm"], bytes=disp_bytes),
+                combine=dict(achieved=comb_gbs, unit="GB/s", frac=comb_gbs / peaks["hbm"], bytes=comb_bytes),
+                layer_tflops=(g1_flop + g2_flop) / (ms_step * 1e-3) / 1e12),
+            e2e=dict(value=e2e_val, unit="tokens/s", h2d_bytes_per_step=T * d * 2, d2h_bytes_per_step=T * d * 2,
+                     timing="host wall clock around synchronous cl_moe_forward_host calls"),
+            gpu_launches=6 * args.steps,
+            clocks=clocks,
+        )
+        if not args.no_cpu_baseline and world == 1:
+            t_s = pick_cpu_tokens(cfg)
+            o, kind, inp, w_in, w_out = cpu_sample(cfg, t_s)
+            jobs = os.cpu_count() or 1
+            cpu_step(o, inp, w_in, w_out, K, jobs)  # warm
+            t0 = time.perf_counter()
+            cpu_step(o, inp, w_in, w_out, K, jobs)
+            dt = time.perf_counter() - t0
+            line["cpu_baseline"] = dict(
+                value=t_s / dt, unit="tokens/s", cores=min(jobs, N), kind=kind,
+                sample=f"{t_s} tokens of the same layer shape, one forward, fp32 (expert fan-out over "
+                       f"{min(jobs, N)} threads)")
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--gemm-ctas", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,13 @@ cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* view);
  * into the device buffer `dst` (`bytes` bytes), stream-ordered after the last call. */
 cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, void* stream);
 
+/* Per-stage device timing with CUDA events recorded on the launch stream between the kernels of
+ * each call: stages 0 router, 1 plan, 2 dispatch, 3 GEMM1(+SwiGLU), 4 GEMM2(+weight), 5 combine.
+ * profile_read returns the summed milliseconds per stage over the calls since enabling/reading
+ * (stage_ms has 6 entries) and the number of calls; it synchronises on the recorded events. */
+cl_status cl_moe_profile(cl_moe* h, int32_t enable);
+cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls);
+
 /* Expert-aware FP8. Calibration (collect_calibration) runs
  * the bf16 layer on `hidden` and accumulates per-expert activation maxima of the GEMM1 input and
  * the SwiGLU output; quantize then sets per-expert activation scales = max/448 and per-(expert,

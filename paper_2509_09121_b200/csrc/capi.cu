@@ -130,6 +130,12 @@ struct cl_moe {
   cudaStream_t own_stream = nullptr;
   int64_t last_rows = 0;
 
+  // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
+  bool prof = false;
+  std::vector<std::vector<cudaEvent_t>> prof_sets;
+  size_t prof_used = 0;
+  std::vector<cudaEvent_t>* cur_ev = nullptr;
+
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
   bool maps_q = false;
@@ -143,6 +149,8 @@ struct cl_moe {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (own_stream) cudaStreamDestroy(own_stream);
+    for (auto& v : prof_sets)
+      for (auto e : v) cudaEventDestroy(e);
   }
 };
 
@@ -162,6 +170,23 @@ cl_status guarded(cl_moe* h, Fn fn) {
     h->last_error = e.what();
     return CL_ERR_RUN;
   }
+}
+
+constexpr int kStages = 6;  // router, plan, dispatch, gemm1, gemm2, combine
+
+void prof_begin(cl_moe* h, cudaStream_t st) {
+  h->cur_ev = nullptr;
+  if (!h->prof) return;
+  if (h->prof_used == h->prof_sets.size()) {
+    std::vector<cudaEvent_t> v(kStages + 1);
+    for (auto& e : v) CK(cudaEventCreate(&e));
+    h->prof_sets.push_back(v);
+  }
+  h->cur_ev = &h->prof_sets[h->prof_used++];
+  CK(cudaEventRecord((*h->cur_ev)[0], st));
+}
+void prof_mark(cl_moe* h, int stage, cudaStream_t st) {
+  if (h->cur_ev) CK(cudaEventRecord((*h->cur_ev)[stage + 1], st));
 }
 
 void validate(const cl_moe_config* c) {
@@ -289,11 +314,14 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   const int N4 = (N + 3) / 4 * 4;
   const size_t smem = sizeof(float) * (tpc * (kRouterChunk + 1) + kRouterChunk * N4 + tpc * N4);
+  prof_begin(h, st);
   router_kernel<<<n_tiles, kRouterThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), h->wr, (int)T,
                                                        (int)h->d, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
+  prof_mark(h, 0, st);
   plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
+  prof_mark(h, 1, st);
 }
 
 void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T, cudaStream_t st) {
@@ -304,10 +332,13 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   CK(cudaMemcpyAsync(h->rb.topk_idx, idx, sizeof(int32_t) * T * h->K, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(h->rb.combine_w, w, sizeof(float) * T * h->K, cudaMemcpyDeviceToDevice, st));
+  prof_begin(h, st);
   decision_tiles_kernel<<<n_tiles, 128, 0, st>>>(h->rb.topk_idx, (int)T, N, (int)h->K, tpc, h->rb);
   CK(cudaGetLastError());
+  prof_mark(h, 0, st);
   plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
+  prof_mark(h, 1, st);
 }
 
 // dispatch + expert FFN + combine (local experts; ep_size == 1).
@@ -326,6 +357,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
                                                    (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
                                                    h->perm, h->inv, h->row_w, nullptr);
   CK(cudaGetLastError());
+  prof_mark(h, 2, st);
 
   GemmArgs g1{};
   g1.offsets = h->rb.offsets;
@@ -353,20 +385,25 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   if (!fp8) {
     if (v) {
       launch_gemm<2, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
       launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
     } else {
       launch_gemm<1, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
       launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
     }
   } else {
     if (v) {
       launch_gemm<2, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
       launch_gemm<2, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
     } else {
       launch_gemm<1, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
       launch_gemm<1, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
     }
   }
+  prof_mark(h, 4, st);
   if (out_f32)
     combine_kernel<float><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out),
                                                   h->rb.finite_flag);
@@ -374,6 +411,8 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
     combine_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K,
                                                           static_cast<__nv_bfloat16*>(out), h->rb.finite_flag);
   CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
   h->last_rows = T * h->K;
 }
 
@@ -600,6 +639,31 @@ cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, 
     if (!dst || bytes < 0) throw ConfigErr("bad destination");
     CK(cudaSetDevice(h->cfg.device));
     CK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  });
+}
+
+cl_status cl_moe_profile(cl_moe* h, int32_t enable) {
+  return guarded(h, [&] {
+    h->prof = enable != 0;
+    h->prof_used = 0;
+  });
+}
+
+cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    for (int s = 0; s < kStages; ++s) stage_ms[s] = 0.0;
+    for (size_t c = 0; c < h->prof_used; ++c) {
+      auto& ev = h->prof_sets[c];
+      CK(cudaEventSynchronize(ev[kStages]));
+      for (int s = 0; s < kStages; ++s) {
+        float ms = 0.0f;
+        CK(cudaEventElapsedTime(&ms, ev[s], ev[s + 1]));
+        stage_ms[s] += ms;
+      }
+    }
+    *calls = static_cast<int64_t>(h->prof_used);
+    h->prof_used = 0;
   });
 }
 

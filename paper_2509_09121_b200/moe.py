@@ -207,6 +207,18 @@ class MoELayer:
                     "fp8_scales")
         return a, b, wi, wo
 
+    # ---------------------------------------------------------------- per-stage timing
+    STAGES = ("router", "plan", "dispatch", "gemm1", "gemm2", "combine")
+
+    def profile(self, enable: bool = True):
+        self._check(self.L.cl_moe_profile(self.h, int(enable)), "profile")
+
+    def profile_read(self):
+        ms = (C.c_double * 6)()
+        calls = C.c_int64()
+        self._check(self.L.cl_moe_profile_read(self.h, ms, C.byref(calls)), "profile_read")
+        return {k: ms[i] for i, k in enumerate(self.STAGES)}, calls.value
+
     # ---------------------------------------------------------------- stage access (tests)
     def stage(self, name: str, shape, dtype) -> torch.Tensor:
         out = torch.empty(shape, dtype=dtype, device=self.device)
