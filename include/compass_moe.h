@@ -129,6 +129,15 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
 cl_status cl_moe_forward_host(cl_moe* h, const void* hidden_host, int64_t T, void* out_host,
                               int32_t io_dtype);
 
+/* Pipelined variant of cl_moe_forward_host: enqueues the H2D copy, the layer and the D2H copy
+ * on the handle's internal copy / compute streams and returns. Two internal slots let the copies
+ * of neighbouring calls overlap the compute; `hidden_host` must stay valid and `out_host` must
+ * not be read until cl_moe_host_wait returns (pinned host memory gives asynchronous copies). */
+cl_status cl_moe_forward_host_async(cl_moe* h, const void* hidden_host, int64_t T, void* out_host,
+                                    int32_t io_dtype);
+/* Waits for every enqueued host-buffer call; reports non-finite outputs like cl_moe_sync. */
+cl_status cl_moe_host_wait(cl_moe* h);
+
 /* Waits for `stream` and reports device-side failures: any non-finite router logit or layer
  * output (the reference's check_finite, proj/src/tensor.cpp:35-41) -> CL_ERR_RUN. */
 cl_status cl_moe_sync(cl_moe* h, void* stream);

@@ -82,6 +82,8 @@ _PROTOS = {
     "cl_moe_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cl_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(Decision), C.c_void_p]),
     "cl_moe_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32]),
+    "cl_moe_forward_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32]),
+    "cl_moe_host_wait": (C.c_int, [C.c_void_p]),
     "cl_moe_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cl_moe_stage_buffers": (C.c_int, [C.c_void_p, C.POINTER(StageView)]),
     "cl_moe_copy_stage": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p]),

@@ -104,6 +104,7 @@ struct cl_moe {
 
   // weights
   float* wr = nullptr;                 // [d][N] fp32
+  double* wr64 = nullptr;              // [d][N4] fp64 copy streamed by the router
   __nv_bfloat16* win = nullptr;        // [n_local][2f][d] packed
   __nv_bfloat16* wout = nullptr;       // [n_local][d][f] packed
   uint8_t* win8 = nullptr;             // e4m3 copies
@@ -124,10 +125,19 @@ struct cl_moe {
   int32_t* perm = nullptr;
   int32_t* inv = nullptr;
   float* row_w = nullptr;
-  void* io_in = nullptr;               // staging for the host-buffer entry point
-  void* io_out = nullptr;
-  float* io_f32 = nullptr;
-  cudaStream_t own_stream = nullptr;
+  // host-buffer entry points: two pipeline slots so the H2D of call i+1 and the D2H of call i-1
+  // overlap the layer compute of call i (separate copy streams, event-ordered).
+  struct HostSlot {
+    void* x = nullptr;       // bf16 [cap][d]
+    float* xf = nullptr;     // fp32 staging [cap][d] (fp32 io only)
+    void* out = nullptr;     // [cap][d] bf16 or fp32
+    cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
+    bool used = false;
+  } slot[2];
+  int next_slot = 0;
+  void* io_out = nullptr;              // calibration output scratch
+  cudaStream_t own_stream = nullptr;   // compute stream of the host-buffer path
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   int64_t last_rows = 0;
 
   // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
@@ -141,14 +151,20 @@ struct cl_moe {
   bool maps_q = false;
 
   ~cl_moe() {
-    void* ptrs[] = {wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
+    void* ptrs[] = {wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
                     sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
-                    inv,    row_w,   io_in,   io_out,    io_f32,       rb.logits,    rb.probs,
+                    inv,    row_w,   slot[0].x, slot[0].xf, slot[0].out, slot[1].x, slot[1].xf, slot[1].out,
+                    io_out, rb.logits,    rb.probs,
                     rb.topk_idx, rb.combine_w, rb.local_rank, rb.tile_cnt, rb.tile_psum, rb.tile_lse2,
                     rb.counts, rb.offsets, rb.agg_prob, rb.losses, rb.finite_flag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (own_stream) cudaStreamDestroy(own_stream);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
+    for (auto& sl : slot)
+      for (cudaEvent_t e : {sl.h2d, sl.done, sl.d2h})
+        if (e) cudaEventDestroy(e);
     for (auto& v : prof_sets)
       for (auto e : v) cudaEventDestroy(e);
   }
@@ -241,6 +257,13 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->num_sms = prop.multiProcessorCount;
   h->gemm_ctas = c->gemm_ctas == 0 ? 2 : c->gemm_ctas;
   CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
+  for (auto& sl : h->slot) {
+    CK(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
+  }
 
   const int64_t rows = h->cap * h->K;
   const int tpc = router_tokens_per_cta(static_cast<int>(h->N));
@@ -270,6 +293,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->row_w = dalloc<float>(rows);
 
   h->wr = dalloc<float>(h->d * h->N);
+  h->wr64 = dalloc<double>(h->d * ((h->N + 3) / 4 * 4));
+  CK(cudaFuncSetAttribute(router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);
@@ -312,10 +337,9 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int N = static_cast<int>(h->N);
   const int tpc = router_tokens_per_cta(N);
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
-  const int N4 = (N + 3) / 4 * 4;
-  const size_t smem = sizeof(float) * (tpc * (kRouterChunk + 1) + kRouterChunk * N4 + tpc * N4);
+  const size_t smem = router_smem_bytes(N);
   prof_begin(h, st);
-  router_kernel<<<n_tiles, kRouterThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), h->wr, (int)T,
+  router_kernel<<<n_tiles, kRouterThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T,
                                                        (int)h->d, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
@@ -405,11 +429,10 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   }
   prof_mark(h, 4, st);
   if (out_f32)
-    combine_kernel<float><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out),
-                                                  h->rb.finite_flag);
+    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
   else
-    combine_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(h->y, h->inv, (int)T, (int)h->d, (int)h->K,
-                                                          static_cast<__nv_bfloat16*>(out), h->rb.finite_flag);
+    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                  h->rb.finite_flag, st);
   CK(cudaGetLastError());
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
@@ -487,6 +510,8 @@ static cl_status create_common(const cl_moe_config* cfg, cl_moe** out, const flo
       CK(cudaDeviceSynchronize());
       cudaFree(tmp);
     }
+    widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     build_maps(h, false);
   });
@@ -556,44 +581,69 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, co
   });
 }
 
+static void host_enqueue(cl_moe* h, const void* hidden_host, int64_t T, void* out_host, int32_t io_dtype) {
+  if (!hidden_host || !out_host) throw ConfigErr("null argument");
+  if (io_dtype != CL_MOE_IO_BF16 && io_dtype != CL_MOE_IO_F32) throw ConfigErr("io_dtype must be BF16 or F32");
+  if (T < 1) throw RunErr("moe_forward: B must be >= 1");
+  if (T > h->cap) throw ConfigErr("T exceeds max_tokens");
+  CK(cudaSetDevice(h->cfg.device));
+  auto& sl = h->slot[h->next_slot];
+  h->next_slot ^= 1;
+  const bool f32 = io_dtype == CL_MOE_IO_F32;
+  if (!sl.x) {
+    sl.x = dalloc<__nv_bfloat16>(h->cap * h->d);
+    sl.out = dalloc<float>(h->cap * h->d);
+  }
+  if (f32 && !sl.xf) sl.xf = dalloc<float>(h->cap * h->d);
+  const int64_t n = T * h->d;
+  cudaStream_t st = h->own_stream;
+  // H2D may overwrite the slot's input once the compute of its previous use has consumed it
+  if (sl.used) CK(cudaStreamWaitEvent(h->s_h2d, sl.done, 0));
+  if (f32) CK(cudaMemcpyAsync(sl.xf, hidden_host, n * 4, cudaMemcpyHostToDevice, h->s_h2d));
+  else CK(cudaMemcpyAsync(sl.x, hidden_host, n * 2, cudaMemcpyHostToDevice, h->s_h2d));
+  CK(cudaEventRecord(sl.h2d, h->s_h2d));
+  // compute: after this slot's H2D, and after the D2H of the slot's previous output
+  CK(cudaStreamWaitEvent(st, sl.h2d, 0));
+  if (sl.used) CK(cudaStreamWaitEvent(st, sl.d2h, 0));
+  if (f32) {
+    f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(sl.xf, n, static_cast<__nv_bfloat16*>(sl.x));
+    CK(cudaGetLastError());
+  }
+  run_router(h, sl.x, T, st);
+  run_experts(h, sl.x, T, sl.out, f32, st);
+  CK(cudaEventRecord(sl.done, st));
+  CK(cudaStreamWaitEvent(h->s_d2h, sl.done, 0));
+  CK(cudaMemcpyAsync(out_host, sl.out, n * (f32 ? 4 : 2), cudaMemcpyDeviceToHost, h->s_d2h));
+  CK(cudaEventRecord(sl.d2h, h->s_d2h));
+  sl.used = true;
+}
+
+static void host_wait(cl_moe* h) {
+  CK(cudaSetDevice(h->cfg.device));
+  CK(cudaStreamSynchronize(h->s_d2h));
+  CK(cudaStreamSynchronize(h->own_stream));
+  int flag = 0;
+  CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) {
+    CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
+    throw RunErr("non-finite value produced by op 'moe_forward'");
+  }
+}
+
 cl_status cl_moe_forward_host(cl_moe* h, const void* hidden_host, int64_t T, void* out_host, int32_t io_dtype) {
   return guarded(h, [&] {
-    if (!hidden_host || !out_host) throw ConfigErr("null argument");
-    if (io_dtype != CL_MOE_IO_BF16 && io_dtype != CL_MOE_IO_F32) throw ConfigErr("io_dtype must be BF16 or F32");
-    if (T < 1) throw RunErr("moe_forward: B must be >= 1");
-    if (T > h->cap) throw ConfigErr("T exceeds max_tokens");
-    CK(cudaSetDevice(h->cfg.device));
-    cudaStream_t st = h->own_stream;
-    if (!h->io_in) {
-      h->io_in = dalloc<__nv_bfloat16>(h->cap * h->d);
-      h->io_f32 = dalloc<float>(h->cap * h->d);
-    }
-    const int64_t n = T * h->d;
-    if (io_dtype == CL_MOE_IO_BF16) {
-      CK(cudaMemcpyAsync(h->io_in, hidden_host, n * 2, cudaMemcpyHostToDevice, st));
-    } else {
-      CK(cudaMemcpyAsync(h->io_f32, hidden_host, n * 4, cudaMemcpyHostToDevice, st));
-      f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(h->io_f32, n, static_cast<__nv_bfloat16*>(h->io_in));
-      CK(cudaGetLastError());
-    }
-    run_router(h, h->io_in, T, st);
-    const bool f32 = io_dtype == CL_MOE_IO_F32;
-    // fp32 output reuses the fp32 input staging buffer (already converted to bf16 above)
-    void* dout = h->io_f32;
-    if (!f32) {
-      if (!h->io_out) h->io_out = dalloc<__nv_bfloat16>(h->cap * h->d);
-      dout = h->io_out;
-    }
-    run_experts(h, h->io_in, T, dout, f32, st);
-    CK(cudaMemcpyAsync(out_host, dout, n * (f32 ? 4 : 2), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    int flag = 0;
-    CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
-    if (flag) {
-      CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
-      throw RunErr("non-finite value produced by op 'moe_forward'");
-    }
+    host_enqueue(h, hidden_host, T, out_host, io_dtype);
+    host_wait(h);
   });
+}
+
+cl_status cl_moe_forward_host_async(cl_moe* h, const void* hidden_host, int64_t T, void* out_host,
+                                    int32_t io_dtype) {
+  return guarded(h, [&] { host_enqueue(h, hidden_host, T, out_host, io_dtype); });
+}
+
+cl_status cl_moe_host_wait(cl_moe* h) {
+  return guarded(h, [&] { host_wait(h); });
 }
 
 cl_status cl_moe_sync(cl_moe* h, void* stream) {

@@ -8,7 +8,8 @@
 namespace cmoe {
 
 constexpr int kRouterThreads = 128;
-constexpr int kRouterChunk = 64;  // d-columns staged per step
+constexpr int kRouterChunk = 64;  // d-columns staged per pipeline step (d % 256 == 0 by config)
+constexpr int kRouterTT = 1;      // tokens per thread
 constexpr int kPlanThreads = 1024;
 
 // Device-side routing state shared by the kernels of one forward call.
@@ -25,151 +26,226 @@ struct RouteBufs {
   int32_t* offsets;     // [N+1]
   float* agg_prob;      // [N]
   float* losses;        // [2] aux, z
-  int32_t* finite_flag; // [1] set to 1 on any non-finite router logit (K11)
+  int32_t* finite_flag; // [1] set to 1 on any non-finite router logit or layer output (K11)
 };
 
+// Router tile geometry: one thread per (token, 4 experts); 128 threads per CTA.
 __host__ __device__ inline int router_tokens_per_cta(int n_experts) {
-  const int groups = (n_experts + 3) / 4;  // one thread per (token, 4 experts)
-  return kRouterThreads / groups;
+  const int groups = (n_experts + 3) / 4;
+  return (kRouterThreads / groups) * kRouterTT;
+}
+struct RouterSmem {
+  int tpc, N4, xs;
+  size_t raw_x, sw, sx, slog, sidx, slse, total;
+  __host__ __device__ RouterSmem(int n_experts) {
+    N4 = (n_experts + 3) / 4 * 4;
+    tpc = router_tokens_per_cta(n_experts);
+    xs = kRouterChunk + 2;  // padded fp64 row of one token: 16-byte aligned, conflict-free double2 loads
+    raw_x = 0;
+    sw = raw_x + 2 * (size_t)tpc * kRouterChunk * 2;          // [2][chunk][N4] fp64 (cp.async target)
+    sx = sw + 2 * sizeof(double) * kRouterChunk * N4;         // [tpc][xs] fp64
+    slog = sx + sizeof(double) * tpc * xs;
+    sidx = slog + sizeof(float) * tpc * N4;
+    slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
+    total = slse + sizeof(double) * tpc;
+  }
+};
+__host__ __device__ inline size_t router_smem_bytes(int n_experts) { return RouterSmem(n_experts).total; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// W_r [d][N] fp32 -> fp64 [d][N4] (zero-padded experts), once per handle.
+__global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, double* __restrict__ out) {
+  const int N4 = (N + 3) / 4 * 4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * N4; i += gridDim.x * blockDim.x) {
+    const int l = i / N4, e = i % N4;
+    out[i] = e < N ? static_cast<double>(wr[(size_t)l * N + e]) : 0.0;
+  }
 }
 
 // ---------------------------------------------------------------------------------------
 // K1: router. logits = x W_r with one fp64 accumulator per (token, expert) summed over the
 // hidden dimension in ascending order — the exact accumulation order of the reference gemm_nn
 // (proj/src/tensor.cpp:157-173), so logits are bit-identical to the CPU oracle (each product of
-// two floats is exact in fp64, hence FMA == multiply-then-add). Then per token: softmax in fp64
-// (tensor.cpp:614-621), top-K with lowest-index tie-break (tensor.cpp:1046-1060), renormalised
-// combine weights, per-tile expert counts and local ranks for the stable
-// dispatch permutation, and per-tile partial sums for agg_prob (col_sums, tensor.cpp:545-565) and
-// the Z-loss (tensor.cpp:1011-1040).
+// two floats is exact in fp64, hence FMA == multiply-then-add). x chunks (bf16) and the fp64 copy
+// of W_r stream into shared memory through a double-buffered cp.async pipeline; x is widened to
+// fp64 once per CTA. One thread owns 4 independent accumulator chains (1 token x 4 experts).
+// Then per token: softmax in fp64 (tensor.cpp:614-621), top-K with lowest-index tie-break
+// (tensor.cpp:1046-1060), renormalised combine weights, per-tile expert counts
+// and local ranks for the stable dispatch permutation, and per-tile partial sums for agg_prob
+// (col_sums, tensor.cpp:545-565) and the Z-loss (tensor.cpp:1011-1040).
 __global__ void __launch_bounds__(kRouterThreads) router_kernel(const __nv_bfloat16* __restrict__ x,
-                                                                const float* __restrict__ wr, int T, int d,
+                                                                const double* __restrict__ wr64, int T, int d,
                                                                 int N, int K, RouteBufs rb) {
-  const int groups = (N + 3) / 4;
-  const int tpc = kRouterThreads / groups;  // tokens per CTA
+  const RouterSmem L(N);
+  const int groups = L.N4 / 4;
+  const int N4 = L.N4;
+  const int tg_per_cta = kRouterThreads / groups;
+  const int tpc = L.tpc;  // tokens per CTA
+  const int xs = L.xs;
   const int tile = blockIdx.x;
   const int tok0 = tile * tpc;
-  extern __shared__ uint8_t smem_raw[];
-  float* sx = reinterpret_cast<float*>(smem_raw);                      // [tpc][kRouterChunk+1]
-  float* sw = sx + tpc * (kRouterChunk + 1);                           // [kRouterChunk][N4]
-  const int N4 = groups * 4;
-  float* slog = sw + kRouterChunk * N4;                                // [tpc][N4]
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* rawx = reinterpret_cast<__nv_bfloat16*>(smem_raw + L.raw_x);  // [2][tpc][chunk]
+  double* sw = reinterpret_cast<double*>(smem_raw + L.sw);                     // [2][chunk][N4]
+  double* sx = reinterpret_cast<double*>(smem_raw + L.sx);                     // [tpc][xs]
+  float* slog = reinterpret_cast<float*>(smem_raw + L.slog);                   // [tpc][N4]
+  int* sidx = reinterpret_cast<int*>(smem_raw + L.sidx);                       // [tpc][8]
+  double* slse = reinterpret_cast<double*>(smem_raw + L.slse);                 // [tpc]
 
-  const int t_local = threadIdx.x / groups;
-  const int g = threadIdx.x % groups;
-  const int tok = tok0 + t_local;
-  const bool active = t_local < tpc && tok < T;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int tgi = threadIdx.x / groups;  // token (group)
+  const int g = threadIdx.x % groups;    // expert group
+  const bool worker = tgi < tg_per_cta;
+  double acc[kRouterTT][4];
+#pragma unroll
+  for (int a = 0; a < kRouterTT; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
-  for (int c0 = 0; c0 < d; c0 += kRouterChunk) {
-    const int cw = min(kRouterChunk, d - c0);
-    // stage x[tok0 .. tok0+tpc) x [c0, c0+cw) as fp32, padded rows (bank-conflict free)
-    for (int i = threadIdx.x; i < tpc * kRouterChunk; i += kRouterThreads) {
-      const int r = i / kRouterChunk, c = i % kRouterChunk;
-      float v = 0.0f;
-      if (tok0 + r < T && c < cw) v = __bfloat162float(x[(size_t)(tok0 + r) * d + c0 + c]);
-      sx[r * (kRouterChunk + 1) + c] = v;
+  const int nchunks = d / kRouterChunk;
+  const int xpieces = tpc * kRouterChunk * 2 / 16;  // 16-byte pieces of one x chunk
+  const int wpieces = kRouterChunk * N4 * 8 / 16;
+  auto issue = [&](int c, int buf) {
+    const int c0 = c * kRouterChunk;
+    for (int i = threadIdx.x; i < xpieces; i += kRouterThreads) {
+      const int r = i / (kRouterChunk / 8), q = i % (kRouterChunk / 8);
+      const bool ok = tok0 + r < T;
+      const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
+      cp_async16(rawx + (size_t)buf * tpc * kRouterChunk + r * kRouterChunk + q * 8, src, ok);
     }
-    for (int i = threadIdx.x; i < kRouterChunk * N4; i += kRouterThreads) {
-      const int l = i / N4, e = i % N4;
-      sw[i] = (l < cw && e < N) ? wr[(size_t)(c0 + l) * N + e] : 0.0f;
+    const double* wsrc = wr64 + (size_t)c0 * N4;
+    for (int i = threadIdx.x; i < wpieces; i += kRouterThreads)
+      cp_async16(sw + (size_t)buf * kRouterChunk * N4 + i * 2, wsrc + i * 2, true);
+    cp_async_commit();
+  };
+  issue(0, 0);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) {
+      issue(c + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    if (t_local < tpc) {
-      const float* xr = sx + t_local * (kRouterChunk + 1);
-      const float4* wv = reinterpret_cast<const float4*>(sw) + g;
-      for (int l = 0; l < cw; ++l) {
-        const double xv = static_cast<double>(xr[l]);
-        const float4 w4 = wv[l * groups];
-        acc[0] = fma(xv, static_cast<double>(w4.x), acc[0]);
-        acc[1] = fma(xv, static_cast<double>(w4.y), acc[1]);
-        acc[2] = fma(xv, static_cast<double>(w4.z), acc[2]);
-        acc[3] = fma(xv, static_cast<double>(w4.w), acc[3]);
+    // widen x to fp64, [tok][l] layout
+    const __nv_bfloat16* rx = rawx + (size_t)buf * tpc * kRouterChunk;
+    for (int i = threadIdx.x; i < tpc * kRouterChunk / 2; i += kRouterThreads) {
+      const int r = (2 * i) / kRouterChunk, l = (2 * i) % kRouterChunk;
+      const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(rx)[i];
+      *reinterpret_cast<double2*>(sx + r * xs + l) =
+          make_double2(static_cast<double>(__low2float(v)), static_cast<double>(__high2float(v)));
+    }
+    __syncthreads();
+    if (worker) {
+      const double2* xv = reinterpret_cast<const double2*>(sx + tgi * xs);
+      const double2* wv = reinterpret_cast<const double2*>(sw + (size_t)buf * kRouterChunk * N4 + g * 4);
+#pragma unroll 8
+      for (int l2 = 0; l2 < kRouterChunk / 2; ++l2) {
+        const double2 xx = xv[l2];
+        const double2 wa01 = wv[(2 * l2) * (N4 / 2)];
+        const double2 wa23 = wv[(2 * l2) * (N4 / 2) + 1];
+        const double2 wb01 = wv[(2 * l2 + 1) * (N4 / 2)];
+        const double2 wb23 = wv[(2 * l2 + 1) * (N4 / 2) + 1];
+        acc[0][0] = fma(xx.x, wa01.x, acc[0][0]);
+        acc[0][1] = fma(xx.x, wa01.y, acc[0][1]);
+        acc[0][2] = fma(xx.x, wa23.x, acc[0][2]);
+        acc[0][3] = fma(xx.x, wa23.y, acc[0][3]);
+        acc[0][0] = fma(xx.y, wb01.x, acc[0][0]);
+        acc[0][1] = fma(xx.y, wb01.y, acc[0][1]);
+        acc[0][2] = fma(xx.y, wb23.x, acc[0][2]);
+        acc[0][3] = fma(xx.y, wb23.y, acc[0][3]);
       }
     }
     __syncthreads();
   }
-  if (t_local < tpc) {
+  if (worker) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = g * 4 + i;
-      const float z = static_cast<float>(acc[i]);
-      slog[t_local * N4 + e] = z;
-      if (active && e < N) {
-        rb.logits[(size_t)tok * N + e] = z;
-        if (!isfinite(z)) atomicExch(rb.finite_flag, 1);
+    for (int a = 0; a < kRouterTT; ++a) {
+      const int tl = tgi * kRouterTT + a;
+      const int tok = tok0 + tl;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int e = g * 4 + b;
+        const float z = static_cast<float>(acc[a][b]);
+        slog[tl * N4 + e] = z;
+        if (tok < T && e < N) {
+          rb.logits[(size_t)tok * N + e] = z;
+          if (!isfinite(z)) atomicExch(rb.finite_flag, 1);
+        }
       }
     }
   }
   __syncthreads();
 
-  // ---- per-token softmax / top-K (one thread per token of the tile) ----
-  double lse2 = 0.0;
-  if (threadIdx.x < tpc && tok0 + threadIdx.x < T) {
-    const int j = tok0 + threadIdx.x;
-    const float* z = slog + threadIdx.x * N4;
-    double mx = z[0];
-    for (int e = 1; e < N; ++e) mx = fmax(mx, static_cast<double>(z[e]));
-    double denom = 0.0;
-    for (int e = 0; e < N; ++e) denom += exp(static_cast<double>(z[e]) - mx);
-    float* p = rb.probs + (size_t)j * N;
-    for (int e = 0; e < N; ++e) {
-      const float pe = static_cast<float>(exp(static_cast<double>(z[e]) - mx) / denom);
-      p[e] = pe;
-      slog[threadIdx.x * N4 + e] = pe;  // reuse the row for probs
-    }
-    const double lse = mx + log(denom);
-    lse2 = lse * lse;
-    // top-K by repeated selection: strict '>' keeps the lowest index among equal values.
-    uint64_t taken_lo = 0, taken_hi = 0;  // up to 128 experts tracked in bits; larger N loops
-    float vals[8];
-    int ids[8];
-    const float* prow = slog + threadIdx.x * N4;
-    for (int k = 0; k < K; ++k) {
-      int best = -1;
-      float bv = 0.0f;
+  // ---- per-token softmax / top-K ----
+  const int ntok = min(tpc, T - tok0);
+  for (int tl = threadIdx.x; tl < tpc; tl += kRouterThreads) {
+    double lse2 = 0.0;
+    if (tl < ntok) {
+      const int j = tok0 + tl;
+      float* zrow = slog + tl * N4;
+      double mx = zrow[0];
+      for (int e = 1; e < N; ++e) mx = fmax(mx, static_cast<double>(zrow[e]));
+      double denom = 0.0;
+      for (int e = 0; e < N; ++e) denom += exp(static_cast<double>(zrow[e]) - mx);
+      float* p = rb.probs + (size_t)j * N;
       for (int e = 0; e < N; ++e) {
-        const bool tk = e < 64 ? ((taken_lo >> e) & 1ull) : ((taken_hi >> (e - 64)) & 1ull);
-        if (tk) continue;
-        const float v = prow[e];
-        if (best < 0 || v > bv) { best = e; bv = v; }
+        const float pe = static_cast<float>(exp(static_cast<double>(zrow[e]) - mx) / denom);
+        p[e] = pe;
+        zrow[e] = pe;  // the row now holds probs
       }
-      if (best < 64) taken_lo |= 1ull << best; else taken_hi |= 1ull << (best - 64);
-      vals[k] = bv;
-      ids[k] = best;
+      const double lse = mx + log(denom);
+      lse2 = lse * lse;
+      uint64_t taken_lo = 0, taken_hi = 0;
+      float vals[8];
+      int ids[8];
+      for (int k = 0; k < K; ++k) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < N; ++e) {
+          const bool tk = e < 64 ? ((taken_lo >> e) & 1ull) : ((taken_hi >> (e - 64)) & 1ull);
+          if (tk) continue;
+          const float v = zrow[e];
+          if (best < 0 || v > bv) { best = e; bv = v; }  // strict '>' keeps the lowest index on ties
+        }
+        if (best < 64) taken_lo |= 1ull << best; else taken_hi |= 1ull << (best - 64);
+        vals[k] = bv;
+        ids[k] = best;
+      }
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s += static_cast<double>(vals[k]);
+      for (int k = 0; k < K; ++k) {
+        rb.topk_idx[(size_t)j * K + k] = ids[k];
+        rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / s);
+        sidx[tl * 8 + k] = ids[k];
+      }
     }
-    double s = 0.0;
-    for (int k = 0; k < K; ++k) s += static_cast<double>(vals[k]);
-    for (int k = 0; k < K; ++k) {
-      rb.topk_idx[(size_t)j * K + k] = ids[k];
-      rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / s);
-    }
+    slse[tl] = lse2;
   }
   __syncthreads();
 
   // ---- per-tile statistics: expert counts, local ranks, prob sums (one thread per expert) ----
-  const int ntok = min(tpc, T - tok0);
   for (int e = threadIdx.x; e < N; e += kRouterThreads) {
     int cnt = 0;
     double ps = 0.0;
     for (int t = 0; t < ntok; ++t) {
       ps += static_cast<double>(slog[t * N4 + e]);
-      for (int k = 0; k < K; ++k) {
-        const size_t s = (size_t)(tok0 + t) * K + k;
-        if (rb.topk_idx[s] == e) rb.local_rank[s] = cnt++;
-      }
+      for (int k = 0; k < K; ++k)
+        if (sidx[t * 8 + k] == e) rb.local_rank[(size_t)(tok0 + t) * K + k] = cnt++;
     }
     rb.tile_cnt[(size_t)tile * N + e] = cnt;
     rb.tile_psum[(size_t)tile * N + e] = ps;
   }
-  // tile sum of lse^2 in token order (warp 0 holds the tile's tokens when tpc <= 32; general
-  // case goes through shared memory)
-  __shared__ double s_lse[kRouterThreads];
-  s_lse[threadIdx.x] = lse2;
-  __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0.0;
-    for (int t = 0; t < ntok; ++t) a += s_lse[t];
+    for (int t = 0; t < ntok; ++t) a += slse[t];
     rb.tile_lse2[tile] = a;
   }
 }
@@ -180,23 +256,25 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(const __nv_bfloa
 // and Z-loss reductions in a fixed order. One CTA; deterministic (no atomics).
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int n_tiles, int T, int N, int K, RouteBufs rb) {
   __shared__ int s_chunk[kPlanThreads];
-  __shared__ double s_pchunk[kPlanThreads];
-  __shared__ int s_counts[256];
+  __shared__ double s_red[kPlanThreads];
+  __shared__ double s_p[128];
+  __shared__ int s_counts[128];
   const int chunks = kPlanThreads / N;  // chunks of tiles per expert
   const int per = (n_tiles + chunks - 1) / chunks;
   const int e = threadIdx.x % N;
   const int c = threadIdx.x / N;
   const bool act = c < chunks;
+  const int t_begin = act ? min(n_tiles, c * per) : 0;
+  const int t_end = act ? min(n_tiles, (c + 1) * per) : 0;
   int sum = 0;
   double ps = 0.0;
-  if (act) {
-    for (int t = c * per; t < min(n_tiles, (c + 1) * per); ++t) {
-      sum += rb.tile_cnt[(size_t)t * N + e];
-      ps += rb.tile_psum[(size_t)t * N + e];
-    }
+#pragma unroll 8
+  for (int t = t_begin; t < t_end; ++t) {
+    sum += rb.tile_cnt[(size_t)t * N + e];
+    ps += rb.tile_psum[(size_t)t * N + e];
   }
   s_chunk[threadIdx.x] = sum;
-  s_pchunk[threadIdx.x] = ps;
+  s_red[threadIdx.x] = ps;
   __syncthreads();
   if (threadIdx.x < N) {
     int run = 0;
@@ -205,22 +283,31 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int n_tiles, int T, 
       const int v = s_chunk[cc * N + threadIdx.x];
       s_chunk[cc * N + threadIdx.x] = run;
       run += v;
-      p += s_pchunk[cc * N + threadIdx.x];
+      p += s_red[cc * N + threadIdx.x];
     }
     s_counts[threadIdx.x] = run;
-    s_pchunk[threadIdx.x] = p;  // chunk 0 slot of this expert now holds the expert's prob sum
+    s_p[threadIdx.x] = p;
     rb.counts[threadIdx.x] = run;
     rb.agg_prob[threadIdx.x] = static_cast<float>(p);
   }
   __syncthreads();
-  if (act) {
-    int run = s_chunk[threadIdx.x];
-    for (int t = c * per; t < min(n_tiles, (c + 1) * per); ++t) {
+  {
+    int run = act ? s_chunk[threadIdx.x] : 0;
+    for (int t = t_begin; t < t_end; ++t) {
       const size_t i = (size_t)t * N + e;
       const int v = rb.tile_cnt[i];
       rb.tile_cnt[i] = run;
       run += v;
     }
+  }
+  // Z-loss: fixed-order two-level reduction of the per-tile lse^2 sums.
+  double z = 0.0;
+  for (int t = threadIdx.x; t < n_tiles; t += kPlanThreads) z += rb.tile_lse2[t];
+  s_red[threadIdx.x] = z;
+  __syncthreads();
+  for (int w = kPlanThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
+    __syncthreads();
   }
   if (threadIdx.x == 0) {
     int off = 0;
@@ -228,14 +315,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int n_tiles, int T, 
     for (int x = 0; x < N; ++x) {
       rb.offsets[x] = off;
       off += s_counts[x];
-      aux += s_pchunk[x] * static_cast<double>(s_counts[x]);
+      aux += s_p[x] * static_cast<double>(s_counts[x]);
     }
     rb.offsets[N] = off;
-    double z = 0.0;
-    for (int t = 0; t < n_tiles; ++t) z += rb.tile_lse2[t];
     const double coef = static_cast<double>(N) / (static_cast<double>(T) * T * static_cast<double>(K));
     rb.losses[0] = static_cast<float>(coef * aux);
-    rb.losses[1] = static_cast<float>(z / static_cast<double>(T));
+    rb.losses[1] = static_cast<float>(s_red[0] / static_cast<double>(T));
   }
 }
 
@@ -334,41 +419,70 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
 // K6: weighted combine / un-permute. One warp per token: out[j] = sum_k Y[inv[j,k]] in fp32, slot
 // order (rows of Y already carry the combine weight from the GEMM2 epilogue). Replaces
 // scatter_add_rows + add (proj/src/tensor.cpp:814-845, :248-262) with no intermediate copies.
-template <typename OutT>
+// kK is compile-time so all K x kU 16-byte loads of a lane are in flight together.
+template <typename OutT, int kK>
 __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ inv,
-                                                      int T, int d, int K, OutT* __restrict__ out,
+                                                      int T, int d, OutT* __restrict__ out,
                                                       int32_t* __restrict__ finite_flag) {
+  constexpr int kU = kK <= 2 ? 4 : 2;
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= T) return;
-  int rows[8];
-  for (int k = 0; k < K; ++k) rows[k] = inv[(size_t)j * K + k];
+  const int4* src[kK];
+#pragma unroll
+  for (int k = 0; k < kK; ++k) src[k] = reinterpret_cast<const int4*>(y + (size_t)inv[(size_t)j * kK + k] * d);
   const int nvec = d / 8;
-  for (int v = lane; v < nvec; v += 32) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    int4 raw[8];
-    for (int k = 0; k < K; ++k) raw[k] = ld_nc_v4(reinterpret_cast<const int4*>(y + (size_t)rows[k] * d) + v);
-    for (int k = 0; k < K; ++k) {
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[k]);
+  bool fin = true;
+  for (int v0 = lane; v0 < nvec; v0 += 32 * kU) {
+    int4 raw[kU][kK];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(h[i]);
-    }
-    bool fin = true;
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) fin &= isfinite(acc[i]);
-    if (!fin) atomicExch(finite_flag, 1);
-    if constexpr (sizeof(OutT) == 2) {
-      int4 o;
-      o.x = pack_bf16(acc[0], acc[1]);
-      o.y = pack_bf16(acc[2], acc[3]);
-      o.z = pack_bf16(acc[4], acc[5]);
-      o.w = pack_bf16(acc[6], acc[7]);
-      st_na_v4(reinterpret_cast<int4*>(out + (size_t)j * d) + v, o);
-    } else {
-      float4* o = reinterpret_cast<float4*>(out + (size_t)j * d) + 2 * v;
-      o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      for (int k = 0; k < kK; ++k)
+        if (v0 + u * 32 < nvec) raw[u][k] = ld_nc_v4(src[k] + v0 + u * 32);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int v = v0 + u * 32;
+      if (v >= nvec) break;
+      float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int k = 0; k < kK; ++k) {
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[u][k]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(h[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fin &= isfinite(acc[i]);
+      if constexpr (sizeof(OutT) == 2) {
+        int4 o;
+        o.x = pack_bf16(acc[0], acc[1]);
+        o.y = pack_bf16(acc[2], acc[3]);
+        o.z = pack_bf16(acc[4], acc[5]);
+        o.w = pack_bf16(acc[6], acc[7]);
+        st_na_v4(reinterpret_cast<int4*>(out + (size_t)j * d) + v, o);
+      } else {
+        float4* o = reinterpret_cast<float4*>(out + (size_t)j * d) + 2 * v;
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      }
     }
+  }
+  if (!fin) atomicExch(finite_flag, 1);
+}
+
+template <typename OutT>
+inline void launch_combine(const __nv_bfloat16* y, const int32_t* inv, int T, int d, int K, OutT* out, int32_t* flag,
+                           cudaStream_t st) {
+  const int blocks = (T + 7) / 8;
+  switch (K) {
+    case 1: combine_kernel<OutT, 1><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 2: combine_kernel<OutT, 2><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 3: combine_kernel<OutT, 3><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 4: combine_kernel<OutT, 4><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 5: combine_kernel<OutT, 5><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 6: combine_kernel<OutT, 6><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 7: combine_kernel<OutT, 7><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    default: combine_kernel<OutT, 8><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
   }
 }
 

@@ -167,6 +167,14 @@ class MoELayer:
         self._check(self.L.cl_moe_forward_host(self.h, C.c_void_p(x_ptr), t, C.c_void_p(out_ptr), io_dtype),
                     "forward_host")
 
+    def forward_host_async(self, x_ptr: int, t: int, out_ptr: int, io_dtype: int = _lib.CL_MOE_IO_BF16) -> None:
+        """Pipelined host-buffer call (pinned buffers); completes at host_wait()."""
+        self._check(self.L.cl_moe_forward_host_async(self.h, C.c_void_p(x_ptr), t, C.c_void_p(out_ptr), io_dtype),
+                    "forward_host_async")
+
+    def host_wait(self) -> None:
+        self._check(self.L.cl_moe_host_wait(self.h), "host_wait")
+
     @staticmethod
     def aux_loss(decision: RouterDecision) -> float:
         return float(decision.aux.item())

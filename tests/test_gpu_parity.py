@@ -225,6 +225,13 @@ def test_forward_host_matches_device():
     bits = x.view(torch.int16).cpu().numpy().view(np.uint16)
     out_b = lay.forward_host(bits, "bf16")
     assert np.array_equal(out_b, out.view(torch.int16).cpu().numpy().view(np.uint16))
+    # pipelined host path: several calls in flight, identical results
+    outs = [np.empty_like(bits) for _ in range(3)]
+    for o_ in outs:
+        lay.forward_host_async(bits.ctypes.data, t, o_.ctypes.data)
+    lay.host_wait()
+    for o_ in outs:
+        assert np.array_equal(o_, out_b)
     out_f = lay.forward_host(inp["x"], "f32")
     o = Oracle("port")
     r = o.route(inp["x"], inp["w_router"], k)
