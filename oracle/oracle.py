@@ -234,3 +234,42 @@ def make_inputs(t: int, d: int, n: int, f: int, seed: int = ROOT_SEED, bf16: boo
             w_out = o.round_bf16(w_out)
         out.update(w_in=w_in, w_out=w_out)
     return out
+
+
+def moe_forward_fp8_sim(o: Oracle, x, w_in, w_out, idx, w, s_in, s_mid, ws_in=None, ws_out=None):
+    """Expert-aware FP8 layer simulated with the oracle's E4M3 qdq:
+    per expert e, X_e -> qdq(X_e, s_in[e]); every output channel of W_in[e] / W_out[e] -> qdq with
+    scale = channel absmax / 448 (per-output-channel weight scales); GEMMs in
+    float64; A = silu(G) * U -> qdq(A, s_mid[e]); Y = A_q W_out_q; out = sum_k w * Y in slot order.
+    Returns (out float64 [T x d], ws_in [N x 2f] (reference column order), ws_out [N x d])."""
+    t, d = x.shape
+    n, _, f2 = w_in.shape
+    f = f2 // 2
+    k = idx.shape[1]
+    if ws_in is None:
+        ws_in = np.empty((n, f2), np.float32)
+        ws_out = np.empty((n, d), np.float32)
+        for e in range(n):
+            m = np.abs(w_in[e]).max(0)
+            ws_in[e] = np.where(m > 0, m / np.float32(448.0), np.float32(1.0))
+            m = np.abs(w_out[e]).max(0)
+            ws_out[e] = np.where(m > 0, m / np.float32(448.0), np.float32(1.0))
+    out = np.zeros((t, d), np.float64)
+    for e in range(n):
+        rows, slots = np.nonzero(idx == e)
+        if len(rows) == 0:
+            continue
+        xq = o.fp8_qdq(x[rows], float(s_in[e])).reshape(len(rows), d)
+        wq = np.empty_like(w_in[e])
+        for c in range(f2):
+            wq[:, c] = o.fp8_qdq(w_in[e][:, c], float(ws_in[e][c]))
+        h = xq.astype(np.float64) @ wq.astype(np.float64)
+        g, u = h[:, :f], h[:, f:]
+        a = (g / (1.0 + np.exp(-g)) * u).astype(np.float32)
+        aq = o.fp8_qdq(a, float(s_mid[e])).reshape(a.shape)
+        woq = np.empty_like(w_out[e])
+        for c in range(d):
+            woq[:, c] = o.fp8_qdq(w_out[e][:, c], float(ws_out[e][c]))
+        y = aq.astype(np.float64) @ woq.astype(np.float64)
+        out[rows] += w[rows, slots][:, None].astype(np.float64) * y
+    return out, ws_in, ws_out

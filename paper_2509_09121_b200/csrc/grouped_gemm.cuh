@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           wsg = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
           wsu = wsg + kBN / 2;
         }
-        if constexpr (kOutFp8) so = 1.0f / args.out_scale[ti.e];
+        if constexpr (kOutFp8) so = args.out_scale[ti.e];
 #pragma unroll 1
         for (int c = 0; c < kBN / 2 / 32; ++c) {
           uint32_t g[32], u[32];
@@ -248,10 +248,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               uint32_t p[8];
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
-                const __nv_fp8x2_storage_t lo =
-                    __nv_cvt_float2_to_fp8x2(make_float2(v[4 * i] * so, v[4 * i + 1] * so), __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                    make_float2(__fdiv_rn(v[4 * i], so), __fdiv_rn(v[4 * i + 1], so)), __NV_SATFINITE, __NV_E4M3);
                 const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-                    make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
+                    make_float2(__fdiv_rn(v[4 * i + 2], so), __fdiv_rn(v[4 * i + 3], so)), __NV_SATFINITE, __NV_E4M3);
                 p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
               }
               uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;

@@ -363,13 +363,13 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
   if (j >= T) return;
   const int tile = j / tpc;
   int rows[8];
-  float inv_s[8];
+  float sc[8];
   for (int k = 0; k < K; ++k) {
     const size_t s = (size_t)j * K + k;
     const int e = idx[s];
     const int r = rb.offsets[e] + rb.tile_cnt[(size_t)tile * N + e] + rb.local_rank[s];
     rows[k] = r;
-    if constexpr (kFp8) inv_s[k] = 1.0f / act_scale[e];
+    if constexpr (kFp8) sc[k] = act_scale[e];
     if (lane == 0) {
       inv[s] = r;
       perm[r] = static_cast<int32_t>(s);
@@ -402,10 +402,11 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
         uint32_t p[2];
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
+          // x / scale with IEEE division, then RNE + saturate to E4M3 (SPEC.md:523-531 fp8_qdq)
           const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-              make_float2(f[4 * i] * inv_s[k], f[4 * i + 1] * inv_s[k]), __NV_SATFINITE, __NV_E4M3);
+              make_float2(__fdiv_rn(f[4 * i], sc[k]), __fdiv_rn(f[4 * i + 1], sc[k])), __NV_SATFINITE, __NV_E4M3);
           const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-              make_float2(f[4 * i + 2] * inv_s[k], f[4 * i + 3] * inv_s[k]), __NV_SATFINITE, __NV_E4M3);
+              make_float2(__fdiv_rn(f[4 * i + 2], sc[k]), __fdiv_rn(f[4 * i + 3], sc[k])), __NV_SATFINITE, __NV_E4M3);
           p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
         }
         uint2* dst = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(xperm) + (size_t)rows[k] * d) + v;

@@ -101,11 +101,11 @@ __global__ void quantize_rows_e4m3_kernel(const __nv_bfloat16* __restrict__ w, i
   float m = 0.0f;
   for (int i = lane; i < kdim; i += 32) m = fmaxf(m, fabsf(__bfloat162float(src[i])));
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const float s = m > 0.0f ? m / 448.0f : 1.0f;
+  const float s = m > 0.0f ? __fdiv_rn(m, 448.0f) : 1.0f;
   if (lane == 0) scale[r] = s;
   uint8_t* dst = q + r * kdim;
   for (int i = lane; i < kdim; i += 32)
-    dst[i] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__bfloat162float(src[i]) / s, __NV_SATFINITE, __NV_E4M3));
+    dst[i] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__fdiv_rn(__bfloat162float(src[i]), s), __NV_SATFINITE, __NV_E4M3));
 }
 
 // Calibration (collect_calibration): per-expert max |value| over the rows of
