@@ -178,8 +178,15 @@ def run_ours(args, cfg):
     from paper_2509_09121_b200.moe import MoEConfig, MoELayer
 
     T, d, N, K, f = cfg["T"], cfg["d"], cfg["N"], cfg["K"], cfg["f"]
+    if world > 1 and N % world:
+        raise SystemExit(f"n_experts={N} is not divisible by {world} ranks")
     layer = MoELayer(MoEConfig(d_model=d, n_experts=N, top_k=K, d_ff=f, max_tokens=T, device=local_rank,
-                               gemm_ctas=args.gemm_ctas), seed=SEED)
+                               gemm_ctas=args.gemm_ctas, ep_size=world, ep_rank=rank), seed=SEED)
+    if world > 1:
+        # expert parallelism: NCCL id from rank 0, communicator owned by the library
+        obj = [MoELayer.ep_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        layer.ep_init(obj[0])
     x = layer.synthetic_tokens(T, SEED + rank)
     out = torch.empty_like(x)
     stream = torch.cuda.current_stream()
@@ -265,7 +272,8 @@ def run_ours(args, cfg):
             ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
             data="synthetic (device-generated reference-PRNG tokens and random-init weights)",
             config=dict(workload=cfg["workload"], T=T, d=d, n_experts=N, top_k=K, d_ff=f,
-                        global_batch=T * world, parallelism=("dp%d (replicas)" % world) if world > 1 else "single",
+                        global_batch=T * world, parallelism=("ep%d (experts %d/rank, NCCL all-to-all)" % (world, N // world))
+                        if world > 1 else "single",
                         gemm_ctas=args.gemm_ctas or 2, l2="inputs larger than L2 (x 134 MB, weights 5.6 GB); no flush"),
             roofline=dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
                           peak=peaks["bf16_sus"], unit="TFLOP/s", frac=g1_tf / peaks["bf16_sus"],

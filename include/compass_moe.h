@@ -168,6 +168,24 @@ cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
 cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,
                                 float* w_out_scale);
 
+/* ---- Expert parallelism. One process per GPU; cfg.ep_size ranks, rank
+ * cfg.ep_rank owns experts [rank*N/ep_size, (rank+1)*N/ep_size) (pass only those experts'
+ * weights to cl_moe_create). Every rank routes its own tokens over all N experts; rows travel
+ * to the owning rank over NCCL (NVLink) and back. ---- */
+/* 128-byte NCCL unique id, generated on one rank and distributed by the caller. */
+cl_status cl_moe_ep_unique_id(uint8_t* id_out);
+/* Collective over the ep_size ranks: creates the handle's communicator. */
+cl_status cl_moe_ep_init(cl_moe* h, const uint8_t* id);
+/* Expert-parallel layer forward (cl_moe_forward dispatches here when ep_size > 1; with
+ * ep_size == 1 this runs the same exchange code in loopback). bf16 only. */
+cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
+                            const cl_moe_decision* decision, void* stream);
+/* Pure host helper (no GPU): receive layout of `rank` from the all-gathered count matrix
+ * counts[R][N] (row = source rank). local_offsets[N/R+1], recv_piece[(N/R)*R] indexed
+ * e*R + s = first receive row of (local expert e, source s); recv_total = rows received. */
+cl_status cl_moe_ep_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank,
+                           int64_t* local_offsets, int64_t* recv_piece, int64_t* recv_total);
+
 #ifdef __cplusplus
 }
 #endif

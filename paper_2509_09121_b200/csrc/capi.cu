@@ -20,6 +20,7 @@
 #include "grouped_gemm.cuh"
 #include "moe_kernels.cuh"
 #include "synth_pack.cuh"
+#include "ep.cuh"
 
 using namespace cmoe;
 
@@ -146,6 +147,18 @@ struct cl_moe {
   size_t prof_used = 0;
   std::vector<cudaEvent_t>* cur_ev = nullptr;
 
+  // expert parallelism (ep.cuh)
+  NcclApi::Comm comm = nullptr;
+  int64_t recv_cap = 0;                 // receive-buffer rows (worst case: every rank's every slot)
+  __nv_bfloat16* x_recv = nullptr;      // [recv_cap][d]
+  __nv_bfloat16* act_recv = nullptr;    // [recv_cap][f]
+  __nv_bfloat16* y_recv = nullptr;      // [recv_cap][d]
+  int32_t* ep_counts_dev = nullptr;     // [R][N] all-gathered counts
+  int32_t* ep_off_dev = nullptr;        // [NL+1] local expert offsets in the receive buffer
+  int32_t* ep_counts_host = nullptr;    // pinned mirrors
+  int32_t* ep_off_host = nullptr;
+  CUtensorMap mA1e[2], mA2e[2];
+
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
   bool maps_q = false;
@@ -159,6 +172,11 @@ struct cl_moe {
                     rb.counts, rb.offsets, rb.agg_prob, rb.losses, rb.finite_flag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
+    for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev})
+      if (p) cudaFree(p);
+    if (ep_counts_host) cudaFreeHost(ep_counts_host);
+    if (ep_off_host) cudaFreeHost(ep_off_host);
+    if (comm) NcclApi::get().CommDestroy(comm);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
@@ -365,9 +383,65 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
   prof_mark(h, 1, st);
 }
 
+// GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
+void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
+               const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
+               cudaStream_t st) {
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  GemmArgs g1{};
+  g1.offsets = offsets;
+  g1.n_experts = h->n_local;
+  g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
+  g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
+  g1.b_rows_per_expert = static_cast<int>(2 * h->f);
+  g1.out = act;
+  g1.ldo = static_cast<int>(h->f);
+  g1.act_scale = h->sx_in;
+  g1.w_scale = h->ws_in;
+  g1.out_scale = h->sx_mid;
+  GemmArgs g2{};
+  g2.offsets = offsets;
+  g2.n_experts = h->n_local;
+  g2.n_tiles_n = static_cast<int>(h->d / kBN);
+  g2.num_kb = static_cast<int>(h->f * (fp8 ? 1 : 2) / kBKBytes);
+  g2.b_rows_per_expert = static_cast<int>(h->d);
+  g2.out = y;
+  g2.ldo = static_cast<int>(h->d);
+  g2.row_scale = row_w;
+  g2.act_scale = h->sx_mid;
+  g2.w_scale = h->ws_out;
+  const int v = h->gemm_ctas == 2 ? 1 : 0;
+  if (!fp8) {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<2, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<1, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
+    }
+  } else {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<2, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<1, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
+    }
+  }
+}
+
 // dispatch + expert FFN + combine (local experts; ep_size == 1).
+void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st);
+
 void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
-  if (h->cfg.ep_size > 1) throw ConfigErr("expert-parallel forward goes through the EP entry points");
+  if (h->cfg.ep_size > 1) {
+    run_ep(h, x, T, out, out_f32, st);
+    return;
+  }
   const int N = static_cast<int>(h->N);
   const int tpc = router_tokens_per_cta(N);
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
@@ -383,50 +457,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
 
-  GemmArgs g1{};
-  g1.offsets = h->rb.offsets;
-  g1.n_experts = h->n_local;
-  g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
-  g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
-  g1.b_rows_per_expert = static_cast<int>(2 * h->f);
-  g1.out = h->act;
-  g1.ldo = static_cast<int>(h->f);
-  g1.act_scale = h->sx_in;
-  g1.w_scale = h->ws_in;
-  g1.out_scale = h->sx_mid;
-  GemmArgs g2{};
-  g2.offsets = h->rb.offsets;
-  g2.n_experts = h->n_local;
-  g2.n_tiles_n = static_cast<int>(h->d / kBN);
-  g2.num_kb = static_cast<int>(h->f * (fp8 ? 1 : 2) / kBKBytes);
-  g2.b_rows_per_expert = static_cast<int>(h->d);
-  g2.out = h->y;
-  g2.ldo = static_cast<int>(h->d);
-  g2.row_scale = h->row_w;
-  g2.act_scale = h->sx_mid;
-  g2.w_scale = h->ws_out;
-  const int v = h->gemm_ctas == 2 ? 1 : 0;
-  if (!fp8) {
-    if (v) {
-      launch_gemm<2, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
-    } else {
-      launch_gemm<1, EPI_SWIGLU, false, false>(h, h->mA1[v], h->mB1[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mA2[v], h->mB2[v], g2, st);
-    }
-  } else {
-    if (v) {
-      launch_gemm<2, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<2, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
-    } else {
-      launch_gemm<1, EPI_SWIGLU, true, true>(h, h->mA1q[v], h->mB1q[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<1, EPI_ROWSCALE, true, false>(h, h->mA2q[v], h->mB2q[v], g2, st);
-    }
-  }
+  run_gemms(h, h->rb.offsets, h->act, h->y, h->row_w, h->mA1, h->mA2, h->mA1q, h->mA2q, st);
   prof_mark(h, 4, st);
   if (out_f32)
     launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
@@ -465,9 +496,162 @@ void ensure_fp8_storage(cl_moe* h) {
   build_maps(h, true);
 }
 
+void ep_alloc(cl_moe* h) {
+  if (h->x_recv) return;
+  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  h->recv_cap = h->cap * h->K * R;
+  h->x_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
+  h->act_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->f);
+  h->y_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
+  h->ep_counts_dev = dalloc<int32_t>((size_t)R * h->N);
+  h->ep_off_dev = dalloc<int32_t>(h->n_local + 1);
+  CK(cudaMallocHost(&h->ep_counts_host, sizeof(int32_t) * R * h->N));
+  CK(cudaMallocHost(&h->ep_off_host, sizeof(int32_t) * (h->n_local + 1)));
+  for (int v = 0; v < 2; ++v) {
+    h->mA1e[v] = make_map(h->x_recv, false, h->d, h->recv_cap, 128);
+    h->mA2e[v] = make_map(h->act_recv, false, h->f, h->recv_cap, 128);
+  }
+}
+
+#define NCK(x)                                                                               \
+  do {                                                                                       \
+    int r_ = (x);                                                                            \
+    if (r_ != 0) throw RunErr(fmt("%s failed: %s", #x, NcclApi::get().GetErrorString(r_))); \
+  } while (0)
+
+// Expert-parallel forward (ep.cuh): route + plan + dispatch over all N experts, counts
+// all-gather, (expert, source)-piece exchange, local grouped GEMMs, reverse exchange, weighted
+// combine. Requires cl_moe_ep_init. bf16 only in this round.
+void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
+  if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
+  NcclApi& nc = NcclApi::get();
+  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  const int rank = h->cfg.ep_rank;
+  const int N = static_cast<int>(h->N), NL = h->n_local;
+  const int tpc = router_tokens_per_cta(N);
+  const int blocks = static_cast<int>((T + 7) / 8);
+  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
+                                                 h->inv, h->row_w, nullptr);
+  CK(cudaGetLastError());
+  prof_mark(h, 2, st);
+  // ---- counts exchange ----
+  NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)N, NcclApi::kInt32, h->comm, st));
+  CK(cudaMemcpyAsync(h->ep_counts_host, h->ep_counts_dev, sizeof(int32_t) * R * N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<int64_t> C((size_t)R * N), loc(NL + 1), piece((size_t)NL * R), my_off(N + 1);
+  for (size_t i = 0; i < C.size(); ++i) C[i] = h->ep_counts_host[i];
+  const int64_t total = ep_layout(C.data(), R, N, rank, loc.data(), piece.data());
+  if (total > h->recv_cap) throw RunErr("expert-parallel receive buffer overflow");
+  my_off[0] = 0;
+  for (int g = 0; g < N; ++g) my_off[g + 1] = my_off[g] + C[(size_t)rank * N + g];
+  for (int e = 0; e <= NL; ++e) h->ep_off_host[e] = static_cast<int32_t>(loc[e]);
+  CK(cudaMemcpyAsync(h->ep_off_dev, h->ep_off_host, sizeof(int32_t) * (NL + 1), cudaMemcpyHostToDevice, st));
+  const size_t row_b = static_cast<size_t>(h->d) * 2;
+  const uint8_t* xp = static_cast<const uint8_t*>(h->xperm);
+  // ---- dispatch exchange: piece (dest r, expert g) -> r's (local expert, source) slot ----
+  NCK(nc.GroupStart());
+  for (int r = 0; r < R; ++r)
+    for (int e = 0; e < NL; ++e) {
+      const int g = r * NL + e;
+      const int64_t n = C[(size_t)rank * N + g];
+      if (n) NCK(nc.Send(xp + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
+    }
+  for (int e = 0; e < NL; ++e)
+    for (int s = 0; s < R; ++s) {
+      const int64_t n = C[(size_t)s * N + rank * NL + e];
+      if (n)
+        NCK(nc.Recv(reinterpret_cast<uint8_t*>(h->x_recv) + piece[(size_t)e * R + s] * row_b, n * row_b,
+                    NcclApi::kUint8, s, h->comm, st));
+    }
+  NCK(nc.GroupEnd());
+  // ---- local experts ----
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st);
+  prof_mark(h, 4, st);
+  // ---- reverse exchange into this rank's permutation slots ----
+  NCK(nc.GroupStart());
+  for (int e = 0; e < NL; ++e)
+    for (int s = 0; s < R; ++s) {
+      const int64_t n = C[(size_t)s * N + rank * NL + e];
+      if (n)
+        NCK(nc.Send(reinterpret_cast<const uint8_t*>(h->y_recv) + piece[(size_t)e * R + s] * row_b, n * row_b,
+                    NcclApi::kUint8, s, h->comm, st));
+    }
+  for (int r = 0; r < R; ++r)
+    for (int e = 0; e < NL; ++e) {
+      const int g = r * NL + e;
+      const int64_t n = C[(size_t)rank * N + g];
+      if (n)
+        NCK(nc.Recv(reinterpret_cast<uint8_t*>(h->y) + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm,
+                    st));
+    }
+  NCK(nc.GroupEnd());
+  if (out_f32)
+    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
+                          h->rb.combine_w);
+  else
+    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                  h->rb.finite_flag, st, h->rb.combine_w);
+  CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
+  h->last_rows = T * h->K;
+}
+
 }  // namespace
 
 extern "C" {
+
+cl_status cl_moe_ep_unique_id(uint8_t* id_out) {
+  if (!id_out) return CL_ERR_CONFIG;
+  try {
+    NcclApi::UniqueId id;
+    if (NcclApi::get().GetUniqueId(&id) != 0) return CL_ERR_RUN;
+    std::memcpy(id_out, id.internal, 128);
+    return CL_OK;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "cl_moe_ep_unique_id: %s\n", e.what());
+    return CL_ERR_RUN;
+  }
+}
+
+cl_status cl_moe_ep_init(cl_moe* h, const uint8_t* id) {
+  return guarded(h, [&] {
+    if (!id) throw ConfigErr("id is null");
+    CK(cudaSetDevice(h->cfg.device));
+    const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+    NcclApi::UniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    if (h->comm) {
+      NcclApi::get().CommDestroy(h->comm);
+      h->comm = nullptr;
+    }
+    NCK(NcclApi::get().CommInitRank(&h->comm, R, uid, h->cfg.ep_rank));
+    ep_alloc(h);
+  });
+}
+
+cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
+                            void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    run_router(h, hidden, T, (cudaStream_t)stream);
+    run_ep(h, hidden, T, out, false, (cudaStream_t)stream);
+    export_decision(h, T, decision, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_ep_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank, int64_t* local_offsets,
+                           int64_t* recv_piece, int64_t* recv_total) {
+  if (!counts || !local_offsets || !recv_piece || R < 1 || N < R || N % R || rank < 0 || rank >= R)
+    return CL_ERR_CONFIG;
+  const int64_t t = ep_layout(counts, R, N, rank, local_offsets, recv_piece);
+  if (recv_total) *recv_total = t;
+  return CL_OK;
+}
+
 
 const char* cl_moe_version(void) { return "0.1.0-sm100a"; }
 

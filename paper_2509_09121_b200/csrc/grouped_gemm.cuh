@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
       } else {
-        float rs = valid ? args.row_scale[row] : 0.0f;
+        float rs = valid ? (args.row_scale ? args.row_scale[row] : 1.0f) : 0.0f;
         const float* ws = nullptr;
         if constexpr (kFp8) {
           rs *= args.act_scale[ti.e];

@@ -421,10 +421,12 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
 // order (rows of Y already carry the combine weight from the GEMM2 epilogue). Replaces
 // scatter_add_rows + add (proj/src/tensor.cpp:814-845, :248-262) with no intermediate copies.
 // kK is compile-time so all K x kU 16-byte loads of a lane are in flight together.
+// `wts` (nullable): multiply row k by wts[j*K+k] here (expert-parallel path, where the expert
+// side returns unweighted rows).
 template <typename OutT, int kK>
 __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __restrict__ y, const int32_t* __restrict__ inv,
                                                       int T, int d, OutT* __restrict__ out,
-                                                      int32_t* __restrict__ finite_flag) {
+                                                      int32_t* __restrict__ finite_flag, const float* __restrict__ wts) {
   constexpr int kU = kK <= 2 ? 4 : 2;
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -432,6 +434,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   const int4* src[kK];
 #pragma unroll
   for (int k = 0; k < kK; ++k) src[k] = reinterpret_cast<const int4*>(y + (size_t)inv[(size_t)j * kK + k] * d);
+  float wk[kK];
+#pragma unroll
+  for (int k = 0; k < kK; ++k) wk[k] = wts ? wts[(size_t)j * kK + k] : 1.0f;
   const int nvec = d / 8;
   bool fin = true;
   for (int v0 = lane; v0 < nvec; v0 += 32 * kU) {
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
       for (int k = 0; k < kK; ++k) {
         const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw[u][k]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(h[i]);
+        for (int i = 0; i < 8; ++i) acc[i] += wts ? wk[k] * __bfloat162float(h[i]) : __bfloat162float(h[i]);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) fin &= isfinite(acc[i]);
@@ -473,17 +478,17 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
 
 template <typename OutT>
 inline void launch_combine(const __nv_bfloat16* y, const int32_t* inv, int T, int d, int K, OutT* out, int32_t* flag,
-                           cudaStream_t st) {
+                           cudaStream_t st, const float* wts = nullptr) {
   const int blocks = (T + 7) / 8;
   switch (K) {
-    case 1: combine_kernel<OutT, 1><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 2: combine_kernel<OutT, 2><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 3: combine_kernel<OutT, 3><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 4: combine_kernel<OutT, 4><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 5: combine_kernel<OutT, 5><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 6: combine_kernel<OutT, 6><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    case 7: combine_kernel<OutT, 7><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
-    default: combine_kernel<OutT, 8><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag); break;
+    case 1: combine_kernel<OutT, 1><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 2: combine_kernel<OutT, 2><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 3: combine_kernel<OutT, 3><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 4: combine_kernel<OutT, 4><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 5: combine_kernel<OutT, 5><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 6: combine_kernel<OutT, 6><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    case 7: combine_kernel<OutT, 7><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
+    default: combine_kernel<OutT, 8><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
   }
 }
 

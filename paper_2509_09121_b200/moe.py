@@ -215,6 +215,26 @@ class MoELayer:
                     "fp8_scales")
         return a, b, wi, wo
 
+    # ---------------------------------------------------------------- expert parallelism
+    @staticmethod
+    def ep_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        rc = _lib.lib().cl_moe_ep_unique_id(buf)
+        if rc != _lib.CL_OK:
+            raise MoEError("cl_moe_ep_unique_id failed")
+        return bytes(buf)
+
+    def ep_init(self, uid: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self.L.cl_moe_ep_init(self.h, buf), "ep_init")
+
+    def ep_forward(self, hidden: torch.Tensor) -> torch.Tensor:
+        hidden = self._bf16(hidden)
+        out = torch.empty_like(hidden)
+        self._check(self.L.cl_moe_ep_forward(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), None,
+                                             _stream(self.device)), "ep_forward")
+        return out
+
     # ---------------------------------------------------------------- per-stage timing
     STAGES = ("router", "plan", "dispatch", "gemm1", "gemm2", "combine")
 
@@ -253,3 +273,18 @@ class MoELayer:
         return _lib.Decision(dec.logits.data_ptr(), dec.probs.data_ptr(), dec.topk_idx.data_ptr(),
                              dec.combine_weights.data_ptr(), dec.counts.data_ptr(), dec.agg_prob.data_ptr(),
                              dec.aux.data_ptr(), dec.z.data_ptr())
+
+
+def ep_layout(counts: np.ndarray, rank: int):
+    """Receive layout of `rank` from the all-gathered [R x N] count matrix (pure host, no GPU):
+    returns (local_offsets [N/R+1], recv_piece [N/R x R], total)."""
+    counts = np.ascontiguousarray(counts, np.int64)
+    r, n = counts.shape
+    nl = n // r
+    loc = np.empty(nl + 1, np.int64)
+    piece = np.empty(nl * r, np.int64)
+    tot = C.c_int64()
+    rc = _lib.lib().cl_moe_ep_layout(counts.ctypes.data, r, n, rank, loc.ctypes.data, piece.ctypes.data, C.byref(tot))
+    if rc != _lib.CL_OK:
+        raise MoEConfigError("ep_layout: bad arguments")
+    return loc, piece.reshape(nl, r), tot.value
