@@ -178,6 +178,8 @@ def run_ours(args, cfg):
     from paper_2509_09121_b200.moe import MoEConfig, MoELayer
 
     T, d, N, K, f = cfg["T"], cfg["d"], cfg["N"], cfg["K"], cfg["f"]
+    if args.tokens:
+        T = args.tokens
     if world > 1 and N % world:
         raise SystemExit(f"n_experts={N} is not divisible by {world} ranks")
     layer = MoELayer(MoEConfig(d_model=d, n_experts=N, top_k=K, d_ff=f, max_tokens=T, device=local_rank,
@@ -189,6 +191,10 @@ def run_ours(args, cfg):
         layer.ep_init(obj[0])
     x = layer.synthetic_tokens(T, SEED + rank)
     out = torch.empty_like(x)
+    if args.precision == "fp8":
+        # expert-aware FP8: calibrate on this batch (per-expert activation maxima), quantize weights
+        layer.calibrate(x)
+        layer.quantize_fp8()
     stream = torch.cuda.current_stream()
 
     def step():
@@ -260,6 +266,11 @@ def run_ours(args, cfg):
     comb_bytes = T * K * d * 2 + T * d * 2 + 8 * T * K
     disp_gbs = disp_bytes / (per["dispatch"] * 1e-3) / 1e9
     comb_gbs = comb_bytes / (per["combine"] * 1e-3) / 1e9
+    esz = 1 if args.precision == "fp8" else 2
+    nl = N // world
+    w_bytes = nl * 3 * d * f * esz  # every local expert touched (checked below)
+    g_ms = per["gemm1"] + per["gemm2"]
+    stream_gbs = w_bytes / (g_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
     if os.path.exists(tp):
@@ -269,16 +280,21 @@ def run_ours(args, cfg):
     if rank == 0:
         line = dict(
             metric=METRIC, value=value, unit="tokens/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype="bf16" if args.precision == "bf16" else "e4m3 (fp32 accumulate, bf16 activations in/out)",
             data="synthetic (device-generated reference-PRNG tokens and random-init weights)",
             config=dict(workload=cfg["workload"], T=T, d=d, n_experts=N, top_k=K, d_ff=f,
                         global_batch=T * world, parallelism=("ep%d (experts %d/rank, NCCL all-to-all)" % (world, N // world))
                         if world > 1 else "single",
                         gemm_ctas=args.gemm_ctas or 2, l2="inputs larger than L2 (x 134 MB, weights 5.6 GB); no flush"),
-            roofline=dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
-                          peak=peaks["bf16_sus"], unit="TFLOP/s", frac=g1_tf / peaks["bf16_sus"],
-                          frac_of_burst=g1_tf / peaks["bf16"], peak_kind=f"sustained ({peaks['src']})",
-                          traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"]),
+            roofline=(dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
+                           peak=peaks["bf16_sus"], unit="TFLOP/s", frac=g1_tf / peaks["bf16_sus"],
+                           frac_of_burst=g1_tf / peaks["bf16"], peak_kind=f"sustained ({peaks['src']})",
+                           traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
+                      if (args.precision == "bf16" and T * K >= 256 * nl * 4) else
+                      dict(bound="hbm", kernel="grouped GEMM1+GEMM2 weight streaming (tcgen05)",
+                           achieved=stream_gbs, peak=peaks["hbm"], unit="GB/s", frac=stream_gbs / peaks["hbm"],
+                           traffic=None, bytes_per_launch=w_bytes, ms_per_launch=g_ms)),
             stages=dict(
                 ms=per,
                 gemm2=dict(achieved=g2_tf, unit="TFLOP/s", frac=g2_tf / peaks["bf16_sus"]),
@@ -317,6 +333,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--gemm-ctas", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"])
+    ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per rank)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

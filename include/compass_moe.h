@@ -168,6 +168,18 @@ cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
 cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,
                                 float* w_out_scale);
 
+/* ---- Expert-FFN backward (the reference Tape closures of the layer, tensor.cpp:364-372,
+ * :318-321, :290-300, :411-418, :587-607, :801-809, :834-842). bf16, single GPU; d_ff % 256 == 0.
+ * cl_moe_forward_train = cl_moe_forward that also keeps the SwiGLU pre-activations and the
+ * unweighted expert outputs. cl_moe_backward(dOut) then returns, for that call:
+ *   d_hidden [T x d] bf16 (through dispatch), d_combine_w [T x K] fp32 (mul_rowwise backward),
+ *   dw_in [N_local][d][2f] fp32 and dw_out [N_local][f][d] fp32 (reference layouts, overwritten).
+ * The router backward (d probs -> d logits -> dW_r) is not part of this call. ---- */
+cl_status cl_moe_forward_train(cl_moe* h, const void* hidden, int64_t T, void* out,
+                               const cl_moe_decision* decision, void* stream);
+cl_status cl_moe_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_combine_w,
+                          float* dw_in, float* dw_out, void* stream);
+
 /* ---- Expert parallelism. One process per GPU; cfg.ep_size ranks, rank
  * cfg.ep_rank owns experts [rank*N/ep_size, (rank+1)*N/ep_size) (pass only those experts'
  * weights to cl_moe_create). Every rank routes its own tokens over all N experts; rows travel

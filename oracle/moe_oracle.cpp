@@ -418,6 +418,70 @@ int orc_expert_ffn_backward(const float* xe, std::int64_t m, std::int64_t d, std
   return 0;
 }
 
+// ---- MoE layer backward (the Tape replay of the moe_forward composition) --------------------
+// Given dOut [T x d]: per expert e with rows_e (ascending tokens) and weights w_e:
+//   scatter_add_rows bwd (tensor.cpp:834-842): dYw[r] = dOut[rows_e[r]]
+//   mul_rowwise bwd (tensor.cpp:587-607):      dY[r] = dYw[r] * w[r] (float);
+//                                              d_w[r] = (float) sum_c (double)dYw[r][c] * Y[r][c]
+//   expert FFN bwd (orc_expert_ffn_backward);  dW_in[e], dW_out[e]
+//   gather_rows bwd (tensor.cpp:801-809):      d_hidden[rows_e[r]] += dX[r]
+// Experts are replayed in reverse creation order like Tape::backward (tensor.cpp:142-150).
+// d_combine_w is indexed like topk_idx ([T][K]); dw_in [N][d][2f], dw_out [N][f][d].
+int orc_moe_backward(const float* x, std::int64_t T, std::int64_t d, std::int64_t N, std::int64_t K, std::int64_t f,
+                     const float* w_in, const float* w_out, const std::int64_t* idx, const float* w,
+                     const float* d_out, float* d_hidden, float* d_combine_w, float* dw_in, float* dw_out, int jobs) {
+  std::vector<std::vector<std::int64_t>> rows(static_cast<std::size_t>(N)), slot(static_cast<std::size_t>(N));
+  for (std::int64_t j = 0; j < T; ++j)
+    for (std::int64_t k = 0; k < K; ++k) {
+      const std::int64_t e = idx[j * K + k];
+      if (e < 0 || e >= N) return fail("moe_backward: expert index out of range");
+      rows[static_cast<std::size_t>(e)].push_back(j);
+      slot[static_cast<std::size_t>(e)].push_back(j * K + k);
+    }
+  std::vector<std::vector<float>> dx(static_cast<std::size_t>(N));
+  run_parallel(N, jobs, [&](std::int64_t e) {
+    const auto& re = rows[static_cast<std::size_t>(e)];
+    const auto& se = slot[static_cast<std::size_t>(e)];
+    const std::int64_t m = static_cast<std::int64_t>(re.size());
+    float* gwi = dw_in + e * d * 2 * f;
+    float* gwo = dw_out + e * f * d;
+    if (m == 0) {
+      std::memset(gwi, 0, sizeof(float) * d * 2 * f);
+      std::memset(gwo, 0, sizeof(float) * f * d);
+      return;
+    }
+    std::vector<float> xe(static_cast<std::size_t>(m * d)), y(static_cast<std::size_t>(m * d)),
+        dy(static_cast<std::size_t>(m * d));
+    for (std::int64_t r = 0; r < m; ++r)
+      std::memcpy(&xe[static_cast<std::size_t>(r * d)], x + re[static_cast<std::size_t>(r)] * d, d * sizeof(float));
+    orc_expert_ffn(xe.data(), m, d, f, w_in + e * d * 2 * f, w_out + e * f * d, nullptr, y.data());
+    for (std::int64_t r = 0; r < m; ++r) {
+      const float* g = d_out + re[static_cast<std::size_t>(r)] * d;
+      const float wr = w[se[static_cast<std::size_t>(r)]];
+      double acc = 0.0;
+      for (std::int64_t c = 0; c < d; ++c) {
+        dy[static_cast<std::size_t>(r * d + c)] = g[c] * wr;
+        acc += static_cast<double>(g[c]) * y[static_cast<std::size_t>(r * d + c)];
+      }
+      d_combine_w[se[static_cast<std::size_t>(r)]] = static_cast<float>(acc);
+    }
+    auto& dxe = dx[static_cast<std::size_t>(e)];
+    dxe.resize(static_cast<std::size_t>(m * d));
+    orc_expert_ffn_backward(xe.data(), m, d, f, w_in + e * d * 2 * f, w_out + e * f * d, dy.data(), dxe.data(), gwi,
+                            gwo);
+  });
+  std::memset(d_hidden, 0, sizeof(float) * T * d);
+  for (std::int64_t e = N - 1; e >= 0; --e) {
+    const auto& re = rows[static_cast<std::size_t>(e)];
+    for (std::size_t r = 0; r < re.size(); ++r) {
+      float* o = d_hidden + re[r] * d;
+      const float* s = dx[static_cast<std::size_t>(e)].data() + r * static_cast<std::size_t>(d);
+      for (std::int64_t c = 0; c < d; ++c) o[c] += s[c];
+    }
+  }
+  return 0;
+}
+
 // ---- FP8 E4M3 quantize-dequantize -----------------------------------------
 // q = x/scale in float; RNE onto the enumerated E4M3 grid (ties to the even code), |q| > 448
 // clamps to +-448; result q_hat * scale in float. Non-finite input is an error.

@@ -62,6 +62,8 @@ class Oracle:
         getattr(L, p + "top_k").argtypes = [_f32p, _i64, _i64, _i64p, _f32p]
         getattr(L, p + "moe_forward").argtypes = [_f32p, _i64, _i64, _i64, _i64, _i64, _f32p, _f32p, _i64p, _f32p, _f32p, C.c_int]
         getattr(L, p + "expert_ffn_backward").argtypes = [_f32p, _i64, _i64, _i64, _f32p, _f32p, _f32p, _f32p, _f32p, _f32p]
+        getattr(L, p + "moe_backward").argtypes = ([_f32p, _i64, _i64, _i64, _i64, _i64, _f32p, _f32p, _i64p, _f32p, _f32p,
+                                                     _f32p, _f32p, _f32p, _f32p] + ([C.c_int] if kind == "port" else []))
         if kind == "port":
             L.orc_split_seed.restype = C.c_uint64
             L.orc_split_seed.argtypes = [C.c_uint64, C.c_uint64]
@@ -138,6 +140,24 @@ class Oracle:
         self._call("expert_ffn_backward", xe, m, d, f, np.ascontiguousarray(w_in_e, np.float32),
                    np.ascontiguousarray(w_out_e, np.float32), np.ascontiguousarray(dy, np.float32), dx, dwi, dwo)
         return dx, dwi, dwo
+
+    def moe_backward(self, x, w_in, w_out, idx, w, d_out, jobs: int = 1):
+        """Layer backward: returns (d_hidden [T x d], d_combine_w [T x K], dw_in [N][d][2f], dw_out [N][f][d])."""
+        x = np.ascontiguousarray(x, np.float32)
+        t, d = x.shape
+        n, _, f2 = w_in.shape
+        k = idx.shape[1]
+        dh = np.empty((t, d), np.float32)
+        dcw = np.empty((t, k), np.float32)
+        dwi = np.empty((n, d, f2), np.float32)
+        dwo = np.empty((n, f2 // 2, d), np.float32)
+        args = [x, t, d, n, k, f2 // 2, np.ascontiguousarray(w_in, np.float32), np.ascontiguousarray(w_out, np.float32),
+                np.ascontiguousarray(idx, np.int64), np.ascontiguousarray(w, np.float32),
+                np.ascontiguousarray(d_out, np.float32), dh, dcw, dwi, dwo]
+        if self.kind == "port":
+            args.append(jobs)
+        self._call("moe_backward", *args)
+        return dh, dcw, dwi, dwo
 
     # ---- port-only helpers ----
     def expert_ffn(self, xe, w_in_e, w_out_e):

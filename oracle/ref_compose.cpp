@@ -150,6 +150,54 @@ int ref_expert_ffn_backward(const float* xe, std::int64_t m, std::int64_t d, std
   });
 }
 
+// Full MoE layer backward through the reference Tape: forward composed as in ref_moe_forward
+// (sequential over experts so the tape is single-threaded), loss = sum(out * stop(dOut)), with
+// x, every expert's W_in / W_out and the combine-weight columns as leaves.
+int ref_moe_backward(const float* x, std::int64_t T, std::int64_t d, std::int64_t N, std::int64_t K, std::int64_t f,
+                     const float* w_in, const float* w_out, const std::int64_t* idx, const float* w,
+                     const float* d_out, float* d_hidden, float* d_combine_w, float* dw_in, float* dw_out) {
+  return guarded([&] {
+    Tensor xt = Tensor::param({T, d}, vec(x, T * d));
+    std::vector<std::vector<std::int64_t>> rows(static_cast<std::size_t>(N)), slot(static_cast<std::size_t>(N));
+    std::vector<std::vector<float>> wcol(static_cast<std::size_t>(N));
+    for (std::int64_t j = 0; j < T; ++j)
+      for (std::int64_t k = 0; k < K; ++k) {
+        rows[static_cast<std::size_t>(idx[j * K + k])].push_back(j);
+        slot[static_cast<std::size_t>(idx[j * K + k])].push_back(j * K + k);
+        wcol[static_cast<std::size_t>(idx[j * K + k])].push_back(w[j * K + k]);
+      }
+    std::vector<Tensor> win(static_cast<std::size_t>(N)), wout(static_cast<std::size_t>(N)), wc(static_cast<std::size_t>(N));
+    Tape tape;
+    Tape::Scope scope(tape);
+    Tensor acc = Tensor::zeros({T, d});
+    for (std::int64_t e = 0; e < N; ++e) {
+      win[static_cast<std::size_t>(e)] = Tensor::param({d, 2 * f}, vec(w_in + e * d * 2 * f, d * 2 * f));
+      wout[static_cast<std::size_t>(e)] = Tensor::param({f, d}, vec(w_out + e * f * d, f * d));
+      const auto& re = rows[static_cast<std::size_t>(e)];
+      if (re.empty()) continue;
+      const auto m = static_cast<std::int64_t>(re.size());
+      wc[static_cast<std::size_t>(e)] = Tensor::param({m, 1}, wcol[static_cast<std::size_t>(e)]);
+      Tensor xe = ops::gather_rows(xt, re);
+      Tensor h = ops::matmul(xe, win[static_cast<std::size_t>(e)]);
+      Tensor a = ops::mul(ops::silu(ops::slice_cols(h, 0, f)), ops::slice_cols(h, f, 2 * f));
+      Tensor y = ops::matmul(a, wout[static_cast<std::size_t>(e)]);
+      Tensor yw = ops::mul_rowwise(y, wc[static_cast<std::size_t>(e)]);
+      acc = ops::add(acc, ops::scatter_add_rows(T, yw, re));
+    }
+    Tensor g = Tensor::from_values({T, d}, vec(d_out, T * d));
+    tape.backward(ops::sum_all(ops::mul(acc, ops::stop_grad(g))));
+    std::memcpy(d_hidden, xt.grad().data(), sizeof(float) * T * d);
+    for (std::int64_t e = 0; e < N; ++e) {
+      std::memcpy(dw_in + e * d * 2 * f, win[static_cast<std::size_t>(e)].grad().data(), sizeof(float) * d * 2 * f);
+      std::memcpy(dw_out + e * f * d, wout[static_cast<std::size_t>(e)].grad().data(), sizeof(float) * f * d);
+      const auto& se = slot[static_cast<std::size_t>(e)];
+      if (se.empty()) continue;
+      const auto& gw = wc[static_cast<std::size_t>(e)].grad();
+      for (std::size_t r = 0; r < se.size(); ++r) d_combine_w[se[r]] = gw[r];
+    }
+  });
+}
+
 // The reference's own finite-difference gradient suite (gradcheck.cpp:610-656); returns the
 // number of failing ops (0 = all pass) and the number of ops checked in *n_ops.
 int ref_gradcheck(std::uint64_t seed, int cases, double tol, int* n_ops) {

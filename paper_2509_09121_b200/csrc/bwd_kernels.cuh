@@ -1,0 +1,134 @@
+// Expert-FFN backward helpers (the Tape closures of the reference composition):
+//  * combine backward  = scatter_add_rows bwd (tensor.cpp:834-842) + mul_rowwise bwd (:587-607):
+//      dY[r] = w[s] * dOut[j],  d_w[s] = <dOut[j], Y[r]>   (s = perm[r], j = s / K)
+//  * padded transposes feeding the variable-K weight-gradient GEMMs (dW = Lhs^T Rhs over the
+//    rows of one expert; each expert's rows start at a 64-aligned column so a k-block never
+//    straddles two experts; padding columns are zero);
+//  * reference-layout bf16 weight copies (W_in [d][2f], W_out [f][d]) derived on device from the
+//    packed forward layouts — the K-major B operands of the two dgrad GEMMs.
+#pragma once
+#include "ptx.cuh"
+
+namespace cmoe {
+
+// One warp per permuted row.
+__global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* __restrict__ d_out,
+                                                          const __nv_bfloat16* __restrict__ y,
+                                                          const int32_t* __restrict__ perm,
+                                                          const float* __restrict__ cw, int rows, int d, int K,
+                                                          __nv_bfloat16* __restrict__ dy, float* __restrict__ d_cw) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const int s = perm[r];
+  const int j = s / K;
+  const float w = cw[s];
+  const int4* g = reinterpret_cast<const int4*>(d_out + (size_t)j * d);
+  const int4* yr = reinterpret_cast<const int4*>(y + (size_t)r * d);
+  int4* o = reinterpret_cast<int4*>(dy + (size_t)r * d);
+  float acc = 0.0f;
+  for (int v = lane; v < d / 8; v += 32) {
+    const int4 gv = ld_nc_v4(g + v);
+    const int4 yv = ld_nc_v4(yr + v);
+    const __nv_bfloat16* gh = reinterpret_cast<const __nv_bfloat16*>(&gv);
+    const __nv_bfloat16* yh = reinterpret_cast<const __nv_bfloat16*>(&yv);
+    float f[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float gg = __bfloat162float(gh[i]);
+      acc = fmaf(gg, __bfloat162float(yh[i]), acc);
+      f[i] = w * gg;
+    }
+    int4 ov;
+    ov.x = pack_bf16(f[0], f[1]);
+    ov.y = pack_bf16(f[2], f[3]);
+    ov.z = pack_bf16(f[4], f[5]);
+    ov.w = pack_bf16(f[6], f[7]);
+    st_na_v4(o + v, ov);
+  }
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) d_cw[s] = acc;
+}
+
+// poff[e] = 64-aligned first padded row of expert e; kb_off[e] = poff[e] / 64 (k-blocks of the
+// bf16 K-major transposes). One thread.
+__global__ void pad_plan_kernel(const int32_t* __restrict__ offsets, int n, int32_t* __restrict__ poff,
+                                int32_t* __restrict__ kb_off) {
+  if (threadIdx.x || blockIdx.x) return;
+  int p = 0;
+  for (int e = 0; e < n; ++e) {
+    poff[e] = p;
+    kb_off[e] = p / 64;
+    p += (offsets[e + 1] - offsets[e] + 63) / 64 * 64;
+  }
+  poff[n] = p;
+  kb_off[n] = p / 64;
+}
+
+// dst[c][p] = src[offsets[e] + p - poff[e]][c] for p inside expert e's padded range, 0 in the
+// padding. src is [rows][C] bf16 row-major, dst is [C][Rp_cap]. 64 x 64 tiles through smem.
+__global__ void __launch_bounds__(256) transpose_pad_kernel(const __nv_bfloat16* __restrict__ src, int C,
+                                                            const int32_t* __restrict__ offsets,
+                                                            const int32_t* __restrict__ poff, int n,
+                                                            __nv_bfloat16* __restrict__ dst, int64_t rp_cap) {
+  __shared__ __nv_bfloat16 tile[64][66];
+  const int c0 = blockIdx.x * 64;
+  const int p0 = blockIdx.y * 64;
+  if (p0 >= poff[n]) return;
+  int e = 0;
+  while (p0 >= poff[e + 1]) ++e;
+  const int cnt = offsets[e + 1] - offsets[e];
+  const int base_row = offsets[e] + (p0 - poff[e]);
+  const int valid_p = min(64, cnt - (p0 - poff[e]));  // may be <= 0 in a pure padding block
+  // load: 64 rows (p) x 64 cols (c); thread handles 2 consecutive columns
+  for (int i = threadIdx.x; i < 64 * 32; i += 256) {
+    const int pr = i / 32, cc = (i % 32) * 2;
+    __nv_bfloat162 v = __floats2bfloat162_rn(0.0f, 0.0f);
+    if (pr < valid_p && c0 + cc < C)
+      v = *reinterpret_cast<const __nv_bfloat162*>(src + (size_t)(base_row + pr) * C + c0 + cc);
+    tile[pr][cc] = v.x;
+    tile[pr][cc + 1] = v.y;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 64 * 32; i += 256) {
+    const int cr = i / 32, pp = (i % 32) * 2;
+    if (c0 + cr < C) {
+      __nv_bfloat162 v;
+      v.x = tile[pp][cr];
+      v.y = tile[pp + 1][cr];
+      *reinterpret_cast<__nv_bfloat162*>(dst + (size_t)(c0 + cr) * rp_cap + p0 + pp) = v;
+    }
+  }
+}
+
+// dst[i][j] = src[rowmap(j)][i]: src [rows_src][cols_src] bf16 -> dst [cols_src][rows_src].
+// kWinMap: rowmap(c) = packed W_in row of reference column c (inverse of win_col_of_packed_row).
+template <bool kWinMap>
+__global__ void __launch_bounds__(256) transpose_weight_kernel(const __nv_bfloat16* __restrict__ src, int rows_src,
+                                                               int cols_src, int f, __nv_bfloat16* __restrict__ dst) {
+  __shared__ __nv_bfloat16 tile[32][34];
+  const int j0 = blockIdx.x * 32;  // dst column block = source (mapped) row block
+  const int i0 = blockIdx.y * 32;  // dst row block = source column block
+  for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+    const int jj = t / 32, ii = t % 32;
+    const int j = j0 + jj;
+    __nv_bfloat16 v = __float2bfloat16_rn(0.0f);
+    if (j < rows_src && i0 + ii < cols_src) {
+      int r = j;
+      if constexpr (kWinMap) {
+        const int up = j >= f;
+        const int c = up ? j - f : j;
+        r = (c / 128) * 256 + (up ? 128 : 0) + c % 128;
+      }
+      v = src[(size_t)r * cols_src + i0 + ii];
+    }
+    tile[jj][ii] = v;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 32 * 32; t += 256) {
+    const int ii = t / 32, jj = t % 32;
+    if (i0 + ii < cols_src && j0 + jj < rows_src) dst[(size_t)(i0 + ii) * rows_src + j0 + jj] = tile[jj][ii];
+  }
+}
+
+}  // namespace cmoe

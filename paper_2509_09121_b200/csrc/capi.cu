@@ -21,6 +21,7 @@
 #include "moe_kernels.cuh"
 #include "synth_pack.cuh"
 #include "ep.cuh"
+#include "bwd_kernels.cuh"
 
 using namespace cmoe;
 
@@ -99,6 +100,7 @@ struct cl_moe {
   int64_t d = 0, N = 0, K = 0, f = 0, cap = 0;
   int n_local = 0, e0 = 0;
   int gemm_ctas = 2;
+  bool gemm_auto = true;               // pick cta_group per call from the rows per expert
   int num_sms = 148;
   int precision = CL_MOE_BF16;
   std::string last_error;
@@ -140,6 +142,8 @@ struct cl_moe {
   cudaStream_t own_stream = nullptr;   // compute stream of the host-buffer path
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   int64_t last_rows = 0;
+  int tpc_cur = 32;                    // router tile (tokens) of the last routing call
+  int64_t last_tokens = 0;             // T of the current call
 
   // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
   bool prof = false;
@@ -159,6 +163,21 @@ struct cl_moe {
   int32_t* ep_off_host = nullptr;
   CUtensorMap mA1e[2], mA2e[2];
 
+  // training (expert-FFN backward)
+  bool train_ready = false;
+  int64_t train_T = 0;                  // T of the last cl_moe_forward_train
+  int64_t rp_cap = 0;                   // padded-row capacity of the transposes
+  __nv_bfloat16* win_ref = nullptr;     // [NL][d][2f] reference layout (dgrad-2 B operand)
+  __nv_bfloat16* wout_ref = nullptr;    // [NL][f][d]  reference layout (dgrad-1 B operand)
+  __nv_bfloat16* Hbuf = nullptr;        // [cap*K][2f] pre-activations [G | U]
+  __nv_bfloat16* dYbuf = nullptr;       // [cap*K][d]
+  __nv_bfloat16* dHbuf = nullptr;       // [cap*K][2f]
+  __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
+  __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;  // [C][rp_cap]
+  int32_t* poff = nullptr;              // [NL+1]
+  int32_t* kb_off = nullptr;            // [NL+1]
+  CUtensorMap mAdg1[2], mBdg1[2], mAdg2[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
+
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
   bool maps_q = false;
@@ -172,7 +191,9 @@ struct cl_moe {
                     rb.counts, rb.offsets, rb.agg_prob, rb.losses, rb.finite_flag};
     for (void* p : ptrs)
       if (p) cudaFree(p);
-    for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev})
+    for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
+                    (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
+                    (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off})
       if (p) cudaFree(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
@@ -273,6 +294,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaGetDeviceProperties(&prop, c->device));
   if (prop.major != 10) throw RunErr(fmt("device %d is sm_%d%d; this library is built for sm_100a only", c->device, prop.major, prop.minor));
   h->num_sms = prop.multiProcessorCount;
+  h->gemm_auto = c->gemm_ctas == 0;
   h->gemm_ctas = c->gemm_ctas == 0 ? 2 : c->gemm_ctas;
   CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
@@ -284,7 +306,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   }
 
   const int64_t rows = h->cap * h->K;
-  const int tpc = router_tokens_per_cta(static_cast<int>(h->N));
+  const int tpc = router_tokens_per_cta(static_cast<int>(h->N), 32);  // smallest tile of any variant
   h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
   RouteBufs& rb = h->rb;
   rb.logits = dalloc<float>(h->cap * h->N);
@@ -312,7 +334,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
 
   h->wr = dalloc<float>(h->d * h->N);
   h->wr64 = dalloc<double>(h->d * ((h->N + 3) / 4 * 4));
-  CK(cudaFuncSetAttribute(router_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);
@@ -325,13 +348,17 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU_BWD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU_BWD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_WGRAD, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
+  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_WGRAD, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
 }
 
-template <int G, int EPI, bool F8, bool OF8>
+template <int G, int EPI, bool F8, bool OF8, bool WG = false>
 void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((h->num_sms / G) * G);
@@ -345,7 +372,7 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8>, a, b, args));
+  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG>, a, b, args));
 }
 
 // route_tokens on device: K1 + K2.
@@ -353,12 +380,20 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   if (T < 1) throw RunErr("route_tokens: B must be >= 1");
   if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
   const int N = static_cast<int>(h->N);
-  const int tpc = router_tokens_per_cta(N);
+  // small batches: 32-thread CTAs with an 8-deep prefetch ring (latency); large: 128-thread CTAs
+  const bool small = (T + router_tokens_per_cta(N, 128) - 1) / router_tokens_per_cta(N, 128) < 2 * h->num_sms &&
+                     router_smem_bytes(N, 32, 8) <= 220 * 1024;
+  const int tpc = router_tokens_per_cta(N, small ? 32 : 128);
+  h->tpc_cur = tpc;
+  h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
-  const size_t smem = router_smem_bytes(N);
   prof_begin(h, st);
-  router_kernel<<<n_tiles, kRouterThreads, smem, st>>>(static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T,
-                                                       (int)h->d, N, (int)h->K, h->rb);
+  if (small)
+    router_kernel<32, 8><<<n_tiles, 32, router_smem_bytes(N, 32, 8), st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else
+    router_kernel<128, 3><<<n_tiles, 128, router_smem_bytes(N, 128, 3), st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
   plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
@@ -370,7 +405,9 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
   if (T < 1) throw RunErr("moe_forward: B must be >= 1");
   if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
   const int N = static_cast<int>(h->N);
-  const int tpc = router_tokens_per_cta(N);
+  const int tpc = router_tokens_per_cta(N, 128);
+  h->tpc_cur = tpc;
+  h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   CK(cudaMemcpyAsync(h->rb.topk_idx, idx, sizeof(int32_t) * T * h->K, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemcpyAsync(h->rb.combine_w, w, sizeof(float) * T * h->K, cudaMemcpyDeviceToDevice, st));
@@ -386,10 +423,16 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
 // GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
 void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
-               cudaStream_t st) {
+               cudaStream_t st, __nv_bfloat16* h_save = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
+  if (h->gemm_auto) {
+    // M=256 CTA-pair tiles pay off only when experts have enough rows; small batches (decode)
+    // stream weights and are better served by M=128 tiles (less A over-fetch per B byte).
+    const int64_t rows_per_expert = h->last_tokens * h->K * (h->cfg.ep_size > 1 ? h->cfg.ep_size : 1) / h->n_local;
+    h->gemm_ctas = rows_per_expert >= 1024 ? 2 : 1;
+  }
   g1.n_experts = h->n_local;
   g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
   g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
@@ -399,6 +442,8 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g1.act_scale = h->sx_in;
   g1.w_scale = h->ws_in;
   g1.out_scale = h->sx_mid;
+  g1.aux = h_save;
+  g1.ffn = static_cast<int>(h->f);
   GemmArgs g2{};
   g2.offsets = offsets;
   g2.n_experts = h->n_local;
@@ -443,7 +488,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
     return;
   }
   const int N = static_cast<int>(h->N);
-  const int tpc = router_tokens_per_cta(N);
+  const int tpc = h->tpc_cur;
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   const int blocks = static_cast<int>((T + 7) / 8);
   if (fp8)
@@ -529,7 +574,7 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
   const int rank = h->cfg.ep_rank;
   const int N = static_cast<int>(h->N), NL = h->n_local;
-  const int tpc = router_tokens_per_cta(N);
+  const int tpc = h->tpc_cur;
   const int blocks = static_cast<int>((T + 7) / 8);
   dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
@@ -599,6 +644,151 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   h->last_rows = T * h->K;
 }
 
+void ensure_training(cl_moe* h) {
+  if (h->train_ready) return;
+  if (h->f % 256) throw ConfigErr("training needs d_ff to be a multiple of 256");
+  if (h->cfg.ep_size > 1) throw ConfigErr("expert-parallel backward is not supported yet");
+  const int64_t rows = h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
+  h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
+  h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
+  h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
+  h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
+  h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
+  h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
+  h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
+  h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
+  h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
+  h->dYT = dalloc<__nv_bfloat16>(d * h->rp_cap);
+  h->dHT = dalloc<__nv_bfloat16>(2 * f * h->rp_cap);
+  h->poff = dalloc<int32_t>(NL + 1);
+  h->kb_off = dalloc<int32_t>(NL + 1);
+  for (int e = 0; e < NL; ++e) {
+    transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
+        h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, h->win_ref + (size_t)e * d * 2 * f);
+    transpose_weight_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)(f / 32)), 256>>>(
+        h->wout + (size_t)e * d * f, (int)d, (int)f, (int)f, h->wout_ref + (size_t)e * f * d);
+  }
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  for (int v = 0; v < 2; ++v) {
+    const uint32_t brow = v == 0 ? 256 : 128;
+    h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
+    h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
+    h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
+    h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
+    h->mAwo[v] = make_map(h->AT, false, h->rp_cap, f, 128);
+    h->mBwo[v] = make_map(h->dYT, false, h->rp_cap, d, brow);
+    h->mAwi[v] = make_map(h->XT, false, h->rp_cap, d, 128);
+    h->mBwi[v] = make_map(h->dHT, false, h->rp_cap, 2 * f, brow);
+  }
+  h->train_ready = true;
+}
+
+// Training-mode forward: H = [G | U] kept, Y kept unweighted, combine weights applied in the
+// combine (fp32) so the backward can form d(combine_w) = <dOut, Y>.
+void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStream_t st) {
+  if (h->precision != CL_MOE_BF16) throw ConfigErr("training runs in bf16");
+  ensure_training(h);
+  const int N = static_cast<int>(h->N);
+  const int tpc = h->tpc_cur;
+  const int blocks = static_cast<int>((T + 7) / 8);
+  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
+                                                 h->inv, h->row_w, nullptr);
+  CK(cudaGetLastError());
+  prof_mark(h, 2, st);
+  run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf);
+  prof_mark(h, 4, st);
+  launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                h->rb.finite_flag, st, h->rb.combine_w);
+  CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
+  h->last_rows = T * h->K;
+  h->train_T = T;
+}
+
+// Expert-FFN backward of the last training forward.
+void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, float* dw_in, float* dw_out,
+                  cudaStream_t st) {
+  if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
+  const int64_t T = h->train_T, rows = T * h->K, d = h->d, f = h->f;
+  const int NL = h->n_local;
+  // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
+  combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_out), h->y, h->perm,
+                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K, h->dYbuf,
+                                                           d_cw);
+  CK(cudaGetLastError());
+  const int v = (h->gemm_auto ? (h->last_tokens * h->K / NL >= 1024) : h->gemm_ctas == 2) ? 1 : 0;
+  // 2. dA = dY W_out^T fused with the SwiGLU backward -> dH
+  GemmArgs a1{};
+  a1.offsets = h->rb.offsets;
+  a1.n_experts = NL;
+  a1.n_tiles_n = static_cast<int>(f / kBN);
+  a1.num_kb = static_cast<int>(d * 2 / kBKBytes);
+  a1.b_rows_per_expert = static_cast<int>(f);
+  a1.out = h->dHbuf;
+  a1.aux = h->Hbuf;
+  a1.ffn = static_cast<int>(f);
+  // 3. dX = dH W_in^T
+  GemmArgs a2{};
+  a2.offsets = h->rb.offsets;
+  a2.n_experts = NL;
+  a2.n_tiles_n = static_cast<int>(d / kBN);
+  a2.num_kb = static_cast<int>(2 * f * 2 / kBKBytes);
+  a2.b_rows_per_expert = static_cast<int>(d);
+  a2.out = h->dXbuf;
+  a2.ldo = static_cast<int>(d);
+  if (v) {
+    launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
+  } else {
+    launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
+  }
+  // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]
+  launch_combine<__nv_bfloat16>(h->dXbuf, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
+                                h->rb.finite_flag, st);
+  CK(cudaGetLastError());
+  // 5. weight gradients over each expert's rows (variable K): padded K-major transposes, then
+  //    dW_out[e] = A_e^T dY_e ([f x d]) and dW_in[e] = X_e^T dH_e ([d x 2f]), fp32.
+  pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, NL, h->poff, h->kb_off);
+  const unsigned pb = static_cast<unsigned>(h->rp_cap / 64);
+  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)d,
+                                                                     h->rb.offsets, h->poff, NL, h->XT, h->rp_cap);
+  transpose_pad_kernel<<<dim3((unsigned)(f / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)f,
+                                                                     h->rb.offsets, h->poff, NL, h->AT, h->rp_cap);
+  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, h->rb.offsets, h->poff, NL,
+                                                                     h->dYT, h->rp_cap);
+  transpose_pad_kernel<<<dim3((unsigned)(2 * f / 64), pb), 256, 0, st>>>(h->dHbuf, (int)(2 * f), h->rb.offsets,
+                                                                         h->poff, NL, h->dHT, h->rp_cap);
+  CK(cudaGetLastError());
+  const int gw = (f % 256 == 0) ? 2 : 1;
+  GemmArgs wo{};
+  wo.n_experts = NL;
+  wo.kb_off = h->kb_off;
+  wo.m_tiles = static_cast<int>(f / (128 * gw));
+  wo.n_tiles_n = static_cast<int>(d / kBN);
+  wo.out = dw_out;
+  wo.ldo = static_cast<int>(d);
+  wo.out_estride = f * d;
+  GemmArgs wi{};
+  wi.n_experts = NL;
+  wi.kb_off = h->kb_off;
+  wi.m_tiles = static_cast<int>(d / (128 * gw));
+  wi.n_tiles_n = static_cast<int>(2 * f / kBN);
+  wi.out = dw_in;
+  wi.ldo = static_cast<int>(2 * f);
+  wi.out_estride = d * 2 * f;
+  if (gw == 2) {
+    launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwo[1], h->mBwo[1], wo, st);
+    launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwi[1], h->mBwi[1], wi, st);
+  } else {
+    launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwo[0], h->mBwo[0], wo, st);
+    launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwi[0], h->mBwi[0], wi, st);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -640,6 +830,27 @@ cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
     run_router(h, hidden, T, (cudaStream_t)stream);
     run_ep(h, hidden, T, out, false, (cudaStream_t)stream);
     export_decision(h, T, decision, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_forward_train(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
+                               void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    ensure_training(h);
+    run_router(h, hidden, T, (cudaStream_t)stream);
+    run_forward_train(h, hidden, T, out, (cudaStream_t)stream);
+    export_decision(h, T, decision, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_combine_w, float* dw_in, float* dw_out,
+                          void* stream) {
+  return guarded(h, [&] {
+    if (!d_out || !d_hidden || !d_combine_w || !dw_in || !dw_out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    run_backward(h, d_out, d_hidden, d_combine_w, dw_in, dw_out, (cudaStream_t)stream);
   });
 }
 

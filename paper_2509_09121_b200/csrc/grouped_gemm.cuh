@@ -1,16 +1,22 @@
-// Grouped (per-expert) GEMM on the 5th-generation tensor cores for the MoE expert FFN.
+// Grouped (per-expert) GEMM on the 5th-generation tensor cores for the MoE expert FFN, forward
+// and backward.
 //
-//   GEMM1 (EPI_SWIGLU):   A_act[r, :] = silu(X[r,:] W_gate[e]) * (X[r,:] W_up[e])      (bf16 or e4m3 out)
-//   GEMM2 (EPI_ROWSCALE): Y[r, :]     = w[r] * (A_act[r,:] W_out[e])                    (bf16 out)
+// Row-grouped modes (M = the rows of one expert segment, K fixed):
+//   EPI_SWIGLU       A_act[r,:] = silu(X[r,:] W_gate[e]) * (X[r,:] W_up[e])   (bf16 or e4m3 out;
+//                    training mode also stores the pre-activations H = [G | U], bf16)
+//   EPI_ROWSCALE     Y[r,:] = w[r] * (A_act[r,:] W_out[e])                      (bf16; w optional)
+//   EPI_SWIGLU_BWD   dA = dY[r,:] W_out[e]^T, fused with the SwiGLU backward:
+//                    dH[r, c] = dA*U*silu'(G), dH[r, f+c] = dA*silu(G)           (bf16)
+// K-grouped mode (kWgrad; M, N = weight dims, K = the rows of expert e, variable):
+//   EPI_WGRAD        dW[e] = Lhs_e^T Rhs_e accumulated over the expert's rows    (fp32)
 //
-// Rows r of the permuted activation matrix are grouped by expert (offsets[e] .. offsets[e+1]);
-// expert e multiplies against its own weight block. Replaces the per-expert ops::matmul +
-// slice_cols + silu + mul (+ mul_rowwise) chain of the reference composition
-// (proj/src/tensor.cpp:350-375, :398-420, :315-322, :283-303, :572-610).
+// Replaces the per-expert ops::matmul + slice_cols + silu + mul (+ mul_rowwise) chain of the
+// reference composition and its Tape backward closures (proj/src/tensor.cpp:350-375 incl. the
+// gemm_nt / gemm_tn closures :364-372, :398-420, :315-322, :283-303, :572-610).
 //
 // Design (sm_100a):
 //  * persistent kernel, one CTA (or CTA pair) per SM, static round-robin over output tiles in
-//    (expert, n-block, m-block) order so CTAs running together share the weight n-block in L2;
+//    (expert, n-block, m-block) order so CTAs running together share the B n-block in L2;
 //  * warp-specialised: warp 0 = TMA producer, warp 1 = tcgen05.mma issuer (one elected thread),
 //    warp 2 = TMEM allocator, warps 4-7 = epilogue (TMEM -> registers -> global);
 //  * operands staged by TMA into 128-byte-swizzled K-major tiles, kStages-deep mbarrier ring;
@@ -25,20 +31,25 @@
 
 namespace cmoe {
 
-enum GemmEpi : int { EPI_SWIGLU = 0, EPI_ROWSCALE = 1 };
+enum GemmEpi : int { EPI_SWIGLU = 0, EPI_ROWSCALE = 1, EPI_SWIGLU_BWD = 2, EPI_WGRAD = 3 };
 
 struct GemmArgs {
-  const int32_t* offsets;   // [n_experts+1] first permuted row of each expert (device)
+  const int32_t* offsets;   // row-grouped: [n_experts+1] first permuted row of each expert
   int32_t n_experts;        // experts on this rank
   int32_t n_tiles_n;        // 256-wide n-blocks per expert
-  int32_t num_kb;           // 128-byte k-blocks
+  int32_t num_kb;           // row-grouped: 128-byte k-blocks
   int32_t b_rows_per_expert;
-  void* out;                // output rows (bf16 or e4m3)
+  void* out;                // output (bf16 / e4m3 / fp32)
   int32_t ldo;              // output row stride (elements)
-  const float* row_scale;   // EPI_ROWSCALE: per permuted row combine weight
+  const float* row_scale;   // EPI_ROWSCALE: per permuted row combine weight (nullable)
   const float* act_scale;   // FP8: per-expert activation scale of the A operand [n_experts]
   const float* w_scale;     // FP8: per-(expert, B row) weight scale [n_experts][b_rows_per_expert]
   const float* out_scale;   // FP8 EPI_SWIGLU: per-expert scale of the e4m3 output [n_experts]
+  void* aux;                // EPI_SWIGLU: H out (nullable, [rows][2f]); EPI_SWIGLU_BWD: H in
+  int32_t ffn;              // f (column offset of the up half in H / dH)
+  const int32_t* kb_off;    // kWgrad: [n_experts+1] first k-block of each expert's (padded) rows
+  int32_t m_tiles;          // kWgrad: m-tiles per expert
+  int64_t out_estride;      // kWgrad: elements between consecutive experts' outputs
 };
 
 constexpr int kGemmThreads = 256;
@@ -60,27 +71,68 @@ struct GemmCfg {
 };
 
 struct TileInfo {
-  int e, mt, nt, row0, row_end;
+  int e, mt, nt;
+  int a_row;     // first A row of the tile (this CTA's half added by the caller)
+  int b_row;     // first B row of the tile
+  int row_end;   // row-grouped: end of the expert segment (epilogue mask)
+  int kb0, nkb;  // k-block range
 };
 
-__device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, int n_experts, int n_tiles_n,
-                                            const int32_t* offsets, int bm, TileInfo& ti) {
-  if (tile >= mt_prefix[n_experts] * n_tiles_n) return false;
+// Row-grouped decode: tiles of expert e = mtiles(e) x n_tiles_n, m fastest.
+__device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, const GemmArgs& a, int bm, TileInfo& ti) {
+  if (tile >= mt_prefix[a.n_experts] * a.n_tiles_n) return false;
   int e = 0;
-  while (tile >= mt_prefix[e + 1] * n_tiles_n) ++e;
-  const int local = tile - mt_prefix[e] * n_tiles_n;
+  while (tile >= mt_prefix[e + 1] * a.n_tiles_n) ++e;
+  const int local = tile - mt_prefix[e] * a.n_tiles_n;
   const int mtiles = mt_prefix[e + 1] - mt_prefix[e];
   ti.e = e;
   ti.nt = local / mtiles;
   ti.mt = local - ti.nt * mtiles;
-  ti.row0 = offsets[e] + ti.mt * bm;
-  ti.row_end = offsets[e + 1];
+  ti.a_row = a.offsets[e] + ti.mt * bm;
+  ti.b_row = e * a.b_rows_per_expert + ti.nt * kBN;
+  ti.row_end = a.offsets[e + 1];
+  ti.kb0 = 0;
+  ti.nkb = a.num_kb;
+  return true;
+}
+
+// K-grouped decode (weight gradients): every expert has m_tiles x n_tiles_n tiles; the K range
+// is the expert's padded row range.
+__device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, int bm, TileInfo& ti) {
+  const int per = a.m_tiles * a.n_tiles_n;
+  if (tile >= a.n_experts * per) return false;
+  const int e = tile / per;
+  const int local = tile - e * per;
+  ti.e = e;
+  ti.nt = local / a.m_tiles;
+  ti.mt = local - ti.nt * a.m_tiles;
+  ti.a_row = ti.mt * bm;
+  ti.b_row = ti.nt * kBN;
+  ti.row_end = 1 << 30;
+  ti.kb0 = a.kb_off[e];
+  ti.nkb = a.kb_off[e + 1] - a.kb_off[e];
   return true;
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
-template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8>
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                 pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+}
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int4 r = *reinterpret_cast<const int4*>(src + 8 * i);
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[8 * i + j] = __bfloat162float(h[j]);
+  }
+}
+
+template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8, bool kWgrad = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmArgs args) {
@@ -109,7 +161,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int cluster = kCtaGroup == 1 ? blockIdx.x : cluster_id_x();
   const int nclusters = kCtaGroup == 1 ? gridDim.x : nclusters_x();
 
-  if (threadIdx.x == 0) {
+  if (!kWgrad && threadIdx.x == 0) {
     int acc = 0;
     mt_prefix[0] = 0;
     for (int e = 0; e < args.n_experts; ++e) {
@@ -139,18 +191,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  auto next_tile = [&](int tile, TileInfo& ti) -> bool {
+    if constexpr (kWgrad) return decode_tile_wgrad(tile, args, Cfg::kBM, ti);
+    else return decode_tile(tile, mt_prefix, args, Cfg::kBM, ti);
+  };
+
   if (warp == 0) {
     // ===================== TMA producer =====================
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
       TileInfo ti;
-      for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
-                                           Cfg::kBM, ti);
-           tile += nclusters) {
-        const int a_row = ti.row0 + cta_rank * Cfg::kRowsPerCta;
-        const int b_row = ti.e * args.b_rows_per_expert + ti.nt * kBN + cta_rank * Cfg::kBRowsPerCta;
-        for (int kb = 0; kb < args.num_kb; ++kb) {
+      for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
+        const int a_row = ti.a_row + cta_rank * Cfg::kRowsPerCta;
+        const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
+        for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           if constexpr (kCtaGroup == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
@@ -174,13 +229,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int acc = 0;
       uint32_t aph = 0;
       TileInfo ti;
-      for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
-                                           Cfg::kBM, ti);
-           tile += nclusters) {
+      for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
-        for (int kb = 0; kb < args.num_kb; ++kb) {
+        for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t adesc = sdesc_k_sw128(smem_u32(sA + s * Cfg::kStageA));
@@ -193,6 +246,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mma_commit<kCtaGroup>(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
+        // (an empty k-range commits with no MMA outstanding: the epilogue then writes zeros)
         mma_commit<kCtaGroup>(&tfull[acc]);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
@@ -205,13 +259,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     TileInfo ti;
-    for (int tile = cluster; decode_tile(tile, mt_prefix, args.n_experts, args.n_tiles_n, args.offsets,
-                                         Cfg::kBM, ti);
-         tile += nclusters) {
+    for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int row = ti.row0 + cta_rank * Cfg::kRowsPerCta + row_in_cta;
+      const int row = ti.a_row + cta_rank * Cfg::kRowsPerCta + row_in_cta;
       const bool valid = row < ti.row_end;
+      const bool has_acc = ti.nkb > 0;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kBN;
       if constexpr (kEpi == EPI_SWIGLU) {
         float sg = 1.0f, su = 1.0f, so = 1.0f;
@@ -231,16 +284,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tmem_ld32(t_row + c * 32, g);
           tmem_ld32(t_row + kBN / 2 + c * 32, u);
           tmem_ld_wait();
-          float v[32];
+          float v[32], gv[32], uv[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            float gv = __uint_as_float(g[i]) * sg;
-            float uv = __uint_as_float(u[i]) * su;
+            gv[i] = __uint_as_float(g[i]) * sg;
+            uv[i] = __uint_as_float(u[i]) * su;
             if constexpr (kFp8) {
-              gv *= wsg[c * 32 + i];
-              uv *= wsu[c * 32 + i];
+              gv[i] *= wsg[c * 32 + i];
+              uv[i] *= wsu[c * 32 + i];
             }
-            v[i] = silu_f(gv) * uv;
+            v[i] = silu_f(gv[i]) * uv[i];
           }
           if (valid) {
             const int col = ti.nt * (kBN / 2) + c * 32;
@@ -258,15 +311,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               st_global_v4(dst, p[0], p[1], p[2], p[3]);
               st_global_v4(dst + 16, p[4], p[5], p[6], p[7]);
             } else {
-              __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col;
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                             pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
+              if (args.aux) {  // training: keep H = [G | U] for the SwiGLU backward
+                __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
+                store_bf16x32(hrow + col, gv);
+                store_bf16x32(hrow + args.ffn + col, uv);
+              }
             }
           }
         }
-      } else {
+      } else if constexpr (kEpi == EPI_ROWSCALE) {
         float rs = valid ? (args.row_scale ? args.row_scale[row] : 1.0f) : 0.0f;
         const float* ws = nullptr;
         if constexpr (kFp8) {
@@ -285,13 +339,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               v[i] = __uint_as_float(a[i]) * rs;
               if constexpr (kFp8) v[i] *= ws[c * 32 + i];
             }
-            __nv_bfloat16* dst =
-                reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                           pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32, v);
           }
+        }
+      } else if constexpr (kEpi == EPI_SWIGLU_BWD) {
+        // acc = dA for FFN channels [nt*256, nt*256+256); H = [G | U] of the forward pass.
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t a[32];
+          tmem_ld32(t_row + c * 32, a);
+          tmem_ld_wait();
+          if (valid) {
+            const int col = ti.nt * kBN + c * 32;
+            const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
+            float g[32], u[32], dg[32], du[32];
+            load_bf16x32(hrow + col, g);
+            load_bf16x32(hrow + args.ffn + col, u);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const float da = __uint_as_float(a[i]);
+              const float s = 1.0f / (1.0f + __expf(-g[i]));
+              du[i] = da * (g[i] * s);
+              dg[i] = da * u[i] * (s * (1.0f + g[i] * (1.0f - s)));
+            }
+            __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * (2 * args.ffn);
+            store_bf16x32(drow + col, dg);
+            store_bf16x32(drow + args.ffn + col, du);
+          }
+        }
+      } else {  // EPI_WGRAD: fp32 [M][N] per expert
+        float* base = reinterpret_cast<float*>(args.out) + (size_t)ti.e * args.out_estride + (size_t)row * args.ldo +
+                      ti.nt * kBN;
+#pragma unroll 1
+        for (int c = 0; c < kBN / 32; ++c) {
+          uint32_t a[32];
+          if (has_acc) {
+            tmem_ld32(t_row + c * 32, a);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) a[i] = 0u;
+          }
+          float* dst = base + c * 32;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) st_global_v4(dst + 4 * i, a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
         }
       }
       tc_fence_before();

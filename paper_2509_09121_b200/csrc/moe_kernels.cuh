@@ -7,7 +7,6 @@
 
 namespace cmoe {
 
-constexpr int kRouterThreads = 128;
 constexpr int kRouterChunk = 64;  // d-columns staged per pipeline step (d % 256 == 0 by config)
 constexpr int kRouterTT = 1;      // tokens per thread
 constexpr int kPlanThreads = 1024;
@@ -29,28 +28,32 @@ struct RouteBufs {
   int32_t* finite_flag; // [1] set to 1 on any non-finite router logit or layer output (K11)
 };
 
-// Router tile geometry: one thread per (token, 4 experts); 128 threads per CTA.
-__host__ __device__ inline int router_tokens_per_cta(int n_experts) {
+// Router tile geometry: one thread per (token, 4 experts). Two variants: 128-thread CTAs with a
+// 3-deep ring for large batches (throughput), 32-thread CTAs with an 8-deep ring for small batches
+// (latency: more CTAs in flight and a deeper prefetch of the sequential chunk stream).
+__host__ __device__ inline int router_tokens_per_cta(int n_experts, int threads) {
   const int groups = (n_experts + 3) / 4;
-  return (kRouterThreads / groups) * kRouterTT;
+  return (threads / groups) * kRouterTT;
 }
 struct RouterSmem {
   int tpc, N4, xs;
   size_t raw_x, sw, sx, slog, sidx, slse, total;
-  __host__ __device__ RouterSmem(int n_experts) {
+  __host__ __device__ RouterSmem(int n_experts, int threads, int stages) {
     N4 = (n_experts + 3) / 4 * 4;
-    tpc = router_tokens_per_cta(n_experts);
+    tpc = router_tokens_per_cta(n_experts, threads);
     xs = kRouterChunk + 2;  // padded fp64 row of one token: 16-byte aligned, conflict-free double2 loads
     raw_x = 0;
-    sw = raw_x + 2 * (size_t)tpc * kRouterChunk * 2;          // [2][chunk][N4] fp64 (cp.async target)
-    sx = sw + 2 * sizeof(double) * kRouterChunk * N4;         // [tpc][xs] fp64
+    sw = raw_x + (size_t)stages * tpc * kRouterChunk * 2;     // [stages][chunk][N4] fp64 (cp.async target)
+    sx = sw + (size_t)stages * sizeof(double) * kRouterChunk * N4;  // [tpc][xs] fp64
     slog = sx + sizeof(double) * tpc * xs;
     sidx = slog + sizeof(float) * tpc * N4;
     slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
     total = slse + sizeof(double) * tpc;
   }
 };
-__host__ __device__ inline size_t router_smem_bytes(int n_experts) { return RouterSmem(n_experts).total; }
+__host__ __device__ inline size_t router_smem_bytes(int n_experts, int threads, int stages) {
+  return RouterSmem(n_experts, threads, stages).total;
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 16 : 0)
@@ -80,10 +83,11 @@ __global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, 
 // (tensor.cpp:1046-1060), renormalised combine weights, per-tile expert counts
 // and local ranks for the stable dispatch permutation, and per-tile partial sums for agg_prob
 // (col_sums, tensor.cpp:545-565) and the Z-loss (tensor.cpp:1011-1040).
-__global__ void __launch_bounds__(kRouterThreads) router_kernel(const __nv_bfloat16* __restrict__ x,
+template <int kRouterThreads, int kStages>
+__global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bfloat16* __restrict__ x,
                                                                 const double* __restrict__ wr64, int T, int d,
                                                                 int N, int K, RouteBufs rb) {
-  const RouterSmem L(N);
+  const RouterSmem L(N, kRouterThreads, kStages);
   const int groups = L.N4 / 4;
   const int N4 = L.N4;
   const int tg_per_cta = kRouterThreads / groups;
@@ -124,16 +128,16 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(const __nv_bfloa
       cp_async16(sw + (size_t)buf * kRouterChunk * N4 + i * 2, wsrc + i * 2, true);
     cp_async_commit();
   };
-  issue(0, 0);
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < nchunks) issue(c, c);
+    else cp_async_commit();
+  }
   for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nchunks) {
-      issue(c + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
+    const int buf = c % kStages;
+    cp_async_wait<kStages - 2>();  // chunk c has landed (one group committed per chunk)
+    __syncthreads();               // ... and every thread is done with chunk c-1's buffers
+    if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
+    else cp_async_commit();
     // widen x to fp64, [tok][l] layout
     const __nv_bfloat16* rx = rawx + (size_t)buf * tpc * kRouterChunk;
     for (int i = threadIdx.x; i < tpc * kRouterChunk / 2; i += kRouterThreads) {
@@ -146,21 +150,41 @@ __global__ void __launch_bounds__(kRouterThreads) router_kernel(const __nv_bfloa
     if (worker) {
       const double2* xv = reinterpret_cast<const double2*>(sx + tgi * xs);
       const double2* wv = reinterpret_cast<const double2*>(sw + (size_t)buf * kRouterChunk * N4 + g * 4);
-#pragma unroll 8
-      for (int l2 = 0; l2 < kRouterChunk / 2; ++l2) {
-        const double2 xx = xv[l2];
-        const double2 wa01 = wv[(2 * l2) * (N4 / 2)];
-        const double2 wa23 = wv[(2 * l2) * (N4 / 2) + 1];
-        const double2 wb01 = wv[(2 * l2 + 1) * (N4 / 2)];
-        const double2 wb23 = wv[(2 * l2 + 1) * (N4 / 2) + 1];
-        acc[0][0] = fma(xx.x, wa01.x, acc[0][0]);
-        acc[0][1] = fma(xx.x, wa01.y, acc[0][1]);
-        acc[0][2] = fma(xx.x, wa23.x, acc[0][2]);
-        acc[0][3] = fma(xx.x, wa23.y, acc[0][3]);
-        acc[0][0] = fma(xx.y, wb01.x, acc[0][0]);
-        acc[0][1] = fma(xx.y, wb01.y, acc[0][1]);
-        acc[0][2] = fma(xx.y, wb23.x, acc[0][2]);
-        acc[0][3] = fma(xx.y, wb23.y, acc[0][3]);
+      // Register double buffer: the operands of l-pair block b+1 are requested before block b is
+      // consumed, so the four accumulator chains never wait on a shared-memory round trip.
+      constexpr int kU = 4;
+      double2 cur[kU][5], nxt[kU][5];
+      auto load = [&](double2 (&r)[kU][5], int l2b) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int l2 = l2b + u;
+          r[u][0] = xv[l2];
+          r[u][1] = wv[(2 * l2) * (N4 / 2)];
+          r[u][2] = wv[(2 * l2) * (N4 / 2) + 1];
+          r[u][3] = wv[(2 * l2 + 1) * (N4 / 2)];
+          r[u][4] = wv[(2 * l2 + 1) * (N4 / 2) + 1];
+        }
+      };
+      load(cur, 0);
+#pragma unroll
+      for (int l2b = 0; l2b < kRouterChunk / 2; l2b += kU) {
+        if (l2b + kU < kRouterChunk / 2) load(nxt, l2b + kU);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const double2 xx = cur[u][0];
+          acc[0][0] = fma(xx.x, cur[u][1].x, acc[0][0]);
+          acc[0][1] = fma(xx.x, cur[u][1].y, acc[0][1]);
+          acc[0][2] = fma(xx.x, cur[u][2].x, acc[0][2]);
+          acc[0][3] = fma(xx.x, cur[u][2].y, acc[0][3]);
+          acc[0][0] = fma(xx.y, cur[u][3].x, acc[0][0]);
+          acc[0][1] = fma(xx.y, cur[u][3].y, acc[0][1]);
+          acc[0][2] = fma(xx.y, cur[u][4].x, acc[0][2]);
+          acc[0][3] = fma(xx.y, cur[u][4].y, acc[0][3]);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int q = 0; q < 5; ++q) cur[u][q] = nxt[u][q];
       }
     }
     __syncthreads();

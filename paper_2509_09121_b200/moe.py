@@ -215,6 +215,44 @@ class MoELayer:
                     "fp8_scales")
         return a, b, wi, wo
 
+    # ---------------------------------------------------------------- training (expert-FFN backward)
+    def forward_train(self, hidden: torch.Tensor, want_decision: bool = False):
+        hidden = self._bf16(hidden)
+        out = torch.empty_like(hidden)
+        dec, cd = None, None
+        if want_decision:
+            dec = self._new_decision(hidden.shape[0])
+            cd = C.byref(self._decision_struct(dec))
+        self._check(self.L.cl_moe_forward_train(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), cd,
+                                                _stream(self.device)), "forward_train")
+        return (out, dec) if want_decision else out
+
+    def backward(self, d_out: torch.Tensor):
+        """Expert-FFN backward of the last forward_train: (d_hidden, d_combine_w, dW_in, dW_out)."""
+        d_out = self._bf16(d_out)
+        t = d_out.shape[0]
+        nl = self.cfg.n_experts // self.cfg.ep_size
+        d, f, k = self.cfg.d_model, self.cfg.d_ff, self.cfg.top_k
+        dh = torch.empty_like(d_out)
+        dcw = torch.empty(t, k, dtype=torch.float32, device=self.device)
+        dwi = torch.empty(nl, d, 2 * f, dtype=torch.float32, device=self.device)
+        dwo = torch.empty(nl, f, d, dtype=torch.float32, device=self.device)
+        self._check(self.L.cl_moe_backward(self.h, _ptr(d_out), _ptr(dh), _ptr(dcw), _ptr(dwi), _ptr(dwo),
+                                           _stream(self.device)), "backward")
+        return dh, dcw, dwi, dwo
+
+    def _new_decision(self, t: int) -> "RouterDecision":
+        n, k, dev = self.cfg.n_experts, self.cfg.top_k, self.device
+        return RouterDecision(
+            logits=torch.empty(t, n, dtype=torch.float32, device=dev),
+            probs=torch.empty(t, n, dtype=torch.float32, device=dev),
+            topk_idx=torch.empty(t, k, dtype=torch.int32, device=dev),
+            combine_weights=torch.empty(t, k, dtype=torch.float32, device=dev),
+            counts=torch.empty(n, dtype=torch.int64, device=dev),
+            agg_prob=torch.empty(n, dtype=torch.float32, device=dev),
+            aux=torch.empty(1, dtype=torch.float32, device=dev),
+            z=torch.empty(1, dtype=torch.float32, device=dev), B=t, K=k)
+
     # ---------------------------------------------------------------- expert parallelism
     @staticmethod
     def ep_unique_id() -> bytes:

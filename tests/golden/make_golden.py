@@ -37,7 +37,11 @@ def main():
         rows = np.where((r["topk_idx"] == 0).any(1))[0]
         dy = make_inputs(len(rows), d, 1, f, seed=7, experts=False)["x"]
         dx, dwi, dwo = ref.expert_ffn_backward(inp["x"][rows], inp["w_in"][0], inp["w_out"][0], dy)
+        gl = make_inputs(t, d, 1, f, seed=11, experts=False)["x"]
+        ldh, ldcw, ldwi, ldwo = ref.moe_backward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"],
+                                                 r["combine_weights"], gl)
         np.savez_compressed(os.path.join(HERE, f"{name}.npz"), shape=np.array([t, d, n, k, f]),
+                            layer_d_hidden=ldh, layer_d_combine_w=ldcw, layer_dw_in=ldwi, layer_dw_out=ldwo,
                             skew=np.array([np.nan if skew is None else skew]), logits=r["logits"], probs=r["probs"],
                             topk_idx=r["topk_idx"], combine_weights=r["combine_weights"], counts=r["counts"],
                             agg_prob=r["agg_prob"], aux=np.float32(aux), z=np.float32(z), out=out, bwd_rows=rows,

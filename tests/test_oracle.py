@@ -38,6 +38,11 @@ def test_oracle_matches_reference_golden(oracle_port, path):
     dy = make_inputs(len(rows), d, 1, f, seed=7, experts=False)["x"]
     dx, dwi, dwo = oracle_port.expert_ffn_backward(inp["x"][rows], inp["w_in"][0], inp["w_out"][0], dy)
     assert np.array_equal(dx, g["dx"]) and np.array_equal(dwi, g["dw_in"]) and np.array_equal(dwo, g["dw_out"])
+    # full layer backward (reference Tape over the whole composition)
+    gl = make_inputs(t, d, 1, f, seed=11, experts=False)["x"]
+    got = oracle_port.moe_backward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], gl, jobs=2)
+    for a, key in zip(got, ("layer_d_hidden", "layer_d_combine_w", "layer_dw_in", "layer_dw_out")):
+        assert np.array_equal(a, g[key]), key
 
 
 # ------------------------------------------------------------------ direct reference comparison
@@ -53,6 +58,17 @@ def test_oracle_bit_exact_vs_reference_build(oracle_port, oracle_ref, t, d, n, k
     assert np.array_equal(ya, yb)
     assert oracle_port.aux_loss(a["probs"], a["counts"], k) == oracle_ref.aux_loss(a["probs"], a["counts"], k)
     assert oracle_port.z_loss(a["logits"]) == oracle_ref.z_loss(a["logits"])
+
+
+@pytest.mark.parametrize("t,d,n,k,f", [(41, 32, 4, 2, 16), (30, 64, 8, 3, 32)])
+def test_layer_backward_bit_exact_vs_reference_tape(oracle_port, oracle_ref, t, d, n, k, f):
+    inp = make_inputs(t, d, n, f)
+    r = oracle_port.route(inp["x"], inp["w_router"], k)
+    g = make_inputs(t, d, 1, f, seed=9, experts=False)["x"]
+    a = oracle_port.moe_backward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], g, jobs=4)
+    b = oracle_ref.moe_backward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], g)
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
 
 
 def test_reference_gradcheck_suite_passes(oracle_ref):
