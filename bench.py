@@ -36,6 +36,9 @@ CONFIGS = {
     # BASELINE.json configs[3] decode-size batch at the C2 layer shape (bf16 path)
     "c4": dict(workload="decode-size batch at the C2 layer shape (BASELINE configs[3])", T=256, d=4096, N=16, K=2,
                f=14336),
+    # BASELINE.json configs[4]: skewed routing, forward + expert-FFN backward
+    "c5": dict(workload="skewed-routing stress, fwd + expert-FFN bwd (BASELINE configs[4])", T=65536, d=4096, N=16,
+               K=2, f=14336, skew=1.8, train=True),
 }
 SEED = 20261018
 METRIC = "MoE-layer tokens/sec at 1/2/4/8 B200; % tcgen05 peak (GEMM), % HBM BW (dispatch)"
@@ -189,8 +192,18 @@ def run_ours(args, cfg):
         obj = [MoELayer.ep_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         layer.ep_init(obj[0])
-    x = layer.synthetic_tokens(T, SEED + rank)
+    train = bool(cfg.get("train"))
+    if cfg.get("skew"):
+        layer.synthetic_skew(cfg["skew"])
+    x = layer.synthetic_tokens(T, SEED + rank, shift=1.0 if cfg.get("skew") else 0.0)
     out = torch.empty_like(x)
+    if train:
+        g_out = layer.synthetic_tokens(T, SEED + 7 + rank)
+        d_hid = torch.empty_like(x)
+        nl_ = N // world
+        d_cw = torch.empty(T, K, dtype=torch.float32, device=x.device)
+        dwi = torch.empty(nl_, d, 2 * f, dtype=torch.float32, device=x.device)
+        dwo = torch.empty(nl_, f, d, dtype=torch.float32, device=x.device)
     if args.precision == "fp8":
         # expert-aware FP8: calibrate on this batch (per-expert activation maxima), quantize weights
         layer.calibrate(x)
@@ -198,8 +211,14 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
 
     def step():
-        layer._check(layer.L.cl_moe_forward(layer.h, x.data_ptr(), T, out.data_ptr(), None, stream.cuda_stream),
-                     "forward")
+        if train:
+            layer._check(layer.L.cl_moe_forward_train(layer.h, x.data_ptr(), T, out.data_ptr(), None,
+                                                      stream.cuda_stream), "forward_train")
+            layer._check(layer.L.cl_moe_backward(layer.h, g_out.data_ptr(), d_hid.data_ptr(), d_cw.data_ptr(),
+                                                 dwi.data_ptr(), dwo.data_ptr(), stream.cuda_stream), "backward")
+        else:
+            layer._check(layer.L.cl_moe_forward(layer.h, x.data_ptr(), T, out.data_ptr(), None, stream.cuda_stream),
+                         "forward")
 
     for _ in range(args.warmup):
         step()
@@ -233,22 +252,47 @@ def run_ours(args, cfg):
     ms_step = ms / args.steps
     value = world * T * args.steps / (ms / 1e3)
 
+    if train:
+        xh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+        gh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+        oh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+        dh_h = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+        xh.copy_(x)
+        gh.copy_(g_out)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_steps = max(2, args.steps // 2)
+        for _ in range(e2e_steps):
+            x.copy_(xh, non_blocking=True)
+            g_out.copy_(gh, non_blocking=True)
+            step()
+            oh.copy_(out, non_blocking=True)
+            dh_h.copy_(d_hid, non_blocking=True)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        e2e_val = world * T * e2e_steps / e2e_s
+        h2d_b, d2h_b = 2 * T * d * 2, 2 * T * d * 2
+    else:
+        h2d_b, d2h_b = T * d * 2, T * d * 2
     # ---- end to end through the host-buffer C-ABI (pinned host bf16 in/out, pipelined calls) ----
-    xh = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+    xh = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)] if not train else []
     for b in xh:
         b.copy_(x)
-    oh = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
-    for i in range(2):
-        layer.forward_host_async(xh[i].data_ptr(), T, oh[i].data_ptr())
-    layer.host_wait()
-    e2e_steps = args.steps
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        layer.forward_host_async(xh[i % 2].data_ptr(), T, oh[i % 2].data_ptr())
-    layer.host_wait()
-    e2e_s = time.perf_counter() - t0
+    if not train:
+        oh = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+        for i in range(2):
+            layer.forward_host_async(xh[i].data_ptr(), T, oh[i].data_ptr())
+        layer.host_wait()
+        e2e_steps = args.steps
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(e2e_steps):
+            layer.forward_host_async(xh[i % 2].data_ptr(), T, oh[i % 2].data_ptr())
+        layer.host_wait()
+        e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -257,7 +301,8 @@ def run_ours(args, cfg):
 
     # ---- roofline of the dominant kernel (GEMM1 + SwiGLU) and of dispatch ----
     peaks = load_peaks()
-    per = {k: v / max(calls, 1) for k, v in stage_ms.items()}
+    nf, nb = calls
+    per = {k: v / max(nb if i >= 6 else nf, 1) for i, (k, v) in enumerate(stage_ms.items()) if (i < 6 or nb)}
     g1_flop = 2.0 * T * K * d * (2 * f)
     g2_flop = 2.0 * T * K * f * d
     g1_tf = g1_flop / (per["gemm1"] * 1e-3) / 1e12
@@ -287,7 +332,13 @@ def run_ours(args, cfg):
                         global_batch=T * world, parallelism=("ep%d (experts %d/rank, NCCL all-to-all)" % (world, N // world))
                         if world > 1 else "single",
                         gemm_ctas=args.gemm_ctas or 2, l2="inputs larger than L2 (x 134 MB, weights 5.6 GB); no flush"),
-            roofline=(dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
+            roofline=(dict(bound="tensor", kernel="grouped GEMMs fwd+bwd (tcgen05, 6 launches)",
+                           achieved=3 * (g1_flop + g2_flop) / (sum(per[k] for k in ("gemm1", "gemm2", "dgrad1_swiglu_bwd",
+                                                                                      "dgrad2", "wgrad_out", "wgrad_in"))
+                                                                * 1e-3) / 1e12,
+                           peak=peaks["bf16_sus"], unit="TFLOP/s", traffic=None,
+                           flop_per_step=3 * (g1_flop + g2_flop)) if train else
+                      dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05)", achieved=g1_tf,
                            peak=peaks["bf16_sus"], unit="TFLOP/s", frac=g1_tf / peaks["bf16_sus"],
                            frac_of_burst=g1_tf / peaks["bf16"], peak_kind=f"sustained ({peaks['src']})",
                            traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
@@ -301,9 +352,11 @@ def run_ours(args, cfg):
                 dispatch=dict(achieved=disp_gbs, unit="GB/s", frac=disp_gbs / peaks["hbm"], bytes=disp_bytes),
                 combine=dict(achieved=comb_gbs, unit="GB/s", frac=comb_gbs / peaks["hbm"], bytes=comb_bytes),
                 layer_tflops=(g1_flop + g2_flop) / (ms_step * 1e-3) / 1e12),
-            e2e=dict(value=e2e_val, unit="tokens/s", h2d_bytes_per_step=T * d * 2, d2h_bytes_per_step=T * d * 2,
-                     timing="host wall clock around K pipelined cl_moe_forward_host_async calls + cl_moe_host_wait"),
-            gpu_launches=6 * args.steps,
+            e2e=dict(value=e2e_val, unit="tokens/s", h2d_bytes_per_step=h2d_b, d2h_bytes_per_step=d2h_b,
+                     timing=("host wall clock: pinned H2D of x and dOut, forward_train + backward, D2H of out and "
+                             "d_hidden, every step" if train else
+                             "host wall clock around K pipelined cl_moe_forward_host_async calls + cl_moe_host_wait")),
+            gpu_launches=(6 + 13) * args.steps if train else 6 * args.steps,
             clocks=clocks,
         )
         if not args.no_cpu_baseline and world == 1:
@@ -318,6 +371,11 @@ def run_ours(args, cfg):
                 value=t_s / dt, unit="tokens/s", cores=min(jobs, N), kind=kind,
                 sample=f"{t_s} tokens of the same layer shape, one forward, fp32 (expert fan-out over "
                        f"{min(jobs, N)} threads)")
+        if "frac" not in line["roofline"]:
+            line["roofline"]["frac"] = line["roofline"]["achieved"] / line["roofline"]["peak"]
+        if train:
+            line["config"]["skew_gamma"] = cfg["skew"]
+            line["config"]["mode"] = "forward_train + expert-FFN backward per step"
         print(json.dumps(line), flush=True)
     layer.close()
     if world > 1:

@@ -111,6 +111,12 @@ const char* cl_moe_last_error(const cl_moe* h);
 /* Synthetic tokens x = split(1) N(0,1) of root seed `seed`, rounded to bf16: [T x d] device. */
 cl_status cl_moe_synthetic_tokens(cl_moe* h, uint64_t seed, int64_t T, void* x, void* stream);
 
+/* Skewed-routing stress construction: tokens x = N(0,1) + shift (then
+ * bf16), and router columns W_r[:, i] += gamma * ln(1/(i+1)^1.2) / d. */
+cl_status cl_moe_synthetic_tokens_shifted(cl_moe* h, uint64_t seed, int64_t T, float shift, void* x,
+                                          void* stream);
+cl_status cl_moe_synthetic_skew(cl_moe* h, double gamma);
+
 /* route_tokens. */
 cl_status cl_moe_route_tokens(cl_moe* h, const void* hidden, int64_t T, const cl_moe_decision* out,
                               void* stream);
@@ -150,9 +156,11 @@ cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* view);
 cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, void* stream);
 
 /* Per-stage device timing with CUDA events recorded on the launch stream between the kernels of
- * each call: stages 0 router, 1 plan, 2 dispatch, 3 GEMM1(+SwiGLU), 4 GEMM2(+weight), 5 combine.
- * profile_read returns the summed milliseconds per stage over the calls since enabling/reading
- * (stage_ms has 6 entries) and the number of calls; it synchronises on the recorded events. */
+ * each call. Forward stages 0 router, 1 plan, 2 dispatch, 3 GEMM1(+SwiGLU), 4 GEMM2(+weight),
+ * 5 combine; backward stages 6 combine-bwd, 7 dgrad-1(+SwiGLU-bwd), 8 dgrad-2, 9 dispatch-bwd,
+ * 10 transposes, 11 wgrad dW_out, 12 wgrad dW_in. profile_read returns the summed milliseconds
+ * per stage (stage_ms has 13 entries) since enabling/reading and calls[0] forward / calls[1]
+ * backward call counts; it synchronises on the recorded events. */
 cl_status cl_moe_profile(cl_moe* h, int32_t enable);
 cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls);
 

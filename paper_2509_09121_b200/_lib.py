@@ -78,6 +78,9 @@ _PROTOS = {
     "cl_moe_destroy": (None, [C.c_void_p]),
     "cl_moe_last_error": (C.c_char_p, [C.c_void_p]),
     "cl_moe_synthetic_tokens": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "cl_moe_synthetic_tokens_shifted": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_float, C.c_void_p,
+                                                  C.c_void_p]),
+    "cl_moe_synthetic_skew": (C.c_int, [C.c_void_p, C.c_double]),
     "cl_moe_route_tokens": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Decision), C.c_void_p]),
     "cl_moe_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cl_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(Decision), C.c_void_p]),

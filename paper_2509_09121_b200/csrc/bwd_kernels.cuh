@@ -101,6 +101,19 @@ __global__ void __launch_bounds__(256) transpose_pad_kernel(const __nv_bfloat16*
   }
 }
 
+// Zero the padding columns [poff[e] + cnt_e, poff[e+1]) of a transposed buffer [C][rp] whose data
+// columns are written by a GEMM epilogue. Grid: (C / 256, n_experts), 256 threads.
+__global__ void zero_pad_cols_kernel(__nv_bfloat16* __restrict__ buf, int C, int64_t rp,
+                                     const int32_t* __restrict__ offsets, const int32_t* __restrict__ poff) {
+  const int e = blockIdx.y;
+  const int c = blockIdx.x * 256 + threadIdx.x;
+  if (c >= C) return;
+  const int64_t start = poff[e] + (offsets[e + 1] - offsets[e]);
+  const int64_t end = poff[e + 1];
+  __nv_bfloat16* row = buf + (size_t)c * rp;
+  for (int64_t k = start; k < end; ++k) row[k] = __float2bfloat16_rn(0.0f);
+}
+
 // dst[i][j] = src[rowmap(j)][i]: src [rows_src][cols_src] bf16 -> dst [cols_src][rows_src].
 // kWinMap: rowmap(c) = packed W_in row of reference column c (inverse of win_col_of_packed_row).
 template <bool kWinMap>

@@ -148,6 +148,7 @@ struct cl_moe {
   // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
   bool prof = false;
   std::vector<std::vector<cudaEvent_t>> prof_sets;
+  std::vector<int> prof_kind;          // 0 forward (6 stages), 1 backward (7 stages)
   size_t prof_used = 0;
   std::vector<cudaEvent_t>* cur_ev = nullptr;
 
@@ -227,16 +228,19 @@ cl_status guarded(cl_moe* h, Fn fn) {
   }
 }
 
-constexpr int kStages = 6;  // router, plan, dispatch, gemm1, gemm2, combine
+constexpr int kStages = 6;     // forward: router, plan, dispatch, gemm1, gemm2, combine
+constexpr int kBwdStages = 7;  // backward: combine-bwd, dgrad1, dgrad2, dispatch-bwd, transposes, wgrad-out, wgrad-in
 
-void prof_begin(cl_moe* h, cudaStream_t st) {
+void prof_begin(cl_moe* h, cudaStream_t st, int kind = 0) {
   h->cur_ev = nullptr;
   if (!h->prof) return;
   if (h->prof_used == h->prof_sets.size()) {
-    std::vector<cudaEvent_t> v(kStages + 1);
+    std::vector<cudaEvent_t> v(kBwdStages + 1);
     for (auto& e : v) CK(cudaEventCreate(&e));
     h->prof_sets.push_back(v);
+    h->prof_kind.push_back(0);
   }
+  h->prof_kind[h->prof_used] = kind;
   h->cur_ev = &h->prof_sets[h->prof_used++];
   CK(cudaEventRecord((*h->cur_ev)[0], st));
 }
@@ -444,6 +448,11 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g1.out_scale = h->sx_mid;
   g1.aux = h_save;
   g1.ffn = static_cast<int>(h->f);
+  if (h_save) {  // training: also write A^T into the padded K-major buffer of the dW_out GEMM
+    g1.aux_t = h->AT;
+    g1.rp = h->rp_cap;
+    g1.poff = h->poff;
+  }
   GemmArgs g2{};
   g2.offsets = offsets;
   g2.n_experts = h->n_local;
@@ -695,6 +704,7 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
                                                  h->inv, h->row_w, nullptr);
+  pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, h->n_local, h->poff, h->kb_off);
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
   run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf);
@@ -714,11 +724,13 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
   const int64_t T = h->train_T, rows = T * h->K, d = h->d, f = h->f;
   const int NL = h->n_local;
+  prof_begin(h, st, 1);
   // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
   combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_out), h->y, h->perm,
                                                            h->rb.combine_w, (int)rows, (int)d, (int)h->K, h->dYbuf,
                                                            d_cw);
   CK(cudaGetLastError());
+  prof_mark(h, 0, st);
   const int v = (h->gemm_auto ? (h->last_tokens * h->K / NL >= 1024) : h->gemm_ctas == 2) ? 1 : 0;
   // 2. dA = dY W_out^T fused with the SwiGLU backward -> dH
   GemmArgs a1{};
@@ -730,6 +742,9 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   a1.out = h->dHbuf;
   a1.aux = h->Hbuf;
   a1.ffn = static_cast<int>(f);
+  a1.aux_t = h->dHT;  // dH^T straight from the epilogue (dW_in GEMM operand)
+  a1.rp = h->rp_cap;
+  a1.poff = h->poff;
   // 3. dX = dH W_in^T
   GemmArgs a2{};
   a2.offsets = h->rb.offsets;
@@ -741,28 +756,35 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   a2.ldo = static_cast<int>(d);
   if (v) {
     launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    prof_mark(h, 1, st);
     launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
   } else {
     launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    prof_mark(h, 1, st);
     launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
   }
+  prof_mark(h, 2, st);
   // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]
   launch_combine<__nv_bfloat16>(h->dXbuf, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
                                 h->rb.finite_flag, st);
   CK(cudaGetLastError());
+  prof_mark(h, 3, st);
   // 5. weight gradients over each expert's rows (variable K): padded K-major transposes, then
   //    dW_out[e] = A_e^T dY_e ([f x d]) and dW_in[e] = X_e^T dH_e ([d x 2f]), fp32.
-  pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, NL, h->poff, h->kb_off);
+  //    (A^T and dH^T were written by the GEMM1 / dgrad-1 epilogues; only their padding columns
+  //    need zeroing. X^T and dY^T go through the transpose kernel.)
   const unsigned pb = static_cast<unsigned>(h->rp_cap / 64);
   transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)d,
                                                                      h->rb.offsets, h->poff, NL, h->XT, h->rp_cap);
-  transpose_pad_kernel<<<dim3((unsigned)(f / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)f,
-                                                                     h->rb.offsets, h->poff, NL, h->AT, h->rp_cap);
   transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, h->rb.offsets, h->poff, NL,
                                                                      h->dYT, h->rp_cap);
-  transpose_pad_kernel<<<dim3((unsigned)(2 * f / 64), pb), 256, 0, st>>>(h->dHbuf, (int)(2 * f), h->rb.offsets,
-                                                                         h->poff, NL, h->dHT, h->rp_cap);
+  zero_pad_cols_kernel<<<dim3((unsigned)((f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap,
+                                                                                        h->rb.offsets, h->poff);
+  zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
+                                                                                            h->rp_cap, h->rb.offsets,
+                                                                                            h->poff);
   CK(cudaGetLastError());
+  prof_mark(h, 4, st);
   const int gw = (f % 256 == 0) ? 2 : 1;
   GemmArgs wo{};
   wo.n_experts = NL;
@@ -782,11 +804,15 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   wi.out_estride = d * 2 * f;
   if (gw == 2) {
     launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwo[1], h->mBwo[1], wo, st);
+    prof_mark(h, 5, st);
     launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwi[1], h->mBwi[1], wi, st);
   } else {
     launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwo[0], h->mBwo[0], wo, st);
+    prof_mark(h, 5, st);
     launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwi[0], h->mBwi[0], wi, st);
   }
+  prof_mark(h, 6, st);
+  h->cur_ev = nullptr;
 }
 
 }  // namespace
@@ -936,13 +962,36 @@ void cl_moe_destroy(cl_moe* h) {
   delete h;
 }
 
-cl_status cl_moe_synthetic_tokens(cl_moe* h, uint64_t seed, int64_t T, void* x, void* stream) {
+cl_status cl_moe_synthetic_tokens_shifted(cl_moe* h, uint64_t seed, int64_t T, float shift, void* x, void* stream) {
   return guarded(h, [&] {
     if (!x || T < 1) throw ConfigErr("bad arguments");
     CK(cudaSetDevice(h->cfg.device));
     synth_bf16_kernel<<<grid_for(T * h->d), 256, 0, (cudaStream_t)stream>>>(split_seed(seed, 1), T * h->d, 1.0f,
-                                                                             static_cast<__nv_bfloat16*>(x));
+                                                                             static_cast<__nv_bfloat16*>(x), shift);
     CK(cudaGetLastError());
+  });
+}
+
+cl_status cl_moe_synthetic_tokens(cl_moe* h, uint64_t seed, int64_t T, void* x, void* stream) {
+  return cl_moe_synthetic_tokens_shifted(h, seed, T, 0.0f, x, stream);
+}
+
+cl_status cl_moe_synthetic_skew(cl_moe* h, double gamma) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    const int64_t d = h->d, N = h->N;
+    std::vector<float> wr(d * N), add(N);
+    for (int64_t i = 0; i < N; ++i)
+      add[i] = static_cast<float>(gamma * std::log(1.0 / std::pow(static_cast<double>(i + 1), 1.2)) /
+                                  static_cast<double>(d));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(wr.data(), h->wr, sizeof(float) * d * N, cudaMemcpyDeviceToHost));
+    for (int64_t l = 0; l < d; ++l)
+      for (int64_t i = 0; i < N; ++i) wr[l * N + i] = wr[l * N + i] + add[i];
+    CK(cudaMemcpy(h->wr, wr.data(), sizeof(float) * d * N, cudaMemcpyHostToDevice));
+    widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
   });
 }
 
@@ -1097,17 +1146,20 @@ cl_status cl_moe_profile(cl_moe* h, int32_t enable) {
 cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls) {
   return guarded(h, [&] {
     CK(cudaSetDevice(h->cfg.device));
-    for (int s = 0; s < kStages; ++s) stage_ms[s] = 0.0;
+    for (int s = 0; s < kStages + kBwdStages; ++s) stage_ms[s] = 0.0;
+    calls[0] = calls[1] = 0;
     for (size_t c = 0; c < h->prof_used; ++c) {
       auto& ev = h->prof_sets[c];
-      CK(cudaEventSynchronize(ev[kStages]));
-      for (int s = 0; s < kStages; ++s) {
+      const int kind = h->prof_kind[c];
+      const int n = kind == 0 ? kStages : kBwdStages;
+      CK(cudaEventSynchronize(ev[n]));
+      for (int s = 0; s < n; ++s) {
         float ms = 0.0f;
         CK(cudaEventElapsedTime(&ms, ev[s], ev[s + 1]));
-        stage_ms[s] += ms;
+        stage_ms[(kind == 0 ? 0 : kStages) + s] += ms;
       }
+      calls[kind] += 1;
     }
-    *calls = static_cast<int64_t>(h->prof_used);
     h->prof_used = 0;
   });
 }

@@ -50,6 +50,9 @@ struct GemmArgs {
   const int32_t* kb_off;    // kWgrad: [n_experts+1] first k-block of each expert's (padded) rows
   int32_t m_tiles;          // kWgrad: m-tiles per expert
   int64_t out_estride;      // kWgrad: elements between consecutive experts' outputs
+  void* aux_t;              // training: transposed copy of the output, bf16 [C][rp] (nullable)
+  int64_t rp;               // row stride of aux_t (padded-row capacity)
+  const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
 };
 
 constexpr int kGemmThreads = 256;
@@ -130,6 +133,13 @@ __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v)
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[8 * i + j] = __bfloat162float(h[j]);
   }
+}
+
+// Transposed store of 32 consecutive columns of one row: lanes of a warp hold consecutive rows, so
+// each 2-byte store instruction writes one contiguous 64-byte run of the transposed matrix.
+__device__ __forceinline__ void store_t_bf16x32(__nv_bfloat16* dst, int64_t stride, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) dst[(size_t)i * stride] = __float2bfloat16_rn(v[i]);
 }
 
 template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8, bool kWgrad = false>
@@ -265,6 +275,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int row = ti.a_row + cta_rank * Cfg::kRowsPerCta + row_in_cta;
       const bool valid = row < ti.row_end;
       const bool has_acc = ti.nkb > 0;
+      const int64_t prow = args.aux_t ? (int64_t)args.poff[ti.e] + (row - args.offsets[ti.e]) : 0;
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kBN;
       if constexpr (kEpi == EPI_SWIGLU) {
         float sg = 1.0f, su = 1.0f, so = 1.0f;
@@ -317,6 +328,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 store_bf16x32(hrow + col, gv);
                 store_bf16x32(hrow + args.ffn + col, uv);
               }
+              if (args.aux_t)  // training: A^T (padded K-major) for the dW_out gradient GEMM
+                store_t_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)col * args.rp + prow, args.rp, v);
             }
           }
         }
@@ -344,17 +357,38 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       } else if constexpr (kEpi == EPI_SWIGLU_BWD) {
         // acc = dA for FFN channels [nt*256, nt*256+256); H = [G | U] of the forward pass.
+        // H of chunk c+1 is requested before chunk c is processed (hides the global latency).
+        const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
+        int4 hg[4], hu[4];
+        auto fetch = [&](int c) {
+          const int col = ti.nt * kBN + c * 32;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            hg[i] = *reinterpret_cast<const int4*>(hrow + col + 8 * i);
+            hu[i] = *reinterpret_cast<const int4*>(hrow + args.ffn + col + 8 * i);
+          }
+        };
+        if (valid) fetch(0);
 #pragma unroll 1
         for (int c = 0; c < kBN / 32; ++c) {
           uint32_t a[32];
           tmem_ld32(t_row + c * 32, a);
+          float g[32], u[32];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const __nv_bfloat16* pg = reinterpret_cast<const __nv_bfloat16*>(&hg[i]);
+            const __nv_bfloat16* pu = reinterpret_cast<const __nv_bfloat16*>(&hu[i]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              g[8 * i + j] = __bfloat162float(pg[j]);
+              u[8 * i + j] = __bfloat162float(pu[j]);
+            }
+          }
+          if (valid && c + 1 < kBN / 32) fetch(c + 1);
           tmem_ld_wait();
           if (valid) {
             const int col = ti.nt * kBN + c * 32;
-            const __nv_bfloat16* hrow = reinterpret_cast<const __nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
-            float g[32], u[32], dg[32], du[32];
-            load_bf16x32(hrow + col, g);
-            load_bf16x32(hrow + args.ffn + col, u);
+            float dg[32], du[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float da = __uint_as_float(a[i]);
@@ -365,6 +399,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * (2 * args.ffn);
             store_bf16x32(drow + col, dg);
             store_bf16x32(drow + args.ffn + col, du);
+            if (args.aux_t) {  // dH^T (padded K-major) for the dW_in gradient GEMM
+              __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(args.aux_t) + prow;
+              store_t_bf16x32(t + (size_t)col * args.rp, args.rp, dg);
+              store_t_bf16x32(t + (size_t)(args.ffn + col) * args.rp, args.rp, du);
+            }
           }
         }
       } else {  // EPI_WGRAD: fp32 [M][N] per expert

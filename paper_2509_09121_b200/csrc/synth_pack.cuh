@@ -38,9 +38,9 @@ __device__ __forceinline__ int win_col_of_packed_row(int p, int f) {
   return i < 128 ? b * 128 + i : f + b * 128 + (i - 128);
 }
 
-__global__ void synth_bf16_kernel(uint64_t seed, int64_t n, float stddev, __nv_bfloat16* out) {
+__global__ void synth_bf16_kernel(uint64_t seed, int64_t n, float stddev, __nv_bfloat16* out, float shift = 0.0f) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = __float2bfloat16_rn(prng_normal_f(seed, i, stddev));
+    out[i] = __float2bfloat16_rn(prng_normal_f(seed, i, stddev) + shift);
 }
 __global__ void synth_f32_kernel(uint64_t seed, int64_t n, float stddev, float* out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -274,16 +274,18 @@ class MoELayer:
         return out
 
     # ---------------------------------------------------------------- per-stage timing
-    STAGES = ("router", "plan", "dispatch", "gemm1", "gemm2", "combine")
+    STAGES = ("router", "plan", "dispatch", "gemm1", "gemm2", "combine",
+              "combine_bwd", "dgrad1_swiglu_bwd", "dgrad2", "dispatch_bwd", "transposes", "wgrad_out", "wgrad_in")
 
     def profile(self, enable: bool = True):
         self._check(self.L.cl_moe_profile(self.h, int(enable)), "profile")
 
     def profile_read(self):
-        ms = (C.c_double * 6)()
-        calls = C.c_int64()
-        self._check(self.L.cl_moe_profile_read(self.h, ms, C.byref(calls)), "profile_read")
-        return {k: ms[i] for i, k in enumerate(self.STAGES)}, calls.value
+        """Summed per-stage ms since the last read, and (forward calls, backward calls)."""
+        ms = (C.c_double * 16)()
+        calls = (C.c_int64 * 2)()
+        self._check(self.L.cl_moe_profile_read(self.h, ms, calls), "profile_read")
+        return {k: ms[i] for i, k in enumerate(self.STAGES)}, (calls[0], calls[1])
 
     # ---------------------------------------------------------------- stage access (tests)
     def stage(self, name: str, shape, dtype) -> torch.Tensor:
@@ -293,10 +295,14 @@ class MoELayer:
                     "copy_stage")
         return out
 
-    def synthetic_tokens(self, t: int, seed: int) -> torch.Tensor:
+    def synthetic_tokens(self, t: int, seed: int, shift: float = 0.0) -> torch.Tensor:
         x = torch.empty(t, self.cfg.d_model, dtype=torch.bfloat16, device=self.device)
-        self._check(self.L.cl_moe_synthetic_tokens(self.h, seed, t, _ptr(x), _stream(self.device)), "synthetic_tokens")
+        self._check(self.L.cl_moe_synthetic_tokens_shifted(self.h, seed, t, shift, _ptr(x), _stream(self.device)),
+                    "synthetic_tokens")
         return x
+
+    def synthetic_skew(self, gamma: float):
+        self._check(self.L.cl_moe_synthetic_skew(self.h, gamma), "synthetic_skew")
 
     # ---------------------------------------------------------------- helpers
     def _bf16(self, x: torch.Tensor) -> torch.Tensor:

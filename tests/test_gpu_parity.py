@@ -294,3 +294,21 @@ def test_synthetic_weights_match_host_prng():
     assert (a == b).float().mean().item() > 0.999
     host.close()
     syn.close()
+
+
+def test_device_skew_construction_matches_oracle():
+    """cl_moe_synthetic_skew + shifted tokens reproduce make_inputs(skew=gamma) routing exactly."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 512, 512, 16, 2, 128
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, f, skew=1.8)
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t), seed=20261018)
+    lay.synthetic_skew(1.8)
+    x = lay.synthetic_tokens(t, 20261018, shift=1.0)
+    dec = lay.route_tokens(x)
+    lay.sync()
+    assert (x.float().cpu().numpy() == inp["x"]).mean() > 0.9999
+    r = o.route(x.float().cpu().numpy(), inp["w_router"], k)
+    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), r["topk_idx"])
+    assert dec.counts.cpu().numpy().max() > 0.25 * t * k  # hot expert
+    lay.close()
