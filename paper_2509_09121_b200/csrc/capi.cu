@@ -310,7 +310,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   }
 
   const int64_t rows = h->cap * h->K;
-  const int tpc = router_tokens_per_cta(static_cast<int>(h->N), 32);  // smallest tile of any variant
+  const int tpc = std::min(router_tokens_per_cta(static_cast<int>(h->N), 32),
+                           RouterBigSmem(static_cast<int>(h->N), 32, 3).tpc);  // smallest tile of any variant
   h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
   RouteBufs& rb = h->rb;
   rb.logits = dalloc<float>(h->cap * h->N);
@@ -340,6 +341,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->wr64 = dalloc<double>(h->d * ((h->N + 3) / 4 * 4));
   CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);
@@ -384,15 +386,20 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   if (T < 1) throw RunErr("route_tokens: B must be >= 1");
   if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
   const int N = static_cast<int>(h->N);
-  // small batches: 32-thread CTAs with an 8-deep prefetch ring (latency); large: 128-thread CTAs
-  const bool small = (T + router_tokens_per_cta(N, 128) - 1) / router_tokens_per_cta(N, 128) < 2 * h->num_sms &&
-                     router_smem_bytes(N, 32, 8) <= 220 * 1024;
-  const int tpc = router_tokens_per_cta(N, small ? 32 : 128);
+  // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
+  // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
+  const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
+  const bool big = (T + tpc_big - 1) / tpc_big >= 2 * h->num_sms && RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  const bool small = !big && router_smem_bytes(N, 32, 8) <= 220 * 1024;
+  const int tpc = big ? tpc_big : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   prof_begin(h, st);
-  if (small)
+  if (big)
+    router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (small)
     router_kernel<32, 8><<<n_tiles, 32, router_smem_bytes(N, 32, 8), st>>>(
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   else

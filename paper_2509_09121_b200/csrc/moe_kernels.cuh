@@ -72,6 +72,75 @@ __global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, 
   }
 }
 
+// Per-token softmax (fp64, tensor.cpp:614-621), top-K with lowest-index tie-break
+// (tensor.cpp:1046-1060), renormalised combine weights, and the per-tile
+// statistics (expert counts, local ranks, prob sums, lse^2 sums) of one router tile whose fp32
+// logits sit in slog[tpc][N4]. Called by all threads of the CTA after a barrier.
+__device__ __forceinline__ void router_finish(int tile, int tok0, int tpc, int T, int N, int N4, int K, float* slog,
+                                              int* sidx, double* slse, const RouteBufs& rb, int nthreads) {
+  const int ntok = min(tpc, T - tok0);
+  for (int tl = threadIdx.x; tl < tpc; tl += nthreads) {
+    double lse2 = 0.0;
+    if (tl < ntok) {
+      const int j = tok0 + tl;
+      float* zrow = slog + tl * N4;
+      double mx = zrow[0];
+      for (int e = 1; e < N; ++e) mx = fmax(mx, static_cast<double>(zrow[e]));
+      double denom = 0.0;
+      for (int e = 0; e < N; ++e) denom += exp(static_cast<double>(zrow[e]) - mx);
+      float* p = rb.probs + (size_t)j * N;
+      for (int e = 0; e < N; ++e) {
+        const float pe = static_cast<float>(exp(static_cast<double>(zrow[e]) - mx) / denom);
+        p[e] = pe;
+        zrow[e] = pe;  // the row now holds probs
+      }
+      const double lse = mx + log(denom);
+      lse2 = lse * lse;
+      uint64_t taken_lo = 0, taken_hi = 0;
+      float vals[8];
+      int ids[8];
+      for (int k = 0; k < K; ++k) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < N; ++e) {
+          const bool tk = e < 64 ? ((taken_lo >> e) & 1ull) : ((taken_hi >> (e - 64)) & 1ull);
+          if (tk) continue;
+          const float v = zrow[e];
+          if (best < 0 || v > bv) { best = e; bv = v; }  // strict '>' keeps the lowest index on ties
+        }
+        if (best < 64) taken_lo |= 1ull << best; else taken_hi |= 1ull << (best - 64);
+        vals[k] = bv;
+        ids[k] = best;
+      }
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s += static_cast<double>(vals[k]);
+      for (int k = 0; k < K; ++k) {
+        rb.topk_idx[(size_t)j * K + k] = ids[k];
+        rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / s);
+        sidx[tl * 8 + k] = ids[k];
+      }
+    }
+    slse[tl] = lse2;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += nthreads) {
+    int cnt = 0;
+    double ps = 0.0;
+    for (int t = 0; t < ntok; ++t) {
+      ps += static_cast<double>(slog[t * N4 + e]);
+      for (int k = 0; k < K; ++k)
+        if (sidx[t * 8 + k] == e) rb.local_rank[(size_t)(tok0 + t) * K + k] = cnt++;
+    }
+    rb.tile_cnt[(size_t)tile * N + e] = cnt;
+    rb.tile_psum[(size_t)tile * N + e] = ps;
+  }
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < ntok; ++t) a += slse[t];
+    rb.tile_lse2[tile] = a;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K1: router. logits = x W_r with one fp64 accumulator per (token, expert) summed over the
 // hidden dimension in ascending order — the exact accumulation order of the reference gemm_nn
@@ -208,70 +277,135 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
   }
   __syncthreads();
 
-  // ---- per-token softmax / top-K ----
-  const int ntok = min(tpc, T - tok0);
-  for (int tl = threadIdx.x; tl < tpc; tl += kRouterThreads) {
-    double lse2 = 0.0;
-    if (tl < ntok) {
-      const int j = tok0 + tl;
-      float* zrow = slog + tl * N4;
-      double mx = zrow[0];
-      for (int e = 1; e < N; ++e) mx = fmax(mx, static_cast<double>(zrow[e]));
-      double denom = 0.0;
-      for (int e = 0; e < N; ++e) denom += exp(static_cast<double>(zrow[e]) - mx);
-      float* p = rb.probs + (size_t)j * N;
-      for (int e = 0; e < N; ++e) {
-        const float pe = static_cast<float>(exp(static_cast<double>(zrow[e]) - mx) / denom);
-        p[e] = pe;
-        zrow[e] = pe;  // the row now holds probs
-      }
-      const double lse = mx + log(denom);
-      lse2 = lse * lse;
-      uint64_t taken_lo = 0, taken_hi = 0;
-      float vals[8];
-      int ids[8];
-      for (int k = 0; k < K; ++k) {
-        int best = -1;
-        float bv = 0.0f;
-        for (int e = 0; e < N; ++e) {
-          const bool tk = e < 64 ? ((taken_lo >> e) & 1ull) : ((taken_hi >> (e - 64)) & 1ull);
-          if (tk) continue;
-          const float v = zrow[e];
-          if (best < 0 || v > bv) { best = e; bv = v; }  // strict '>' keeps the lowest index on ties
+  router_finish(tile, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb, kRouterThreads);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1, large-batch variant: one thread owns 4 tokens x 4 experts (16 independent fp64 chains, each
+// still summed over l in ascending order — bit-identical to the reference gemm_nn). x rows stay
+// raw bf16 in shared memory (16-byte chunks XOR-swizzled by token group so the per-token 16-byte
+// loads of a quarter-warp hit distinct banks) and are widened in registers, amortised over the
+// 4 experts; the fp64 copy of W_r streams through a cp.async ring. Shared-memory traffic is
+// ~1.25 wavefronts per 64 DFMA instead of ~5 in the 1x4 layout.
+struct RouterBigSmem {
+  int tpc, N4;
+  size_t rx, sw, slog, sidx, slse, total;
+  __host__ __device__ RouterBigSmem(int n_experts, int threads, int stages) {
+    N4 = (n_experts + 3) / 4 * 4;
+    tpc = (threads / (N4 / 4)) * 4;
+    rx = 0;
+    sw = rx + (size_t)stages * tpc * kRouterChunk * 2;
+    slog = sw + (size_t)stages * sizeof(double) * kRouterChunk * N4;
+    sidx = slog + sizeof(float) * tpc * N4;
+    slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
+    total = slse + sizeof(double) * tpc;
+  }
+};
+
+template <int kThreads, int kStages>
+__global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                 const double* __restrict__ wr64, int T, int d, int N,
+                                                                 int K, RouteBufs rb) {
+  const RouterBigSmem L(N, kThreads, kStages);
+  const int N4 = L.N4;
+  const int groups = N4 / 4;
+  const int tg_per_cta = kThreads / groups;
+  const int tpc = L.tpc;
+  const int tile = blockIdx.x;
+  const int tok0 = tile * tpc;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* rawx = smem_raw + L.rx;                               // [stages][tpc][128 B] swizzled
+  double* sw = reinterpret_cast<double*>(smem_raw + L.sw);       // [stages][chunk][N4]
+  float* slog = reinterpret_cast<float*>(smem_raw + L.slog);
+  int* sidx = reinterpret_cast<int*>(smem_raw + L.sidx);
+  double* slse = reinterpret_cast<double*>(smem_raw + L.slse);
+  const int tg = threadIdx.x / groups;
+  const int g = threadIdx.x % groups;
+  const bool worker = tg < tg_per_cta;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+
+  const int nchunks = d / kRouterChunk;
+  const int xpieces = tpc * 8;  // 8 x 16-byte chunks per token row per stage
+  const int wpieces = kRouterChunk * N4 / 2;
+  auto issue = [&](int c, int buf) {
+    const int c0 = c * kRouterChunk;
+    for (int i = threadIdx.x; i < xpieces; i += kThreads) {
+      const int r = i >> 3, q = i & 7;
+      const bool ok = tok0 + r < T;
+      const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
+      const int qs = q ^ ((r >> 2) & 7);
+      cp_async16(rawx + ((size_t)buf * tpc + r) * 128 + qs * 16, src, ok);
+    }
+    const double* wsrc = wr64 + (size_t)c0 * N4;
+    for (int i = threadIdx.x; i < wpieces; i += kThreads)
+      cp_async16(sw + (size_t)buf * kRouterChunk * N4 + i * 2, wsrc + i * 2, true);
+    cp_async_commit();
+  };
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < nchunks) issue(c, c);
+    else cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c % kStages;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
+    else cp_async_commit();
+    if (worker) {
+      const uint8_t* xb = rawx + (size_t)buf * tpc * 128;
+      const double2* wv = reinterpret_cast<const double2*>(sw + (size_t)buf * kRouterChunk * N4 + g * 4);
+#pragma unroll 1
+      for (int q = 0; q < kRouterChunk / 8; ++q) {
+        // 8 l-columns of the 4 tokens, widened to fp64 once for all 4 experts
+        double xd[4][8];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int r = tg * 4 + a;
+          const int4 raw = *reinterpret_cast<const int4*>(xb + (size_t)r * 128 + ((q ^ ((r >> 2) & 7)) * 16));
+          const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xd[a][i] = static_cast<double>(__bfloat162float(hv[i]));
         }
-        if (best < 64) taken_lo |= 1ull << best; else taken_hi |= 1ull << (best - 64);
-        vals[k] = bv;
-        ids[k] = best;
-      }
-      double s = 0.0;
-      for (int k = 0; k < K; ++k) s += static_cast<double>(vals[k]);
-      for (int k = 0; k < K; ++k) {
-        rb.topk_idx[(size_t)j * K + k] = ids[k];
-        rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / s);
-        sidx[tl * 8 + k] = ids[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int l = q * 8 + i;
+          const double2 w01 = wv[l * (N4 / 2)];
+          const double2 w23 = wv[l * (N4 / 2) + 1];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            acc[a][0] = fma(xd[a][i], w01.x, acc[a][0]);
+            acc[a][1] = fma(xd[a][i], w01.y, acc[a][1]);
+            acc[a][2] = fma(xd[a][i], w23.x, acc[a][2]);
+            acc[a][3] = fma(xd[a][i], w23.y, acc[a][3]);
+          }
+        }
       }
     }
-    slse[tl] = lse2;
   }
   __syncthreads();
-
-  // ---- per-tile statistics: expert counts, local ranks, prob sums (one thread per expert) ----
-  for (int e = threadIdx.x; e < N; e += kRouterThreads) {
-    int cnt = 0;
-    double ps = 0.0;
-    for (int t = 0; t < ntok; ++t) {
-      ps += static_cast<double>(slog[t * N4 + e]);
-      for (int k = 0; k < K; ++k)
-        if (sidx[t * 8 + k] == e) rb.local_rank[(size_t)(tok0 + t) * K + k] = cnt++;
+  if (worker) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int tl = tg * 4 + a;
+      const int tok = tok0 + tl;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int e = g * 4 + b;
+        const float z = static_cast<float>(acc[a][b]);
+        slog[tl * N4 + e] = z;
+        if (tok < T && e < N) {
+          rb.logits[(size_t)tok * N + e] = z;
+          if (!isfinite(z)) atomicExch(rb.finite_flag, 1);
+        }
+      }
     }
-    rb.tile_cnt[(size_t)tile * N + e] = cnt;
-    rb.tile_psum[(size_t)tile * N + e] = ps;
   }
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int t = 0; t < ntok; ++t) a += slse[t];
-    rb.tile_lse2[tile] = a;
-  }
+  __syncthreads();
+  router_finish(tile, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb, kThreads);
 }
 
 // ---------------------------------------------------------------------------------------

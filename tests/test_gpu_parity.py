@@ -47,7 +47,10 @@ def _rel(out, ref):
     return rf, rm
 
 
-@pytest.mark.parametrize("t,d,n,k", [(300, 256, 8, 2), (1000, 512, 16, 2), (257, 256, 16, 4), (64, 1024, 8, 1)])
+# T=10000 / N=16 and T=20000 / N=8 select the large-batch router variant (4 tokens x 4 experts per
+# thread); the others the small-batch one.
+@pytest.mark.parametrize("t,d,n,k", [(300, 256, 8, 2), (1000, 512, 16, 2), (257, 256, 16, 4), (64, 1024, 8, 1),
+                                     (10000, 256, 16, 2), (20000, 256, 8, 2), (9999, 512, 32, 4)])
 def test_route_tokens_bit_exact(t, d, n, k):
     o = Oracle("port")
     inp = make_inputs(t, d, n, 128, experts=False)
