@@ -120,10 +120,11 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, i
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+  const uint64_t pol = l2_policy_evict_first();
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                 pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+    st_global_v4_hint(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                      pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]), pol);
 }
 __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v) {
 #pragma unroll
@@ -153,6 +154,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr uint32_t kIdesc = idesc_f32acc<kFp8>(Cfg::kBM, kBN);
   constexpr int kElemBytes = kFp8 ? 1 : 2;
   constexpr int kBKElems = kBKBytes / kElemBytes;
+  // Row-grouped: the A rows of an expert are re-read for every n-block -> keep them in L2.
+  constexpr uint64_t kAHint = kWgrad ? kEvictNormal : kEvictLast;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -219,11 +222,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty[s], ph ^ 1);
           if constexpr (kCtaGroup == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
-            tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kEvictNormal);
+            tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
             tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
           } else {
             if (cta_rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
-            tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kEvictNormal);
+            tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
             tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
           }
           if (++s == S) { s = 0; ph ^= 1; }
