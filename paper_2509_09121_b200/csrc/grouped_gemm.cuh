@@ -55,7 +55,8 @@ struct GemmArgs {
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
 };
 
-constexpr int kGemmThreads = 256;
+constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
+constexpr int kEpiWarps = 8;      // two warps per TMEM lane quarter, each owning half of the columns
 constexpr int kBN = 256;                 // MMA N (output columns of one tile, pre-SwiGLU)
 constexpr int kBKBytes = 128;            // one swizzle atom along K
 constexpr int kMaxExperts = 256;
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4 * kCtaGroup);
+      mbar_init(&tempty[a], kEpiWarps * kCtaGroup);
     }
     fence_mbar_init();
   }
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp >= 4) {
     // ===================== epilogue: TMEM -> registers -> global =====================
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (warp - 4) >> 2;  // which half of the tile's columns this warp handles
     const int row_in_cta = q * 32 + lane;
     int acc = 0;
     uint32_t aph = 0;
@@ -291,9 +293,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           wsg = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
           wsu = wsg + kBN / 2;
         }
-        if constexpr (kOutFp8) so = args.out_scale[ti.e];
+        if constexpr (kOutFp8) so = 1.0f / args.out_scale[ti.e];  // act / s_mid as a multiply
 #pragma unroll 1
-        for (int c = 0; c < kBN / 2 / 32; ++c) {
+        for (int c = half * (kBN / 64 / 2); c < (half + 1) * (kBN / 64 / 2); ++c) {
           uint32_t g[32], u[32];
           tmem_ld32(t_row + c * 32, g);
           tmem_ld32(t_row + kBN / 2 + c * 32, u);
@@ -316,9 +318,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
                 const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-                    make_float2(__fdiv_rn(v[4 * i], so), __fdiv_rn(v[4 * i + 1], so)), __NV_SATFINITE, __NV_E4M3);
+                    make_float2(v[4 * i] * so, v[4 * i + 1] * so), __NV_SATFINITE, __NV_E4M3);
                 const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-                    make_float2(__fdiv_rn(v[4 * i + 2], so), __fdiv_rn(v[4 * i + 3], so)), __NV_SATFINITE, __NV_E4M3);
+                    make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
                 p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
               }
               uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ws = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
         }
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = half * (kBN / 64); c < (half + 1) * (kBN / 64); ++c) {
           uint32_t a[32];
           tmem_ld32(t_row + c * 32, a);
           tmem_ld_wait();
@@ -371,9 +373,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             hu[i] = *reinterpret_cast<const int4*>(hrow + args.ffn + col + 8 * i);
           }
         };
-        if (valid) fetch(0);
+        const int c_begin = half * (kBN / 64), c_end = (half + 1) * (kBN / 64);
+        if (valid) fetch(c_begin);
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = c_begin; c < c_end; ++c) {
           uint32_t a[32];
           tmem_ld32(t_row + c * 32, a);
           float g[32], u[32];
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               u[8 * i + j] = __bfloat162float(pu[j]);
             }
           }
-          if (valid && c + 1 < kBN / 32) fetch(c + 1);
+          if (valid && c + 1 < c_end) fetch(c + 1);
           tmem_ld_wait();
           if (valid) {
             const int col = ti.nt * kBN + c * 32;
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         float* base = reinterpret_cast<float*>(args.out) + (size_t)ti.e * args.out_estride + (size_t)row * args.ldo +
                       ti.nt * kBN;
 #pragma unroll 1
-        for (int c = 0; c < kBN / 32; ++c) {
+        for (int c = half * (kBN / 64); c < (half + 1) * (kBN / 64); ++c) {
           uint32_t a[32];
           if (has_acc) {
             tmem_ld32(t_row + c * 32, a);
