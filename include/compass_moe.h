@@ -188,6 +188,15 @@ cl_status cl_moe_forward_train(cl_moe* h, const void* hidden, int64_t T, void* o
 cl_status cl_moe_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_combine_w,
                           float* dw_in, float* dw_out, void* stream);
 
+/* Full layer backward of the last cl_moe_forward_train, router included:
+ * gradient of  sum(out * d_out) + g_aux * L_aux + g_z * L_Z  (the total-loss coefficients of
+ * SPEC.md:183-188) with respect to hidden (d_hidden, bf16, expert + router paths summed in fp32),
+ * W_r (dw_router [d x N] fp32), W_in / W_out (as cl_moe_backward); d_combine_w optional (NULL).
+ * The hidden tensor of the forward call must still be valid. top_k in {1, 2, 4}. */
+cl_status cl_moe_backward_full(cl_moe* h, const void* d_out, float g_aux, float g_z, void* d_hidden,
+                               float* dw_router, float* dw_in, float* dw_out, float* d_combine_w,
+                               void* stream);
+
 /* ---- Expert parallelism. One process per GPU; cfg.ep_size ranks, rank
  * cfg.ep_rank owns experts [rank*N/ep_size, (rank+1)*N/ep_size) (pass only those experts'
  * weights to cl_moe_create). Every rank routes its own tokens over all N experts; rows travel

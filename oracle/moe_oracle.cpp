@@ -482,6 +482,61 @@ int orc_moe_backward(const float* x, std::int64_t T, std::int64_t d, std::int64_
   return 0;
 }
 
+// ---- router backward --------------------------------------
+// Gradient of  sum_jk d_cw[j,k] * w[j,k]  +  g_aux * L_aux  +  g_z * L_Z  with respect to the router
+// logits, then through matmul(x, W_r). Analytic, in fp64 (the reference Tape composition of the
+// same function -- gather_cols_per_row, row_sums, recip, mul_rowwise (tensor.cpp:847-874, :510-543,
+// :324-328, :572-610), moe_aux_loss / z_loss backward (:998-1006, :1026-1037), softmax_rows
+// backward (:641-652), matmul backward (:364-372) -- is compared in tests with a 1e-5 tolerance):
+//   w_k = v_k / s, s = sum_k v_k, v_k = p[idx_k]:   dv_k = (d_cw_k - sum_k' d_cw_k' w_k') / s
+//   dp_i = sum_{k: idx_k = i} dv_k + g_aux * N / (B^2 K) * c_i
+//   dz_i = p_i (dp_i - sum_i' dp_i' p_i') + g_z * 2 lse / B * p_i
+//   dx += dz W_r^T (added into dx_accum),  dW_r = x^T dz.
+int orc_router_backward(const float* x, const float* wr, std::int64_t T, std::int64_t d, std::int64_t N,
+                        std::int64_t K, const float* logits, const float* probs, const std::int64_t* idx,
+                        const std::int64_t* counts, const float* d_cw, float g_aux, float g_z, float* dx_accum,
+                        float* dw_router) {
+  if (T == 0) return fail("router_backward: empty batch");
+  std::vector<double> dz(static_cast<std::size_t>(T * N));
+  const double coef = static_cast<double>(N) / (static_cast<double>(T) * T * static_cast<double>(K));
+  for (std::int64_t j = 0; j < T; ++j) {
+    const float* p = probs + j * N;
+    const float* zr = logits + j * N;
+    double s = 0.0;
+    for (std::int64_t k = 0; k < K; ++k) s += p[idx[j * K + k]];
+    double dot_w = 0.0;
+    for (std::int64_t k = 0; k < K; ++k) dot_w += static_cast<double>(d_cw[j * K + k]) * (p[idx[j * K + k]] / s);
+    std::vector<double> dp(static_cast<std::size_t>(N), 0.0);
+    for (std::int64_t k = 0; k < K; ++k)
+      dp[static_cast<std::size_t>(idx[j * K + k])] += (static_cast<double>(d_cw[j * K + k]) - dot_w) / s;
+    for (std::int64_t i = 0; i < N; ++i) dp[static_cast<std::size_t>(i)] += g_aux * coef * static_cast<double>(counts[i]);
+    double dot = 0.0;
+    for (std::int64_t i = 0; i < N; ++i) dot += dp[static_cast<std::size_t>(i)] * p[i];
+    double mx = zr[0];
+    for (std::int64_t i = 1; i < N; ++i) mx = std::max(mx, static_cast<double>(zr[i]));
+    double den = 0.0;
+    for (std::int64_t i = 0; i < N; ++i) den += std::exp(static_cast<double>(zr[i]) - mx);
+    const double lse = mx + std::log(den);
+    for (std::int64_t i = 0; i < N; ++i)
+      dz[static_cast<std::size_t>(j * N + i)] =
+          p[i] * (dp[static_cast<std::size_t>(i)] - dot) + g_z * 2.0 * lse / static_cast<double>(T) * p[i];
+  }
+  for (std::int64_t j = 0; j < T; ++j)
+    for (std::int64_t l = 0; l < d; ++l) {
+      double a = 0.0;
+      for (std::int64_t i = 0; i < N; ++i) a += dz[static_cast<std::size_t>(j * N + i)] * wr[l * N + i];
+      dx_accum[j * d + l] = static_cast<float>(dx_accum[j * d + l] + a);
+    }
+  std::vector<double> acc(static_cast<std::size_t>(d * N), 0.0);
+  for (std::int64_t j = 0; j < T; ++j)
+    for (std::int64_t l = 0; l < d; ++l) {
+      const double xv = x[j * d + l];
+      for (std::int64_t i = 0; i < N; ++i) acc[static_cast<std::size_t>(l * N + i)] += xv * dz[static_cast<std::size_t>(j * N + i)];
+    }
+  for (std::size_t i = 0; i < acc.size(); ++i) dw_router[i] = static_cast<float>(acc[i]);
+  return 0;
+}
+
 // ---- FP8 E4M3 quantize-dequantize -----------------------------------------
 // q = x/scale in float; RNE onto the enumerated E4M3 grid (ties to the even code), |q| > 448
 // clamps to +-448; result q_hat * scale in float. Non-finite input is an error.

@@ -75,8 +75,12 @@ class Oracle:
             L.orc_expert_ffn.argtypes = [_f32p, _i64, _i64, _i64, _f32p, _f32p, C.c_void_p, _f32p]
             L.orc_fp8_qdq.argtypes = [_f32p, _i64, C.c_float, _f32p]
             L.orc_fp8_encode.argtypes = [_f32p, _i64, _u8p]
+            L.orc_router_backward.argtypes = [_f32p, _f32p, _i64, _i64, _i64, _i64, _f32p, _f32p, _i64p, _i64p, _f32p,
+                                              C.c_float, C.c_float, _f32p, _f32p]
         else:
             L.ref_gradcheck.argtypes = [C.c_uint64, C.c_int, C.c_double, C.POINTER(C.c_int)]
+            L.ref_moe_backward_full.argtypes = [_f32p, _f32p, _i64, _i64, _i64, _i64, _i64, _f32p, _f32p, _f32p,
+                                                C.c_float, C.c_float, _f32p, _f32p, _f32p, _f32p]
 
     def _call(self, name, *args):
         rc = getattr(self.lib, self._p + name)(*args)
@@ -158,6 +162,28 @@ class Oracle:
             args.append(jobs)
         self._call("moe_backward", *args)
         return dh, dcw, dwi, dwo
+
+    def moe_backward_full(self, x, wr, w_in, w_out, d_out, g_aux, g_z, k, jobs: int = 1):
+        """Layer + router backward: (d_hidden, dW_r, dW_in, dW_out). "reference": the Tape over the
+        reference ops; "port": orc_moe_backward + orc_router_backward (analytic router part)."""
+        x = np.ascontiguousarray(x, np.float32)
+        wr = np.ascontiguousarray(wr, np.float32)
+        t, d = x.shape
+        n, _, f2 = w_in.shape
+        dh = np.empty((t, d), np.float32)
+        dwr = np.empty((d, n), np.float32)
+        dwi = np.empty((n, d, f2), np.float32)
+        dwo = np.empty((n, f2 // 2, d), np.float32)
+        d_out = np.ascontiguousarray(d_out, np.float32)
+        if self.kind == "reference":
+            self._call("moe_backward_full", x, wr, t, d, n, k, f2 // 2, np.ascontiguousarray(w_in, np.float32),
+                       np.ascontiguousarray(w_out, np.float32), d_out, g_aux, g_z, dh, dwr, dwi, dwo)
+            return dh, dwr, dwi, dwo
+        r = self.route(x, wr, k)
+        dh, dcw, dwi, dwo = self.moe_backward(x, w_in, w_out, r["topk_idx"], r["combine_weights"], d_out, jobs=jobs)
+        self._call("router_backward", x, wr, t, d, n, k, r["logits"], r["probs"], r["topk_idx"], r["counts"], dcw,
+                   g_aux, g_z, dh, dwr)
+        return dh, dwr, dwi, dwo
 
     # ---- port-only helpers ----
     def expert_ffn(self, xe, w_in_e, w_out_e):

@@ -198,6 +198,66 @@ int ref_moe_backward(const float* x, std::int64_t T, std::int64_t d, std::int64_
   });
 }
 
+// Full training step of the layer through the reference Tape, router included:
+//   z = matmul(x, W_r); p = softmax_rows(z); vals = gather_cols_per_row(p, idx, K);
+//   w = mul_rowwise(vals, recip(row_sums(vals)))          (renormalised top-K, differentiable)
+//   per expert: w_e = gather_elems_col(w, slots_e), the expert chain, mul_rowwise(y, w_e),
+//   scatter_add_rows, add; loss = sum(out * stop(dOut)) + g_aux * moe_aux_loss(p, c, K)
+//   + g_z * z_loss(z). Outputs dx, dW_r, dW_in, dW_out.
+int ref_moe_backward_full(const float* x, const float* wr, std::int64_t T, std::int64_t d, std::int64_t N,
+                          std::int64_t K, std::int64_t f, const float* w_in, const float* w_out, const float* d_out,
+                          float g_aux, float g_z, float* d_hidden, float* dw_router, float* dw_in, float* dw_out) {
+  return guarded([&] {
+    Tensor xt = Tensor::param({T, d}, vec(x, T * d));
+    Tensor wrt = Tensor::param({d, N}, vec(wr, d * N));
+    std::vector<Tensor> win(static_cast<std::size_t>(N)), wout(static_cast<std::size_t>(N));
+    Tape tape;
+    Tape::Scope scope(tape);
+    Tensor z = ops::matmul(xt, wrt);
+    Tensor p = ops::softmax_rows(z);
+    std::vector<std::int64_t> idx(static_cast<std::size_t>(T * K));
+    std::vector<float> val(static_cast<std::size_t>(K));
+    std::vector<std::int64_t> counts(static_cast<std::size_t>(N), 0);
+    for (std::int64_t j = 0; j < T; ++j) {
+      ops::top_k(p.values().data() + j * N, N, K, idx.data() + j * K, val.data());
+      for (std::int64_t k = 0; k < K; ++k) counts[static_cast<std::size_t>(idx[j * K + k])] += 1;
+    }
+    Tensor vals = ops::gather_cols_per_row(p, idx, K);
+    Tensor w = ops::mul_rowwise(vals, ops::recip(ops::row_sums(vals)));
+    std::vector<std::vector<std::int64_t>> rows(static_cast<std::size_t>(N));
+    std::vector<std::vector<std::pair<std::int64_t, std::int64_t>>> coords(static_cast<std::size_t>(N));
+    for (std::int64_t j = 0; j < T; ++j)
+      for (std::int64_t k = 0; k < K; ++k) {
+        rows[static_cast<std::size_t>(idx[j * K + k])].push_back(j);
+        coords[static_cast<std::size_t>(idx[j * K + k])].push_back({j, k});
+      }
+    Tensor acc = Tensor::zeros({T, d});
+    for (std::int64_t e = 0; e < N; ++e) {
+      win[static_cast<std::size_t>(e)] = Tensor::param({d, 2 * f}, vec(w_in + e * d * 2 * f, d * 2 * f));
+      wout[static_cast<std::size_t>(e)] = Tensor::param({f, d}, vec(w_out + e * f * d, f * d));
+      const auto& re = rows[static_cast<std::size_t>(e)];
+      if (re.empty()) continue;
+      Tensor xe = ops::gather_rows(xt, re);
+      Tensor h = ops::matmul(xe, win[static_cast<std::size_t>(e)]);
+      Tensor a = ops::mul(ops::silu(ops::slice_cols(h, 0, f)), ops::slice_cols(h, f, 2 * f));
+      Tensor y = ops::matmul(a, wout[static_cast<std::size_t>(e)]);
+      Tensor yw = ops::mul_rowwise(y, ops::gather_elems_col(w, coords[static_cast<std::size_t>(e)]));
+      acc = ops::add(acc, ops::scatter_add_rows(T, yw, re));
+    }
+    Tensor g = Tensor::from_values({T, d}, vec(d_out, T * d));
+    Tensor loss = ops::add(ops::add(ops::sum_all(ops::mul(acc, ops::stop_grad(g))),
+                                    ops::scale(ops::moe_aux_loss(p, counts, K), g_aux)),
+                           ops::scale(ops::z_loss(z), g_z));
+    tape.backward(loss);
+    std::memcpy(d_hidden, xt.grad().data(), sizeof(float) * T * d);
+    std::memcpy(dw_router, wrt.grad().data(), sizeof(float) * d * N);
+    for (std::int64_t e = 0; e < N; ++e) {
+      std::memcpy(dw_in + e * d * 2 * f, win[static_cast<std::size_t>(e)].grad().data(), sizeof(float) * d * 2 * f);
+      std::memcpy(dw_out + e * f * d, wout[static_cast<std::size_t>(e)].grad().data(), sizeof(float) * f * d);
+    }
+  });
+}
+
 // The reference's own finite-difference gradient suite (gradcheck.cpp:610-656); returns the
 // number of failing ops (0 = all pass) and the number of ops checked in *n_ops.
 int ref_gradcheck(std::uint64_t seed, int cases, double tol, int* n_ops) {

@@ -144,4 +144,112 @@ __global__ void __launch_bounds__(256) transpose_weight_kernel(const __nv_bfloat
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Router backward. One thread per token:
+//   dv_k = (d_cw_k - sum_k' d_cw_k' w_k') / s,  s = sum_k p[idx_k]      (renormalised top-K)
+//   dp_i = sum_{k: idx_k=i} dv_k + g_aux * N/(B^2 K) * c_i             (moe_aux_loss bwd)
+//   dz_i = p_i (dp_i - <dp, p>) + g_z * 2 lse / B * p_i                (softmax / z_loss bwd)
+__global__ void router_bwd_dz_kernel(const float* __restrict__ probs, const float* __restrict__ logits,
+                                     const int32_t* __restrict__ idx, const float* __restrict__ d_cw,
+                                     const int32_t* __restrict__ counts, int T, int N, int K, float g_aux, float g_z,
+                                     float* __restrict__ dz) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= T) return;
+  const float* p = probs + (size_t)j * N;
+  const float* zr = logits + (size_t)j * N;
+  double s = 0.0;
+  for (int k = 0; k < K; ++k) s += p[idx[(size_t)j * K + k]];
+  double dot_w = 0.0;
+  for (int k = 0; k < K; ++k) dot_w += static_cast<double>(d_cw[(size_t)j * K + k]) * (p[idx[(size_t)j * K + k]] / s);
+  const double coef = static_cast<double>(N) / (static_cast<double>(T) * T * static_cast<double>(K));
+  double mx = zr[0];
+  for (int i = 1; i < N; ++i) mx = fmax(mx, static_cast<double>(zr[i]));
+  double den = 0.0;
+  for (int i = 0; i < N; ++i) den += exp(static_cast<double>(zr[i]) - mx);
+  const double lse = mx + log(den);
+  // dp is sparse except for the dense aux term: dot = sum_i dp_i p_i computed on the fly
+  double dot = 0.0;
+  for (int i = 0; i < N; ++i) dot += g_aux * coef * static_cast<double>(counts[i]) * p[i];
+  for (int k = 0; k < K; ++k) {
+    const int i = idx[(size_t)j * K + k];
+    dot += (static_cast<double>(d_cw[(size_t)j * K + k]) - dot_w) / s * p[i];
+  }
+  for (int i = 0; i < N; ++i) {
+    double dpi = g_aux * coef * static_cast<double>(counts[i]);
+    for (int k = 0; k < K; ++k)
+      if (idx[(size_t)j * K + k] == i) dpi += (static_cast<double>(d_cw[(size_t)j * K + k]) - dot_w) / s;
+    dz[(size_t)j * N + i] =
+        static_cast<float>(p[i] * (dpi - dot) + g_z * 2.0 * lse / static_cast<double>(T) * p[i]);
+  }
+}
+
+// dW_r partials: grid (d/64, T-chunks, ceil(N4/16)); thread = (l, 4 experts); fp32 partial sums over
+// the chunk's tokens, reduced in a fixed order by router_wgrad_reduce_kernel (deterministic).
+constexpr int kRwTokens = 512;
+__global__ void __launch_bounds__(256) router_wgrad_partial_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const float* __restrict__ dz, int T, int d, int N,
+                                                                   float* __restrict__ part) {
+  const int l = blockIdx.x * 64 + threadIdx.x / 4;
+  const int e0 = blockIdx.z * 16 + (threadIdx.x % 4) * 4;
+  const int t0 = blockIdx.y * kRwTokens;
+  const int t1 = min(T, t0 + kRwTokens);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (l < d) {
+    for (int j = t0; j < t1; ++j) {
+      const float xv = __bfloat162float(x[(size_t)j * d + l]);
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (e0 + b < N) acc[b] = fmaf(xv, dz[(size_t)j * N + e0 + b], acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (e0 + b < N) part[((size_t)blockIdx.y * d + l) * N + e0 + b] = acc[b];
+  }
+}
+__global__ void router_wgrad_reduce_kernel(const float* __restrict__ part, int chunks, int dn, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dn) return;
+  float a = 0.0f;
+  for (int c = 0; c < chunks; ++c) a += part[(size_t)c * dn + i];
+  out[i] = a;
+}
+
+// Dispatch backward with the router term fused: d_hidden[j] = sum_k dX[inv[j,k]] +
+// sum_e dz[j][e] W_r[:, e]  (fp32 accumulation, one rounding to bf16). One warp per token.
+template <int kK>
+__global__ void __launch_bounds__(256) dispatch_bwd_router_kernel(const __nv_bfloat16* __restrict__ dx,
+                                                                  const int32_t* __restrict__ inv, int T, int d,
+                                                                  const float* __restrict__ dz,
+                                                                  const float* __restrict__ wr, int N,
+                                                                  __nv_bfloat16* __restrict__ out) {
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= T) return;
+  const int4* src[kK];
+#pragma unroll
+  for (int k = 0; k < kK; ++k) src[k] = reinterpret_cast<const int4*>(dx + (size_t)inv[(size_t)j * kK + k] * d);
+  const float* dzj = dz + (size_t)j * N;
+  for (int v = lane; v < d / 8; v += 32) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < kK; ++k) {
+      const int4 raw = ld_nc_v4(src[k] + v);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += __bfloat162float(h[i]);
+    }
+    for (int e = 0; e < N; ++e) {
+      const float g = dzj[e];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(g, wr[(size_t)(8 * v + i) * N + e], acc[i]);
+    }
+    int4 o;
+    o.x = pack_bf16(acc[0], acc[1]);
+    o.y = pack_bf16(acc[2], acc[3]);
+    o.z = pack_bf16(acc[4], acc[5]);
+    o.w = pack_bf16(acc[6], acc[7]);
+    st_na_v4(reinterpret_cast<int4*>(out + (size_t)j * d) + v, o);
+  }
+}
+
 }  // namespace cmoe

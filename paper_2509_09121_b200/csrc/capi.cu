@@ -167,6 +167,7 @@ struct cl_moe {
   // training (expert-FFN backward)
   bool train_ready = false;
   int64_t train_T = 0;                  // T of the last cl_moe_forward_train
+  const void* cur_x = nullptr;          // hidden of the last cl_moe_forward_train (caller-owned)
   int64_t rp_cap = 0;                   // padded-row capacity of the transposes
   __nv_bfloat16* win_ref = nullptr;     // [NL][d][2f] reference layout (dgrad-2 B operand)
   __nv_bfloat16* wout_ref = nullptr;    // [NL][f][d]  reference layout (dgrad-1 B operand)
@@ -176,6 +177,9 @@ struct cl_moe {
   __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
   __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;  // [C][rp_cap]
   int32_t* poff = nullptr;              // [NL+1]
+  float* rdz = nullptr;                 // router backward: dz [cap][N] fp32
+  float* rpart = nullptr;               // dW_r partials [chunks][d][N]
+  float* dcw_scratch = nullptr;         // d(combine weights) [cap][K] when the caller does not want them
   int32_t* kb_off = nullptr;            // [NL+1]
   CUtensorMap mAdg1[2], mBdg1[2], mAdg2[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
 
@@ -194,7 +198,8 @@ struct cl_moe {
       if (p) cudaFree(p);
     for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
                     (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
-                    (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off})
+                    (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
+                    (void*)dcw_scratch})
       if (p) cudaFree(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
@@ -723,11 +728,12 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
   h->train_T = T;
+  h->cur_x = x;
 }
 
 // Expert-FFN backward of the last training forward.
 void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, float* dw_in, float* dw_out,
-                  cudaStream_t st) {
+                  cudaStream_t st, float* dw_router = nullptr, float g_aux = 0.0f, float g_z = 0.0f) {
   if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
   const int64_t T = h->train_T, rows = T * h->K, d = h->d, f = h->f;
   const int NL = h->n_local;
@@ -771,9 +777,30 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
     launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
   }
   prof_mark(h, 2, st);
-  // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]
-  launch_combine<__nv_bfloat16>(h->dXbuf, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
-                                h->rb.finite_flag, st);
+  // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]  (+ router term)
+  if (dw_router) {
+    const int N = static_cast<int>(h->N);
+    if (!h->rdz) {
+      h->rdz = dalloc<float>(h->cap * h->N);
+      h->rpart = dalloc<float>(((h->cap + kRwTokens - 1) / kRwTokens) * h->d * h->N);
+    }
+    router_bwd_dz_kernel<<<(int)((T + 127) / 128), 128, 0, st>>>(h->rb.probs, h->rb.logits, h->rb.topk_idx, d_cw,
+                                                                h->rb.counts, (int)T, N, (int)h->K, g_aux, g_z, h->rdz);
+    const int chunks = static_cast<int>((T + kRwTokens - 1) / kRwTokens);
+    router_wgrad_partial_kernel<<<dim3((unsigned)(d / 64), (unsigned)chunks, (unsigned)((N + 15) / 16)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(h->cur_x), h->rdz, (int)T, (int)d, N, h->rpart);
+    router_wgrad_reduce_kernel<<<(int)((d * N + 255) / 256), 256, 0, st>>>(h->rpart, chunks, (int)(d * N), dw_router);
+    const int blocks = static_cast<int>((T + 7) / 8);
+    switch (h->K) {
+      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      default: throw ConfigErr("router backward supports top_k in {1, 2, 4}");
+    }
+  } else {
+    launch_combine<__nv_bfloat16>(h->dXbuf, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
+                                  h->rb.finite_flag, st);
+  }
   CK(cudaGetLastError());
   prof_mark(h, 3, st);
   // 5. weight gradients over each expert's rows (variable K): padded K-major transposes, then
@@ -884,6 +911,20 @@ cl_status cl_moe_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d
     if (!d_out || !d_hidden || !d_combine_w || !dw_in || !dw_out) throw ConfigErr("null argument");
     CK(cudaSetDevice(h->cfg.device));
     run_backward(h, d_out, d_hidden, d_combine_w, dw_in, dw_out, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_backward_full(cl_moe* h, const void* d_out, float g_aux, float g_z, void* d_hidden, float* dw_router,
+                               float* dw_in, float* dw_out, float* d_combine_w, void* stream) {
+  return guarded(h, [&] {
+    if (!d_out || !d_hidden || !dw_router || !dw_in || !dw_out) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    float* dcw = d_combine_w;
+    if (!dcw) {
+      if (!h->dcw_scratch) h->dcw_scratch = dalloc<float>(h->cap * h->K);
+      dcw = h->dcw_scratch;
+    }
+    run_backward(h, d_out, d_hidden, dcw, dw_in, dw_out, (cudaStream_t)stream, dw_router, g_aux, g_z);
   });
 }
 

@@ -241,6 +241,19 @@ class MoELayer:
                                            _stream(self.device)), "backward")
         return dh, dcw, dwi, dwo
 
+    def backward_full(self, d_out: torch.Tensor, g_aux: float = 0.0, g_z: float = 0.0):
+        """Layer + router backward of the last forward_train: (d_hidden, dW_r, dW_in, dW_out)."""
+        d_out = self._bf16(d_out)
+        nl = self.cfg.n_experts // self.cfg.ep_size
+        d, f, n = self.cfg.d_model, self.cfg.d_ff, self.cfg.n_experts
+        dh = torch.empty_like(d_out)
+        dwr = torch.empty(d, n, dtype=torch.float32, device=self.device)
+        dwi = torch.empty(nl, d, 2 * f, dtype=torch.float32, device=self.device)
+        dwo = torch.empty(nl, f, d, dtype=torch.float32, device=self.device)
+        self._check(self.L.cl_moe_backward_full(self.h, _ptr(d_out), g_aux, g_z, _ptr(dh), _ptr(dwr), _ptr(dwi),
+                                                _ptr(dwo), None, _stream(self.device)), "backward_full")
+        return dh, dwr, dwi, dwo
+
     def _new_decision(self, t: int) -> "RouterDecision":
         n, k, dev = self.cfg.n_experts, self.cfg.top_k, self.device
         return RouterDecision(

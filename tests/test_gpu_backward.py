@@ -64,3 +64,27 @@ def test_backward_requires_forward_train():
     with pytest.raises(MoEConfigError):
         lay.backward(torch.zeros(16, 256, dtype=torch.bfloat16, device="cuda"))
     lay.close()
+
+
+@pytest.mark.parametrize("t,d,n,k,f,ga,gz", [(300, 256, 8, 2, 256, 0.01, 0.001), (257, 512, 16, 4, 256, 1.0, 1.0),
+                                             (2000, 256, 16, 1, 256, 0.1, 0.0)])
+def test_full_backward_with_router_vs_oracle(t, d, n, k, f, ga, gz):
+    """Layer + router backward (aux / Z loss weighted by g_aux / g_z) vs the oracle, which is
+    itself pinned against the reference Tape in tests/test_oracle.py."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, f)
+    g = make_inputs(t, d, 1, f, seed=77, experts=False)["x"]
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    lay.forward_train(x)
+    dh, dwr, dwi, dwo = lay.backward_full(torch.from_numpy(g).cuda().to(torch.bfloat16).contiguous(), ga, gz)
+    lay.sync()
+    rdh, rdwr, rdwi, rdwo = o.moe_backward_full(inp["x"], inp["w_router"], inp["w_in"], inp["w_out"], g, ga, gz, k,
+                                                jobs=JOBS)
+    assert _rel(dh.float().cpu().numpy(), rdh) <= 2e-2
+    assert _rel(dwr.cpu().numpy(), rdwr) <= 2e-2, _rel(dwr.cpu().numpy(), rdwr)
+    assert _rel(dwi.cpu().numpy(), rdwi) <= 2e-2
+    assert _rel(dwo.cpu().numpy(), rdwo) <= 2e-2
+    lay.close()

@@ -302,3 +302,16 @@ def test_fp8_qdq_matches_torch_e4m3_rne():
     s = np.float32(0.37)
     ref_s = (torch.from_numpy(np.clip(x / s, -448, 448)).to(torch.float8_e4m3fn).float().numpy() * s).astype(np.float32)
     assert np.array_equal(o.fp8_qdq(x, float(s)), ref_s)
+
+
+@pytest.mark.parametrize("t,d,n,k,f", [(40, 32, 4, 2, 16), (33, 64, 8, 3, 32), (25, 32, 16, 4, 16)])
+def test_router_backward_restatement_vs_reference_tape(oracle_port, oracle_ref, t, d, n, k, f):
+    """The analytic fp64 router backward (+ expert backward) against the reference Tape over
+    gather_cols_per_row / row_sums / recip / mul_rowwise / moe_aux_loss / z_loss: rel <= 1e-5
+    (the Tape's float roundings of the renormalisation differ from the fp64 pin by an ulp)."""
+    inp = make_inputs(t, d, n, f)
+    g = make_inputs(t, d, 1, f, seed=9, experts=False)["x"]
+    a = oracle_port.moe_backward_full(inp["x"], inp["w_router"], inp["w_in"], inp["w_out"], g, 0.3, 0.7, k)
+    b = oracle_ref.moe_backward_full(inp["x"], inp["w_router"], inp["w_in"], inp["w_out"], g, 0.3, 0.7, k)
+    for u, v in zip(a, b):
+        assert np.abs(u - v).max() <= 1e-5 * np.abs(v).max()
