@@ -171,6 +171,14 @@ cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls);
  * handle's precision. act_scale_* may be given explicitly (host arrays [N_local]) instead. */
 cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream);
 cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float* act_scale_mid);
+/* Unified smoothing. compute: s_j = max|X_j|^alpha / max|W_j|^(1-alpha) from the
+ * calibration per-channel maxima of the layer input and the joint per-input-channel maxima of
+ * every expert's W_in and W_r (zero-max channels -> 1); s_out is a host array [d]. fold: rows
+ * of every W_in and of W_r are scaled by s (the preceding RMSNorm gain must be divided by s by
+ * the caller, i.e. later inputs are x / s). Folding invalidates the FP8 scheme (re-calibrate and
+ * quantize again) and clears the calibration maxima. */
+cl_status cl_moe_compute_smoothing(cl_moe* h, float alpha, float* s_out);
+cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s);
 cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
 /* Host copies of the FP8 scales in use: [N_local], [N_local], [N_local x 2f], [N_local x d]. */
 cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,

@@ -537,6 +537,35 @@ int orc_router_backward(const float* x, const float* wr, std::int64_t T, std::in
   return 0;
 }
 
+// ---- unified smoothing -------------------------------------------------------
+// compute_smoothing: s_j = max|X_j|^alpha / (max|W_j|)^(1-alpha), W_j = row j of every expert's W_in
+// AND of W_r (joint maximum); zero-max channels get s = 1.
+void orc_compute_smoothing(const float* x, std::int64_t T, std::int64_t d, std::int64_t N, std::int64_t f,
+                           const float* w_in, const float* wr, float alpha, float* s) {
+  for (std::int64_t l = 0; l < d; ++l) {
+    float xm = 0.0f, wm = 0.0f;
+    for (std::int64_t j = 0; j < T; ++j) xm = std::max(xm, std::fabs(x[j * d + l]));
+    for (std::int64_t e = 0; e < N; ++e)
+      for (std::int64_t c = 0; c < 2 * f; ++c) wm = std::max(wm, std::fabs(w_in[(e * d + l) * 2 * f + c]));
+    for (std::int64_t i = 0; i < N; ++i) wm = std::max(wm, std::fabs(wr[l * N + i]));
+    s[l] = (xm > 0.0f && wm > 0.0f)
+               ? static_cast<float>(std::pow(static_cast<double>(xm), alpha) / std::pow(static_cast<double>(wm), 1.0 - alpha))
+               : 1.0f;
+  }
+}
+
+// fold_smoothing: gain <- gain / s (upstream: inputs become x / s), W_in rows and W_r rows <- * s.
+void orc_fold_smoothing(const float* s, std::int64_t d, std::int64_t N, std::int64_t f, float* w_in, float* wr,
+                        float* x, std::int64_t T) {
+  for (std::int64_t e = 0; e < N; ++e)
+    for (std::int64_t l = 0; l < d; ++l)
+      for (std::int64_t c = 0; c < 2 * f; ++c) w_in[(e * d + l) * 2 * f + c] *= s[l];
+  for (std::int64_t l = 0; l < d; ++l)
+    for (std::int64_t i = 0; i < N; ++i) wr[l * N + i] *= s[l];
+  for (std::int64_t j = 0; j < T; ++j)
+    for (std::int64_t l = 0; l < d; ++l) x[j * d + l] /= s[l];
+}
+
 // ---- FP8 E4M3 quantize-dequantize -----------------------------------------
 // q = x/scale in float; RNE onto the enumerated E4M3 grid (ties to the even code), |q| > 448
 // clamps to +-448; result q_hat * scale in float. Non-finite input is an error.

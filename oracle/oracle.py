@@ -74,6 +74,8 @@ class Oracle:
             L.orc_plan.argtypes = [_i64p, _i64, _i64, _i64, _i64p, _i64p, _i64p]
             L.orc_expert_ffn.argtypes = [_f32p, _i64, _i64, _i64, _f32p, _f32p, C.c_void_p, _f32p]
             L.orc_fp8_qdq.argtypes = [_f32p, _i64, C.c_float, _f32p]
+            L.orc_compute_smoothing.argtypes = [_f32p, _i64, _i64, _i64, _i64, _f32p, _f32p, C.c_float, _f32p]
+            L.orc_fold_smoothing.argtypes = [_f32p, _i64, _i64, _i64, _f32p, _f32p, _f32p, _i64]
             L.orc_fp8_encode.argtypes = [_f32p, _i64, _u8p]
             L.orc_router_backward.argtypes = [_f32p, _f32p, _i64, _i64, _i64, _i64, _f32p, _f32p, _i64p, _i64p, _f32p,
                                               C.c_float, C.c_float, _f32p, _f32p]
@@ -223,6 +225,24 @@ class Oracle:
         out = np.empty_like(x)
         self._call("fp8_qdq", x, x.size, scale, out)
         return out
+
+    def compute_smoothing(self, x, w_in, wr, alpha):
+        x = np.ascontiguousarray(x, np.float32)
+        t, d = x.shape
+        n, _, f2 = w_in.shape
+        s = np.empty(d, np.float32)
+        self.lib.orc_compute_smoothing(x, t, d, n, f2 // 2, np.ascontiguousarray(w_in, np.float32),
+                                       np.ascontiguousarray(wr, np.float32), alpha, s)
+        return s
+
+    def fold_smoothing(self, s, w_in, wr, x):
+        """Returns folded copies (w_in', wr', x / s)."""
+        w_in = np.array(w_in, np.float32, copy=True)
+        wr = np.array(wr, np.float32, copy=True)
+        x = np.array(x, np.float32, copy=True)
+        n, d, f2 = w_in.shape
+        self.lib.orc_fold_smoothing(np.ascontiguousarray(s, np.float32), d, n, f2 // 2, w_in, wr, x, x.shape[0])
+        return w_in, wr, x
 
     def fp8_encode(self, q):
         q = np.ascontiguousarray(q, np.float32).ravel()

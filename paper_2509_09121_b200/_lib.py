@@ -103,6 +103,8 @@ _PROTOS = {
                                    C.POINTER(C.c_int64)]),
     "cl_moe_calibrate": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
     "cl_moe_quantize_fp8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cl_moe_compute_smoothing": (C.c_int, [C.c_void_p, C.c_float, C.c_void_p]),
+    "cl_moe_fold_smoothing": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cl_moe_set_precision": (C.c_int, [C.c_void_p, C.c_int32]),
     "cl_moe_get_fp8_scales": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }

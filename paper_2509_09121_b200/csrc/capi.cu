@@ -117,6 +117,8 @@ struct cl_moe {
   float* sx_in = nullptr;              // [n_local]
   float* sx_mid = nullptr;             // [n_local]
   float* calib = nullptr;              // [2][n_local] running maxima
+  float* calib_ch = nullptr;           // [d] per-channel max |hidden| over calibration tokens
+  float* smooth = nullptr;             // [d] scratch for fold_smoothing
   bool fp8_ready = false;
 
   // workspaces
@@ -188,7 +190,7 @@ struct cl_moe {
   bool maps_q = false;
 
   ~cl_moe() {
-    void* ptrs[] = {wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
+    void* ptrs[] = {calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
                     sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
                     inv,    row_w,   slot[0].x, slot[0].xf, slot[0].out, slot[1].x, slot[1].xf, slot[1].out,
                     io_out, rb.logits,    rb.probs,
@@ -353,6 +355,9 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->sx_mid = dalloc<float>(h->n_local);
   h->calib = dalloc<float>(2 * h->n_local);
   CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
+  h->calib_ch = dalloc<float>(h->d);
+  CK(cudaMemset(h->calib_ch, 0, sizeof(float) * h->d));
+  h->smooth = dalloc<float>(h->d);
 
   using namespace cmoe;
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
@@ -670,19 +675,33 @@ void ensure_training(cl_moe* h) {
   if (h->f % 256) throw ConfigErr("training needs d_ff to be a multiple of 256");
   if (h->cfg.ep_size > 1) throw ConfigErr("expert-parallel backward is not supported yet");
   const int64_t rows = h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
-  h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
-  h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
-  h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
-  h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-  h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
-  h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-  h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
-  h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
-  h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
-  h->dYT = dalloc<__nv_bfloat16>(d * h->rp_cap);
-  h->dHT = dalloc<__nv_bfloat16>(2 * f * h->rp_cap);
-  h->poff = dalloc<int32_t>(NL + 1);
-  h->kb_off = dalloc<int32_t>(NL + 1);
+  if (!h->win_ref) {  // buffers and descriptors: once per handle
+    h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
+    h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
+    h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
+    h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
+    h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
+    h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
+    h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
+    h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
+    h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
+    h->dYT = dalloc<__nv_bfloat16>(d * h->rp_cap);
+    h->dHT = dalloc<__nv_bfloat16>(2 * f * h->rp_cap);
+    h->poff = dalloc<int32_t>(NL + 1);
+    h->kb_off = dalloc<int32_t>(NL + 1);
+    for (int v = 0; v < 2; ++v) {
+      const uint32_t brow = v == 0 ? 256 : 128;
+      h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
+      h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
+      h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
+      h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
+      h->mAwo[v] = make_map(h->AT, false, h->rp_cap, f, 128);
+      h->mBwo[v] = make_map(h->dYT, false, h->rp_cap, d, brow);
+      h->mAwi[v] = make_map(h->XT, false, h->rp_cap, d, 128);
+      h->mBwi[v] = make_map(h->dHT, false, h->rp_cap, 2 * f, brow);
+    }
+  }
+  // reference-layout weight copies (re-derived whenever the packed weights change)
   for (int e = 0; e < NL; ++e) {
     transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
         h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, h->win_ref + (size_t)e * d * 2 * f);
@@ -691,17 +710,6 @@ void ensure_training(cl_moe* h) {
   }
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
-  for (int v = 0; v < 2; ++v) {
-    const uint32_t brow = v == 0 ? 256 : 128;
-    h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
-    h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
-    h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
-    h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
-    h->mAwo[v] = make_map(h->AT, false, h->rp_cap, f, 128);
-    h->mBwo[v] = make_map(h->dYT, false, h->rp_cap, d, brow);
-    h->mAwi[v] = make_map(h->XT, false, h->rp_cap, d, 128);
-    h->mBwi[v] = make_map(h->dHT, false, h->rp_cap, 2 * f, brow);
-  }
   h->train_ready = true;
 }
 
@@ -1217,7 +1225,12 @@ cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t res
     if (!hidden) throw ConfigErr("hidden is null");
     CK(cudaSetDevice(h->cfg.device));
     cudaStream_t st = (cudaStream_t)stream;
-    if (reset) CK(cudaMemsetAsync(h->calib, 0, sizeof(float) * 2 * h->n_local, st));
+    if (reset) {
+      CK(cudaMemsetAsync(h->calib, 0, sizeof(float) * 2 * h->n_local, st));
+      CK(cudaMemsetAsync(h->calib_ch, 0, sizeof(float) * h->d, st));
+    }
+    col_absmax_kernel<<<dim3((unsigned)((h->d + 255) / 256), (unsigned)((T + 255) / 256)), 256, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(hidden), T, (int)h->d, 256, h->calib_ch);
     const int saved = h->precision;
     h->precision = CL_MOE_BF16;
     run_router(h, hidden, T, st);
@@ -1230,6 +1243,60 @@ cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t res
     segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)h->f,
                                                                  h->rb.offsets, h->n_local, h->calib + h->n_local);
     CK(cudaGetLastError());
+  });
+}
+
+cl_status cl_moe_compute_smoothing(cl_moe* h, float alpha, float* s_out) {
+  return guarded(h, [&] {
+    if (!s_out) throw ConfigErr("s_out is null");
+    if (!(alpha >= 0.0f && alpha <= 1.0f)) throw ConfigErr("alpha must be in [0, 1]");
+    if (h->cfg.ep_size > 1) throw ConfigErr("compute_smoothing needs every expert's weights (ep_size == 1)");
+    CK(cudaSetDevice(h->cfg.device));
+    const int64_t d = h->d, N = h->N;
+    // joint per-input-channel weight maximum over every expert's W_in and the router
+    float* wmax = h->smooth;
+    CK(cudaMemset(wmax, 0, sizeof(float) * d));
+    const int64_t rows = (int64_t)h->n_local * 2 * h->f;
+    col_absmax_kernel<<<dim3((unsigned)((d + 255) / 256), (unsigned)((rows + 1023) / 1024)), 256>>>(h->win, rows, (int)d,
+                                                                                                 1024, wmax);
+    CK(cudaGetLastError());
+    std::vector<float> xm(d), wm(d), wr(d * N);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(xm.data(), h->calib_ch, sizeof(float) * d, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(wm.data(), wmax, sizeof(float) * d, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(wr.data(), h->wr, sizeof(float) * d * N, cudaMemcpyDeviceToHost));
+    for (int64_t l = 0; l < d; ++l) {
+      float m = wm[l];
+      for (int64_t i = 0; i < N; ++i) m = std::max(m, std::fabs(wr[l * N + i]));
+      // s_j = max|X_j|^alpha / max|W_j|^(1-alpha); zero-max channels get s = 1
+      s_out[l] = (xm[l] > 0.0f && m > 0.0f)
+                     ? static_cast<float>(std::pow(static_cast<double>(xm[l]), alpha) /
+                                          std::pow(static_cast<double>(m), 1.0 - alpha))
+                     : 1.0f;
+    }
+  });
+}
+
+cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s) {
+  return guarded(h, [&] {
+    if (!s) throw ConfigErr("s is null");
+    const int64_t d = h->d, N = h->N;
+    for (int64_t l = 0; l < d; ++l)
+      if (!(s[l] > 0.0f) || !std::isfinite(s[l])) throw ConfigErr("smoothing factors must be finite and > 0");
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaMemcpy(h->smooth, s, sizeof(float) * d, cudaMemcpyHostToDevice));
+    const int64_t n = (int64_t)h->n_local * 2 * h->f * d;
+    scale_cols_bf16_kernel<<<grid_for(n), 256>>>(h->win, n, (int)d, h->smooth);
+    scale_rows_f32_kernel<<<(int)((d * N + 255) / 256), 256>>>(h->wr, (int)d, (int)N, h->smooth);
+    widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    // derived copies are stale now
+    h->fp8_ready = false;
+    h->precision = CL_MOE_BF16;
+    h->train_ready = false;
+    CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
+    CK(cudaMemset(h->calib_ch, 0, sizeof(float) * d));
   });
 }
 

@@ -124,6 +124,30 @@ __global__ void segment_absmax_kernel(const __nv_bfloat16* __restrict__ m, int c
   if (lane == 0) atomicMax(reinterpret_cast<int*>(out) + e, __float_as_int(mx));
 }
 
+// Per-column max |value| of a row-major bf16 matrix [rows][cols] into out[cols] (atomicMax on the
+// bit patterns of non-negative floats). Grid (cols/256, row chunks).
+__global__ void col_absmax_kernel(const __nv_bfloat16* __restrict__ m, int64_t rows, int cols, int rows_per_block,
+                                  float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float mx = 0.0f;
+  for (int64_t r = r0; r < r1; ++r) mx = fmaxf(mx, fabsf(__bfloat162float(m[r * cols + c])));
+  atomicMax(reinterpret_cast<int*>(out) + c, __float_as_int(mx));
+}
+
+// fold_smoothing on the packed W_in [rows][d] (K = input channel): w[.][l] *= s[l]
+// (re-rounded to bf16), and W_r [d][N] fp32 rows: wr[l][.] *= s[l].
+__global__ void scale_cols_bf16_kernel(__nv_bfloat16* __restrict__ m, int64_t n, int cols, const float* __restrict__ s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m[i] = __float2bfloat16_rn(__bfloat162float(m[i]) * s[i % cols]);
+}
+__global__ void scale_rows_f32_kernel(float* __restrict__ m, int rows, int cols, const float* __restrict__ s) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < rows * cols) m[i] = m[i] * s[i / cols];
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, int64_t n, __nv_bfloat16* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = __float2bfloat16_rn(in[i]);

@@ -200,6 +200,15 @@ class MoELayer:
             rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
         self._check(rc, "quantize_fp8")
 
+    def compute_smoothing(self, alpha: float = 0.5) -> np.ndarray:
+        s = np.empty(self.cfg.d_model, np.float32)
+        self._check(self.L.cl_moe_compute_smoothing(self.h, alpha, s.ctypes.data), "compute_smoothing")
+        return s
+
+    def fold_smoothing(self, s) -> None:
+        s = np.ascontiguousarray(s, np.float32)
+        self._check(self.L.cl_moe_fold_smoothing(self.h, s.ctypes.data), "fold_smoothing")
+
     def set_precision(self, precision: str):
         code = _lib.CL_MOE_FP8_E4M3 if precision == "fp8" else _lib.CL_MOE_BF16
         self._check(self.L.cl_moe_set_precision(self.h, code), "set_precision")

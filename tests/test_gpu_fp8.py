@@ -88,3 +88,46 @@ def test_fp8_requires_calibration():
     lay.sync()
     assert torch.isfinite(out.float()).all()
     lay.close()
+
+
+def test_smoothing_compute_fold_then_expert_aware_fp8():
+    """SPEC expert-quantizer flow on device: calibrate -> compute_smoothing (joint W max over experts
+    and router) -> fold_smoothing -> re-calibrate on x/s -> quantize -> FP8 forward; each step checked
+    against the oracle."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 512, 512, 8, 2, 256
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, f)
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t), inp["w_router"], inp["w_in"],
+                   inp["w_out"])
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    lay.calibrate(x)
+    s = lay.compute_smoothing(0.5)
+    s_ref = o.compute_smoothing(inp["x"], inp["w_in"], inp["w_router"], 0.5)
+    np.testing.assert_allclose(s, s_ref, rtol=1e-6)
+    lay.fold_smoothing(s)
+    # the folded model the device now holds: bf16(W_in * s), W_r * s (fp32); inputs x' = bf16(x / s)
+    wi_f, wr_f, xs = o.fold_smoothing(s, inp["w_in"], inp["w_router"], inp["x"])
+    wi_f = o.round_bf16(wi_f)
+    xs = o.round_bf16(xs)
+    xd = torch.from_numpy(xs).cuda().to(torch.bfloat16).contiguous()
+    out, dec = lay.forward(xd, want_decision=True)
+    lay.sync()
+    r = o.route(xs, wr_f, k)
+    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), r["topk_idx"])
+    ref = o.moe_forward(xs, wi_f, inp["w_out"], r["topk_idx"], r["combine_weights"], jobs=JOBS)
+    o32 = out.float().cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(o32 - ref) / np.linalg.norm(ref) <= 1e-2
+    # unfolded model on the original inputs gives the same function (SPEC.md:560-561, bf16-level)
+    full0 = o.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], jobs=JOBS)
+    assert np.linalg.norm(o32 - full0) / np.linalg.norm(full0) <= 2e-2
+    # expert-aware FP8 on the folded model
+    lay.calibrate(xd)
+    lay.quantize_fp8()
+    s_in, s_mid, _, _ = lay.fp8_scales()
+    outq = lay.forward(xd)
+    lay.sync()
+    refq, _, _ = moe_forward_fp8_sim(o, xs, wi_f, inp["w_out"], r["topk_idx"], r["combine_weights"], s_in, s_mid)
+    q32 = outq.float().cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(q32 - refq) / np.linalg.norm(refq) <= 2e-2
+    lay.close()

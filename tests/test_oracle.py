@@ -315,3 +315,43 @@ def test_router_backward_restatement_vs_reference_tape(oracle_port, oracle_ref, 
     b = oracle_ref.moe_backward_full(inp["x"], inp["w_router"], inp["w_in"], inp["w_out"], g, 0.3, 0.7, k)
     for u, v in zip(a, b):
         assert np.abs(u - v).max() <= 1e-5 * np.abs(v).max()
+
+
+# ------------------------------------------------------------------ smoothing
+def test_spec_smoothing_examples(oracle_port):
+    rng = np.random.default_rng(5)
+    d, n, f = 8, 2, 4
+    w_in = rng.standard_normal((n, d, 2 * f)).astype(np.float32)
+    wr = rng.standard_normal((d, n)).astype(np.float32)
+    wmax = np.maximum(np.abs(w_in).max(axis=(0, 2)), np.abs(wr).max(1))
+    # max|X_j| = max|W_j|, alpha = 0.5 -> s = 1
+    x = np.zeros((3, d), np.float32)
+    x[0] = wmax
+    assert np.allclose(oracle_port.compute_smoothing(x, w_in, wr, 0.5), 1.0, rtol=1e-6)
+    # alpha = 1 -> s_j = max|X_j|
+    x = rng.standard_normal((5, d)).astype(np.float32)
+    assert np.allclose(oracle_port.compute_smoothing(x, w_in, wr, 1.0), np.abs(x).max(0), rtol=1e-6)
+    # joint max over experts and router governs
+    s = oracle_port.compute_smoothing(x, w_in, wr, 0.5)
+    ref = np.sqrt(np.abs(x).max(0).astype(np.float64)) / np.sqrt(wmax.astype(np.float64))
+    assert np.allclose(s, ref, rtol=1e-6)
+    # zero channel -> 1
+    x[:, 3] = 0
+    assert oracle_port.compute_smoothing(x, w_in, wr, 0.5)[3] == 1.0
+
+
+def test_spec_fold_smoothing_preserves_outputs(oracle_port):
+    """SPEC.md:560-561 and acceptance 11: folding is output-preserving at full precision (<= 1e-5 rel)."""
+    t, d, n, k, f = 50, 32, 4, 2, 16
+    inp = make_inputs(t, d, n, f, bf16=False)
+    s_one = np.ones(d, np.float32)
+    wi1, wr1, x1 = oracle_port.fold_smoothing(s_one, inp["w_in"], inp["w_router"], inp["x"])
+    assert np.array_equal(wi1, inp["w_in"]) and np.array_equal(wr1, inp["w_router"]) and np.array_equal(x1, inp["x"])
+    s = np.exp(np.random.default_rng(1).uniform(-1, 1, d)).astype(np.float32)
+    wi, wr, x2 = oracle_port.fold_smoothing(s, inp["w_in"], inp["w_router"], inp["x"])
+    r0 = oracle_port.route(inp["x"], inp["w_router"], k)
+    r1 = oracle_port.route(x2, wr, k)
+    assert np.abs(r0["logits"] - r1["logits"]).max() <= 1e-5 * np.abs(r0["logits"]).max()
+    y0 = oracle_port.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r0["topk_idx"], r0["combine_weights"])
+    y1 = oracle_port.moe_forward(x2, wi, inp["w_out"], r0["topk_idx"], r0["combine_weights"])
+    assert np.abs(y0 - y1).max() <= 1e-5 * np.abs(y0).max()
