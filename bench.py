@@ -54,6 +54,15 @@ def load_peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
+def fp8_peak():
+    p = os.path.join(ROOT, "profiles", "fp8_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh)["fp8_tflops"], "measured (tools/fp8_peak.py, cuBLASLt e4m3 8192^3)"
+    return 4500.0, "nominal dense"
+
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -343,6 +352,10 @@ def run_ours(args, cfg):
                            frac_of_burst=g1_tf / peaks["bf16"], peak_kind=f"sustained ({peaks['src']})",
                            traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
                       if (args.precision == "bf16" and T * K >= 256 * nl * 4) else
+                      dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05 kind::f8f6f4, e4m3)", achieved=g1_tf,
+                           peak=fp8_peak()[0], unit="TFLOP/s", frac=g1_tf / fp8_peak()[0], peak_kind=fp8_peak()[1],
+                           traffic=None, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
+                      if T * K >= 256 * nl * 4 else
                       dict(bound="hbm", kernel="grouped GEMM1+GEMM2 weight streaming (tcgen05)",
                            achieved=stream_gbs, peak=peaks["hbm"], unit="GB/s", frac=stream_gbs / peaks["hbm"],
                            traffic=None, bytes_per_launch=w_bytes, ms_per_launch=g_ms)),
