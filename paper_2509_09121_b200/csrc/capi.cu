@@ -164,6 +164,9 @@ struct cl_moe {
   int32_t* ep_off_dev = nullptr;        // [NL+1] local expert offsets in the receive buffer
   int32_t* ep_counts_host = nullptr;    // pinned mirrors
   int32_t* ep_off_host = nullptr;
+  std::vector<int64_t> ep_C, ep_piece, ep_myoff;  // exchange layout of the last EP forward
+  __nv_bfloat16* dYsrc = nullptr;       // EP training: source-order dY [cap*K][d]
+  __nv_bfloat16* dXsrc = nullptr;       // EP training: source-order dX [cap*K][d]
   CUtensorMap mA1e[2], mA2e[2];
 
   // training (expert-FFN backward)
@@ -201,7 +204,7 @@ struct cl_moe {
     for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
                     (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
                     (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
-                    (void*)dcw_scratch})
+                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc})
       if (p) cudaFree(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
@@ -506,10 +509,10 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
 }
 
 // dispatch + expert FFN + combine (local experts; ep_size == 1).
-void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st);
+void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train = false);
 
 void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
-  if (h->cfg.ep_size > 1) {
+  if (h->comm) {  // expert parallel (one rank: loopback through the same exchange code)
     run_ep(h, x, T, out, out_f32, st);
     return;
   }
@@ -590,10 +593,54 @@ void ep_alloc(cl_moe* h) {
     if (r_ != 0) throw RunErr(fmt("%s failed: %s", #x, NcclApi::get().GetErrorString(r_))); \
   } while (0)
 
+// One direction of the expert-parallel row exchange (layout of the last EP forward).
+// to_experts: rows of this rank's source permutation `src` (piece g at my_off[g]) go to the
+// owner of expert g, landing at its (local expert, source) slot of `dst`; otherwise the reverse.
+void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStream_t st) {
+  NcclApi& nc = NcclApi::get();
+  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  const int rank = h->cfg.ep_rank;
+  const int N = static_cast<int>(h->N), NL = h->n_local;
+  const size_t row_b = static_cast<size_t>(h->d) * 2;
+  const auto& C = h->ep_C;
+  const auto& piece = h->ep_piece;
+  const auto& my_off = h->ep_myoff;
+  const uint8_t* s8 = static_cast<const uint8_t*>(src);
+  uint8_t* d8 = static_cast<uint8_t*>(dst);
+  NCK(nc.GroupStart());
+  if (to_experts) {
+    for (int r = 0; r < R; ++r)
+      for (int e = 0; e < NL; ++e) {
+        const int g = r * NL + e;
+        const int64_t n = C[(size_t)rank * N + g];
+        if (n) NCK(nc.Send(s8 + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
+      }
+    for (int e = 0; e < NL; ++e)
+      for (int sr = 0; sr < R; ++sr) {
+        const int64_t n = C[(size_t)sr * N + rank * NL + e];
+        if (n) NCK(nc.Recv(d8 + piece[(size_t)e * R + sr] * row_b, n * row_b, NcclApi::kUint8, sr, h->comm, st));
+      }
+  } else {
+    for (int e = 0; e < NL; ++e)
+      for (int sr = 0; sr < R; ++sr) {
+        const int64_t n = C[(size_t)sr * N + rank * NL + e];
+        if (n) NCK(nc.Send(s8 + piece[(size_t)e * R + sr] * row_b, n * row_b, NcclApi::kUint8, sr, h->comm, st));
+      }
+    for (int r = 0; r < R; ++r)
+      for (int e = 0; e < NL; ++e) {
+        const int g = r * NL + e;
+        const int64_t n = C[(size_t)rank * N + g];
+        if (n) NCK(nc.Recv(d8 + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
+      }
+  }
+  NCK(nc.GroupEnd());
+}
+
 // Expert-parallel forward (ep.cuh): route + plan + dispatch over all N experts, counts
 // all-gather, (expert, source)-piece exchange, local grouped GEMMs, reverse exchange, weighted
-// combine. Requires cl_moe_ep_init. bf16 only in this round.
-void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+// combine. Requires cl_moe_ep_init. bf16 only in this round. `train` keeps H / A^T on the expert
+// side for cl_moe_backward.
+void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
   if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
   if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
   NcclApi& nc = NcclApi::get();
@@ -611,53 +658,28 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)N, NcclApi::kInt32, h->comm, st));
   CK(cudaMemcpyAsync(h->ep_counts_host, h->ep_counts_dev, sizeof(int32_t) * R * N, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  std::vector<int64_t> C((size_t)R * N), loc(NL + 1), piece((size_t)NL * R), my_off(N + 1);
-  for (size_t i = 0; i < C.size(); ++i) C[i] = h->ep_counts_host[i];
-  const int64_t total = ep_layout(C.data(), R, N, rank, loc.data(), piece.data());
+  h->ep_C.assign((size_t)R * N, 0);
+  h->ep_piece.assign((size_t)NL * R, 0);
+  h->ep_myoff.assign((size_t)N + 1, 0);
+  std::vector<int64_t> loc(NL + 1);
+  for (size_t i = 0; i < h->ep_C.size(); ++i) h->ep_C[i] = h->ep_counts_host[i];
+  const int64_t total = ep_layout(h->ep_C.data(), R, N, rank, loc.data(), h->ep_piece.data());
   if (total > h->recv_cap) throw RunErr("expert-parallel receive buffer overflow");
-  my_off[0] = 0;
-  for (int g = 0; g < N; ++g) my_off[g + 1] = my_off[g] + C[(size_t)rank * N + g];
+  for (int g = 0; g < N; ++g) h->ep_myoff[g + 1] = h->ep_myoff[g] + h->ep_C[(size_t)rank * N + g];
   for (int e = 0; e <= NL; ++e) h->ep_off_host[e] = static_cast<int32_t>(loc[e]);
   CK(cudaMemcpyAsync(h->ep_off_dev, h->ep_off_host, sizeof(int32_t) * (NL + 1), cudaMemcpyHostToDevice, st));
-  const size_t row_b = static_cast<size_t>(h->d) * 2;
-  const uint8_t* xp = static_cast<const uint8_t*>(h->xperm);
   // ---- dispatch exchange: piece (dest r, expert g) -> r's (local expert, source) slot ----
-  NCK(nc.GroupStart());
-  for (int r = 0; r < R; ++r)
-    for (int e = 0; e < NL; ++e) {
-      const int g = r * NL + e;
-      const int64_t n = C[(size_t)rank * N + g];
-      if (n) NCK(nc.Send(xp + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
-    }
-  for (int e = 0; e < NL; ++e)
-    for (int s = 0; s < R; ++s) {
-      const int64_t n = C[(size_t)s * N + rank * NL + e];
-      if (n)
-        NCK(nc.Recv(reinterpret_cast<uint8_t*>(h->x_recv) + piece[(size_t)e * R + s] * row_b, n * row_b,
-                    NcclApi::kUint8, s, h->comm, st));
-    }
-  NCK(nc.GroupEnd());
+  ep_exchange(h, h->xperm, h->x_recv, true, st);
   // ---- local experts ----
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st);
+  if (train) {
+    pad_plan_kernel<<<1, 32, 0, st>>>(h->ep_off_dev, NL, h->poff, h->kb_off);
+    CK(cudaGetLastError());
+  }
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st,
+            train ? h->Hbuf : nullptr);
   prof_mark(h, 4, st);
   // ---- reverse exchange into this rank's permutation slots ----
-  NCK(nc.GroupStart());
-  for (int e = 0; e < NL; ++e)
-    for (int s = 0; s < R; ++s) {
-      const int64_t n = C[(size_t)s * N + rank * NL + e];
-      if (n)
-        NCK(nc.Send(reinterpret_cast<const uint8_t*>(h->y_recv) + piece[(size_t)e * R + s] * row_b, n * row_b,
-                    NcclApi::kUint8, s, h->comm, st));
-    }
-  for (int r = 0; r < R; ++r)
-    for (int e = 0; e < NL; ++e) {
-      const int g = r * NL + e;
-      const int64_t n = C[(size_t)rank * N + g];
-      if (n)
-        NCK(nc.Recv(reinterpret_cast<uint8_t*>(h->y) + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm,
-                    st));
-    }
-  NCK(nc.GroupEnd());
+  ep_exchange(h, h->y_recv, h->y, false, st);
   if (out_f32)
     launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
                           h->rb.combine_w);
@@ -668,14 +690,24 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
+  if (train) {
+    h->train_T = T;
+    h->cur_x = x;
+  }
 }
 
 void ensure_training(cl_moe* h) {
   if (h->train_ready) return;
   if (h->f % 256) throw ConfigErr("training needs d_ff to be a multiple of 256");
-  if (h->cfg.ep_size > 1) throw ConfigErr("expert-parallel backward is not supported yet");
-  const int64_t rows = h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
+  if (h->cfg.ep_size > 1 && !h->comm) throw ConfigErr("expert-parallel training needs cl_moe_ep_init first");
+  const bool ep = h->comm != nullptr;
+  // expert-side rows: the receive buffer under expert parallelism
+  const int64_t rows = ep ? h->recv_cap : h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
   if (!h->win_ref) {  // buffers and descriptors: once per handle
+    if (ep) {
+      h->dYsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
+      h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
+    }
     h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
     h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
     h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
@@ -718,6 +750,10 @@ void ensure_training(cl_moe* h) {
 void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStream_t st) {
   if (h->precision != CL_MOE_BF16) throw ConfigErr("training runs in bf16");
   ensure_training(h);
+  if (h->comm) {
+    run_ep(h, x, T, out, false, st, true);
+    return;
+  }
   const int N = static_cast<int>(h->N);
   const int tpc = h->tpc_cur;
   const int blocks = static_cast<int>((T + 7) / 8);
@@ -745,17 +781,24 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
   const int64_t T = h->train_T, rows = T * h->K, d = h->d, f = h->f;
   const int NL = h->n_local;
+  const bool ep = h->comm != nullptr;
+  // expert-side views: the receive buffers under expert parallelism
+  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
+  const void* es_x = ep ? static_cast<const void*>(h->x_recv) : h->xperm;
+  __nv_bfloat16* dY_src = ep ? h->dYsrc : h->dYbuf;
+  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
   prof_begin(h, st, 1);
   // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
   combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_out), h->y, h->perm,
-                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K, h->dYbuf,
+                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K, dY_src,
                                                            d_cw);
   CK(cudaGetLastError());
+  if (ep) ep_exchange(h, dY_src, h->dYbuf, true, st);  // dY rows to the experts' owners
   prof_mark(h, 0, st);
-  const int v = (h->gemm_auto ? (h->last_tokens * h->K / NL >= 1024) : h->gemm_ctas == 2) ? 1 : 0;
+  const int v = h->gemm_ctas == 2 ? 1 : 0;  // same variant the training forward chose
   // 2. dA = dY W_out^T fused with the SwiGLU backward -> dH
   GemmArgs a1{};
-  a1.offsets = h->rb.offsets;
+  a1.offsets = es_off;
   a1.n_experts = NL;
   a1.n_tiles_n = static_cast<int>(f / kBN);
   a1.num_kb = static_cast<int>(d * 2 / kBKBytes);
@@ -768,7 +811,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   a1.poff = h->poff;
   // 3. dX = dH W_in^T
   GemmArgs a2{};
-  a2.offsets = h->rb.offsets;
+  a2.offsets = es_off;
   a2.n_experts = NL;
   a2.n_tiles_n = static_cast<int>(d / kBN);
   a2.num_kb = static_cast<int>(2 * f * 2 / kBKBytes);
@@ -784,6 +827,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
     prof_mark(h, 1, st);
     launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
   }
+  if (ep) ep_exchange(h, h->dXbuf, dX_src, false, st);  // dX rows back to their tokens' ranks
   prof_mark(h, 2, st);
   // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]  (+ router term)
   if (dw_router) {
@@ -798,15 +842,18 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
     router_wgrad_partial_kernel<<<dim3((unsigned)(d / 64), (unsigned)chunks, (unsigned)((N + 15) / 16)), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(h->cur_x), h->rdz, (int)T, (int)d, N, h->rpart);
     router_wgrad_reduce_kernel<<<(int)((d * N + 255) / 256), 256, 0, st>>>(h->rpart, chunks, (int)(d * N), dw_router);
+    // the router is replicated: its gradient is the sum over the data-parallel ranks
+    if (ep) NCK(NcclApi::get().AllReduce(dw_router, dw_router, (size_t)(d * N), NcclApi::kFloat32, NcclApi::kSum,
+                                         h->comm, st));
     const int blocks = static_cast<int>((T + 7) / 8);
     switch (h->K) {
-      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
-      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
-      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(h->dXbuf, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
       default: throw ConfigErr("router backward supports top_k in {1, 2, 4}");
     }
   } else {
-    launch_combine<__nv_bfloat16>(h->dXbuf, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
+    launch_combine<__nv_bfloat16>(dX_src, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
                                   h->rb.finite_flag, st);
   }
   CK(cudaGetLastError());
@@ -816,15 +863,14 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   //    (A^T and dH^T were written by the GEMM1 / dgrad-1 epilogues; only their padding columns
   //    need zeroing. X^T and dY^T go through the transpose kernel.)
   const unsigned pb = static_cast<unsigned>(h->rp_cap / 64);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)d,
-                                                                     h->rb.offsets, h->poff, NL, h->XT, h->rp_cap);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, h->rb.offsets, h->poff, NL,
-                                                                     h->dYT, h->rp_cap);
-  zero_pad_cols_kernel<<<dim3((unsigned)((f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap,
-                                                                                        h->rb.offsets, h->poff);
+  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d,
+                                                                     es_off, h->poff, NL, h->XT, h->rp_cap);
+  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT,
+                                                                     h->rp_cap);
+  zero_pad_cols_kernel<<<dim3((unsigned)((f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
+                                                                                        h->poff);
   zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
-                                                                                            h->rp_cap, h->rb.offsets,
-                                                                                            h->poff);
+                                                                                            h->rp_cap, es_off, h->poff);
   CK(cudaGetLastError());
   prof_mark(h, 4, st);
   const int gw = (f % 256 == 0) ? 2 : 1;

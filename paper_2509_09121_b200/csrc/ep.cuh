@@ -27,11 +27,13 @@ struct NcclApi {
   struct UniqueId {
     char internal[128];
   };
-  enum DataType { kUint8 = 1, kInt32 = 2 };
+  enum DataType { kUint8 = 1, kInt32 = 2, kFloat32 = 7 };
+  enum RedOp { kSum = 0 };
   int (*GetUniqueId)(UniqueId*) = nullptr;
   int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
   int (*CommDestroy)(Comm) = nullptr;
   int (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*Send)(const void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
   int (*GroupStart)() = nullptr;
@@ -54,6 +56,7 @@ struct NcclApi {
       api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
       api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
       api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+      api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
       api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
       api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
       api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));

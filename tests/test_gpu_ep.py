@@ -11,6 +11,8 @@ torch = pytest.importorskip("torch")
 
 from oracle.oracle import Oracle, make_inputs  # noqa: E402
 
+JOBS = os.cpu_count() or 1
+
 
 @pytest.mark.parametrize("gemm_ctas", [1, 2])
 def test_ep_loopback_matches_oracle(gemm_ctas):
@@ -31,4 +33,35 @@ def test_ep_loopback_matches_oracle(gemm_ctas):
     for res in (out_ep, out):
         dlt = res.float().cpu().numpy().astype(np.float64) - ref
         assert np.linalg.norm(dlt) / np.linalg.norm(ref) <= 1e-2
+    lay.close()
+
+
+def test_ep_loopback_training_matches_oracle():
+    """Expert-parallel training step (forward_train + backward_full) through the exchange code with
+    a 1-rank communicator: dY pieces out, dX pieces back, dW_r all-reduce."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 600, 256, 8, 2, 256
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, f)
+    g = make_inputs(t, d, 1, f, seed=77, experts=False)["x"]
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    lay.ep_init(MoELayer.ep_unique_id())
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    out = lay.forward_train(x)
+    dh, dwr, dwi, dwo = lay.backward_full(torch.from_numpy(g).cuda().to(torch.bfloat16).contiguous(), 0.01, 0.001)
+    lay.sync()
+    r = o.route(inp["x"], inp["w_router"], k)
+    ref = o.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], jobs=JOBS)
+
+    def rel(a, b):
+        return np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b)
+
+    assert rel(out.float().cpu().numpy(), ref) <= 1e-2
+    rdh, rdwr, rdwi, rdwo = o.moe_backward_full(inp["x"], inp["w_router"], inp["w_in"], inp["w_out"], g, 0.01, 0.001, k,
+                                                jobs=JOBS)
+    assert rel(dh.float().cpu().numpy(), rdh) <= 2e-2
+    assert rel(dwr.cpu().numpy(), rdwr) <= 2e-2
+    assert rel(dwi.cpu().numpy(), rdwi) <= 2e-2
+    assert rel(dwo.cpu().numpy(), rdwo) <= 2e-2
     lay.close()
