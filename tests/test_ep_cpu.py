@@ -144,3 +144,123 @@ def test_ep_gloo_matches_single_process_oracle(tmp_path, world, n, k):
     ref = o.moe_forward(full["x"], full["w_in"], full["w_out"], r["topk_idx"], r["combine_weights"])
     got = np.concatenate([np.load(tmp_path / f"out{i}.npy") for i in range(world)])
     assert np.array_equal(got, ref)
+
+
+def _exchange(rank, world, nl, cmat, offsets, piece, src, dst_rows, d, to_experts, tag0):
+    """gloo p2p restatement of cl_moe's ep_exchange (csrc/capi.cu)."""
+    dst = np.zeros((dst_rows, d), np.float32)
+    reqs, bufs = [], []
+    if to_experts:
+        for r in range(world):
+            for e in range(nl):
+                g = r * nl + e
+                cnt = cmat[rank, g]
+                if not cnt:
+                    continue
+                chunk = np.ascontiguousarray(src[offsets[g]:offsets[g] + cnt])
+                if r == rank:
+                    dst[piece[e, rank]:piece[e, rank] + cnt] = chunk
+                else:
+                    reqs.append(dist.isend(torch.from_numpy(chunk), r, tag=tag0 + g))
+        for e in range(nl):
+            for s in range(world):
+                cnt = cmat[s, rank * nl + e]
+                if cnt and s != rank:
+                    b = torch.zeros(cnt, d)
+                    reqs.append(dist.irecv(b, s, tag=tag0 + rank * nl + e))
+                    bufs.append((piece[e, s], b))
+    else:
+        for e in range(nl):
+            for s in range(world):
+                cnt = cmat[s, rank * nl + e]
+                if not cnt:
+                    continue
+                chunk = np.ascontiguousarray(src[piece[e, s]:piece[e, s] + cnt])
+                g = rank * nl + e
+                if s == rank:
+                    dst[offsets[g]:offsets[g] + cnt] = chunk
+                else:
+                    reqs.append(dist.isend(torch.from_numpy(chunk), s, tag=tag0 + g))
+        for r in range(world):
+            for e in range(nl):
+                g = r * nl + e
+                cnt = cmat[rank, g]
+                if cnt and r != rank:
+                    b = torch.zeros(cnt, d)
+                    reqs.append(dist.irecv(b, r, tag=tag0 + g))
+                    bufs.append((offsets[g], b))
+    for q in reqs:
+        q.wait()
+    for start, b in bufs:
+        dst[start:start + len(b)] = b.numpy()
+    return dst
+
+
+def _ep_bwd_worker(rank, world, port, t, d, n, k, f, result_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle, make_inputs
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    gfull = make_inputs(t * world, d, 1, f, seed=31, experts=False)["x"]
+    nl = n // world
+    xs = full["x"][rank * t:(rank + 1) * t]
+    gs = gfull[rank * t:(rank + 1) * t]
+    r = o.route(xs, full["w_router"], k)
+    idx, w = r["topk_idx"], r["combine_weights"]
+    offsets, perm, inv = o.plan(idx, n)
+    allc = [torch.zeros(n, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, torch.from_numpy(np.diff(offsets).astype(np.int64)))
+    cmat = torch.stack(allc).numpy()
+    loc, piece, tot = ep_layout(cmat, rank)
+    # forward: y (unweighted) back at the source
+    x_recv = _exchange(rank, world, nl, cmat, offsets, piece, xs[perm // k], tot, d, True, 0)
+    y_recv = np.zeros_like(x_recv)
+    for e in range(nl):
+        a, b = loc[e], loc[e + 1]
+        if b > a:
+            _, y_recv[a:b] = o.expert_ffn(x_recv[a:b], full["w_in"][rank * nl + e], full["w_out"][rank * nl + e])
+    y = _exchange(rank, world, nl, cmat, offsets, piece, y_recv, t * k, d, False, 10000)
+    # backward at the source: dY = w * dOut[token], d_cw = <dOut, Y> (fp64 sum like mul_rowwise bwd)
+    wslot = w.ravel()[perm]
+    dy_src = (gs[perm // k] * wslot[:, None]).astype(np.float32)
+    dcw = np.zeros(t * k, np.float32)
+    dcw[perm] = (gs[perm // k].astype(np.float64) * y.astype(np.float64)).sum(1).astype(np.float32)
+    dy_recv = _exchange(rank, world, nl, cmat, offsets, piece, dy_src, tot, d, True, 20000)
+    dx_recv = np.zeros_like(x_recv)
+    dwi = np.zeros((nl, d, 2 * f), np.float32)
+    dwo = np.zeros((nl, f, d), np.float32)
+    for e in range(nl):
+        a, b = loc[e], loc[e + 1]
+        if b > a:
+            dx_recv[a:b], dwi[e], dwo[e] = o.expert_ffn_backward(x_recv[a:b], full["w_in"][rank * nl + e],
+                                                                 full["w_out"][rank * nl + e], dy_recv[a:b])
+    dx = _exchange(rank, world, nl, cmat, offsets, piece, dx_recv, t * k, d, False, 30000)
+    dh = np.zeros((t, d), np.float32)
+    for j in range(t):
+        for kk in range(k):
+            dh[j] = dh[j] + dx[inv[j * k + kk]]
+    np.savez(os.path.join(result_dir, f"bwd{rank}.npz"), dh=dh, dcw=dcw.reshape(t, k), dwi=dwi, dwo=dwo)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,k", [(2, 8, 2), (4, 8, 2)])
+def test_ep_gloo_backward_matches_single_process_oracle(tmp_path, world, n, k):
+    t, d, f = 40, 64, 32
+    mp.spawn(_ep_bwd_worker, args=(world, _free_port(), t, d, n, k, f, str(tmp_path)), nprocs=world, join=True)
+    from oracle.oracle import Oracle, make_inputs
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    g = make_inputs(t * world, d, 1, f, seed=31, experts=False)["x"]
+    r = o.route(full["x"], full["w_router"], k)
+    rdh, rdcw, rdwi, rdwo = o.moe_backward(full["x"], full["w_in"], full["w_out"], r["topk_idx"], r["combine_weights"], g)
+    parts = [np.load(tmp_path / f"bwd{i}.npz") for i in range(world)]
+    assert np.array_equal(np.concatenate([p_["dh"] for p_ in parts]), rdh)
+    assert np.array_equal(np.concatenate([p_["dcw"] for p_ in parts]), rdcw)
+    nl = n // world
+    for i, p_ in enumerate(parts):
+        for e in range(nl):
+            cnt = int((r["topk_idx"] == i * nl + e).sum())
+            if cnt:
+                assert np.array_equal(p_["dwi"][e], rdwi[i * nl + e]), (i, e)
+                assert np.array_equal(p_["dwo"][e], rdwo[i * nl + e]), (i, e)
