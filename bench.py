@@ -33,6 +33,10 @@ CONFIGS = {
     "c2": dict(workload="single-B200 MoE layer bf16 (BASELINE configs[1])", T=16384, d=4096, N=16, K=2, f=14336),
     # BASELINE.json configs[0] shape on the GPU
     "c1": dict(workload="small MoE layer (BASELINE configs[0] shape) bf16 on GPU", T=4096, d=1024, N=8, K=2, f=2816),
+    # BASELINE.json configs[2]: Compass-v3-shaped layer (N=16, K=4; d, f derived in SURVEY §8d),
+    # 8192 tokens per rank (65536 over 8 EP ranks)
+    "c3": dict(workload="Compass-v3-shaped MoE layer, EP over the ranks (BASELINE configs[2])", T=8192, d=8192, N=16,
+               K=4, f=12288),
     # BASELINE.json configs[3] decode-size batch at the C2 layer shape (bf16 path)
     "c4": dict(workload="decode-size batch at the C2 layer shape (BASELINE configs[3])", T=256, d=4096, N=16, K=2,
                f=14336),

@@ -182,6 +182,7 @@ struct cl_moe {
   __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
   __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;  // [C][rp_cap]
   int32_t* poff = nullptr;              // [NL+1]
+  int* tile_counter = nullptr;          // grouped-GEMM dynamic tile scheduler
   float* rdz = nullptr;                 // router backward: dz [cap][N] fp32
   float* rpart = nullptr;               // dW_r partials [chunks][d][N]
   float* dcw_scratch = nullptr;         // d(combine weights) [cap][K] when the caller does not want them
@@ -204,7 +205,7 @@ struct cl_moe {
     for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
                     (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
                     (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
-                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc})
+                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter})
       if (p) cudaFree(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
@@ -378,7 +379,11 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
 }
 
 template <int G, int EPI, bool F8, bool OF8, bool WG = false>
-void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args, cudaStream_t st) {
+void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st) {
+  if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
+  GemmArgs args = args_in;
+  args.tile_counter = h->tile_counter;
+  CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((h->num_sms / G) * G);
   cfg.blockDim = dim3(kGemmThreads);

@@ -50,6 +50,7 @@ struct GemmArgs {
   const int32_t* kb_off;    // kWgrad: [n_experts+1] first k-block of each expert's (padded) rows
   int32_t m_tiles;          // kWgrad: m-tiles per expert
   int64_t out_estride;      // kWgrad: elements between consecutive experts' outputs
+  int* tile_counter;        // dynamic tile scheduler: global counter, zeroed before the launch
   void* aux_t;              // training: transposed copy of the output, bf16 [C][rp] (nullable)
   int64_t rp;               // row stride of aux_t (padded-row capacity)
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
@@ -60,6 +61,7 @@ constexpr int kEpiWarps = 8;      // two warps per TMEM lane quarter, each ownin
 constexpr int kBN = 256;                 // MMA N (output columns of one tile, pre-SwiGLU)
 constexpr int kBKBytes = 128;            // one swizzle atom along K
 constexpr int kMaxExperts = 256;
+constexpr int kTileSlots = 4;            // depth of the tile-index broadcast ring
 
 template <int kCtaGroup>
 struct GemmCfg {
@@ -166,7 +168,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfill = tempty + 2;          // tile-index ring: filled by the leader's producer
+  uint64_t* tfree = tfill + kTileSlots;  //   freed by every consumer role (leader CTA only)
+  int* tile_ring = reinterpret_cast<int*>(tfree + kTileSlots);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
   int* mt_prefix = reinterpret_cast<int*>(smem + S * Cfg::kStageBytes + 256);
 
   const uint32_t warp = warp_id();
@@ -197,6 +202,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * kCtaGroup);
     }
+    // consumers of a tile index: MMA issuer + epilogue warps of the leader, and (pair) the peer's
+    // producer + epilogue warps
+    for (int i = 0; i < kTileSlots; ++i) {
+      mbar_init(&tfill[i], 1);
+      mbar_init(&tfree[i], kCtaGroup == 1 ? 1 + kEpiWarps : 2 + 2 * kEpiWarps);
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, 512);
@@ -205,18 +216,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto next_tile = [&](int tile, TileInfo& ti) -> bool {
+  auto decode = [&](int tile, TileInfo& ti) -> bool {
     if constexpr (kWgrad) return decode_tile_wgrad(tile, args, Cfg::kBM, ti);
     else return decode_tile(tile, mt_prefix, args, Cfg::kBM, ti);
   };
+  const int total_tiles = kWgrad ? args.n_experts * args.m_tiles * args.n_tiles_n : mt_prefix[args.n_experts] * args.n_tiles_n;
+  // Dynamic in-order tile scheduler: the leader's producer takes tiles from a global counter and
+  // broadcasts each index through a small smem ring (written into the peer CTA too), so the
+  // clusters running at any moment always work on consecutive tiles -- they share the weight
+  // n-block and the expert's rows in L2 (a static round-robin drifts apart over ~200 tiles and
+  // thrashes L2). The index total_tiles is the stop sentinel.
+  auto take_tile = [&](int i, bool peer_data) -> int {
+    const int slot = i % kTileSlots;
+    const uint32_t ph = (i / kTileSlots) & 1;
+    if (peer_data) mbar_wait_cluster(&tfill[slot], ph);
+    else mbar_wait(&tfill[slot], ph);
+    return *reinterpret_cast<volatile int*>(&tile_ring[slot]);
+  };
+  auto free_tile = [&](int i) {
+    const int slot = i % kTileSlots;
+    if (kCtaGroup == 1 || cta_rank == 0) mbar_arrive(&tfree[slot]);
+    else mbar_arrive_cluster(&tfree[slot], 0);
+  };
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (leader: also the tile scheduler) =====================
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
       TileInfo ti;
-      for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
+      for (int i = 0;; ++i) {
+        int tile;
+        if (kCtaGroup == 1 || cta_rank == 0) {
+          const int slot = i % kTileSlots;
+          mbar_wait(&tfree[slot], ((i / kTileSlots) & 1) ^ 1);
+          tile = min(atomicAdd(args.tile_counter, 1), total_tiles);
+          tile_ring[slot] = tile;
+          if constexpr (kCtaGroup == 2) st_shared_cluster_u32(mapa(smem_u32(&tile_ring[slot]), 1), (uint32_t)tile);
+          mbar_arrive(&tfill[slot]);
+          if constexpr (kCtaGroup == 2) mbar_arrive_cluster(&tfill[slot], 1);
+        } else {
+          tile = take_tile(i, true);
+          free_tile(i);
+        }
+        if (tile >= total_tiles || !decode(tile, ti)) break;
         const int a_row = ti.a_row + cta_rank * Cfg::kRowsPerCta;
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
@@ -243,7 +286,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int acc = 0;
       uint32_t aph = 0;
       TileInfo ti;
-      for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
+      for (int i = 0;; ++i) {
+        const int tile = take_tile(i, false);
+        free_tile(i);
+        if (tile >= total_tiles || !decode(tile, ti)) break;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
@@ -274,7 +320,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t aph = 0;
     TileInfo ti;
-    for (int tile = cluster; next_tile(tile, ti); tile += nclusters) {
+    for (int i = 0;; ++i) {
+      const int tile = take_tile(i, kCtaGroup == 2 && cta_rank != 0);
+      __syncwarp();
+      if (lane == 0) free_tile(i);
+      if (tile >= total_tiles || !decode(tile, ti)) break;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int row = ti.a_row + cta_rank * Cfg::kRowsPerCta + row_in_cta;
