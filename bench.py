@@ -347,7 +347,10 @@ def run_ours(args, cfg):
             config=dict(workload=cfg["workload"], T=T, d=d, n_experts=N, top_k=K, d_ff=f,
                         global_batch=T * world, parallelism=("ep%d (experts %d/rank, NCCL all-to-all)" % (world, N // world))
                         if world > 1 else "single",
-                        gemm_ctas=args.gemm_ctas or 2, l2="inputs larger than L2 (x 134 MB, weights 5.6 GB); no flush"),
+                        gemm_ctas=args.gemm_ctas or "auto",
+                        l2=(f"inputs larger than L2 (x {T * d * 2 / 1e6:.0f} MB, weights "
+                            f"{N // world * 3 * d * f * (1 if args.precision == 'fp8' else 2) / 1e9:.1f} GB per rank); "
+                            "no flush needed")),
             roofline=(dict(bound="tensor", kernel="grouped GEMMs fwd+bwd (tcgen05, 6 launches)",
                            achieved=3 * (g1_flop + g2_flop) / (sum(per[k] for k in ("gemm1", "gemm2", "dgrad1_swiglu_bwd",
                                                                                       "dgrad2", "wgrad_out", "wgrad_in"))

@@ -407,7 +407,7 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
   const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
-  const bool big = (T + tpc_big - 1) / tpc_big >= 2 * h->num_sms && RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  const bool big = (T + tpc_big - 1) / tpc_big >= h->num_sms && RouterBigSmem(N, 32, 3).total <= 220 * 1024;
   const bool small = !big && router_smem_bytes(N, 32, 8) <= 220 * 1024;
   const int tpc = big ? tpc_big : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;
