@@ -99,13 +99,23 @@ const char* cl_moe_version(void);
 cl_status cl_moe_create(const cl_moe_config* cfg, const float* w_router, const float* w_in,
                         const float* w_out, cl_moe** out);
 
+/* Creates a layer from a reference checkpoint file (CLCKPT1, proj/include/compasslab/checkpoint.hpp)
+ * holding "<prefix>router" [d x N] and "<prefix>experts.<e>.w_in" [d x 2f] /
+ * "<prefix>experts.<e>.w_out" [f x d] (fp32). Missing tensor / wrong shape -> CL_ERR_RUN. */
+cl_status cl_moe_create_from_checkpoint(const cl_moe_config* cfg, const char* path, const char* prefix,
+                                        cl_moe** out);
+/* Writes the layer's weights (as stored: bf16-valued fp32) in the same format and naming; the
+ * file round-trips byte-exactly through the reference's load_checkpoint / save_checkpoint. */
+cl_status cl_moe_save_checkpoint(cl_moe* h, const char* path, const char* prefix);
+
 /* Creates a layer whose weights are generated on the device from the reference counter PRNG
  * (proj/include/compasslab/prng.hpp) exactly as SURVEY.md §8(d) prescribes (root seed `seed`). */
 cl_status cl_moe_create_synthetic(const cl_moe_config* cfg, uint64_t seed, cl_moe** out);
 
 void cl_moe_destroy(cl_moe* h);
 
-/* Message of the most recent failing call on this handle ("" if none); owned by the handle. */
+/* Message of the most recent failing call on this handle ("" if none); owned by the handle.
+ * With h == NULL: the most recent failing create entry on this thread. */
 const char* cl_moe_last_error(const cl_moe* h);
 
 /* Synthetic tokens x = split(1) N(0,1) of root seed `seed`, rounded to bf16: [T x d] device. */
@@ -171,6 +181,16 @@ cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls);
  * handle's precision. act_scale_* may be given explicitly (host arrays [N_local]) instead. */
 cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream);
 cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float* act_scale_mid);
+/* balance_calibration: with the expert counts of the routed `base` tokens
+ * (bf16 device [T_base x d], may be NULL), pre-route the `pool` tokens (router only, in order)
+ * and select every pool token routed to an expert still below `tau`, until all counts reach tau.
+ * selected (host, capacity P) receives the chosen pool row indices, n_selected their number,
+ * final_counts (host [N]) the resulting counts. Pool exhausted with an expert below tau ->
+ * CL_ERR_RUN naming the expert; tau < 1 -> CL_ERR_CONFIG. */
+cl_status cl_moe_balance_calibration(cl_moe* h, const void* base, int64_t T_base, const void* pool,
+                                     int64_t P, int64_t tau, int64_t* selected, int64_t* n_selected,
+                                     int64_t* final_counts, void* stream);
+
 /* Unified smoothing. compute: s_j = max|X_j|^alpha / max|W_j|^(1-alpha) from the
  * calibration per-channel maxima of the layer input and the joint per-input-channel maxima of
  * every expert's W_in and W_r (zero-max channels -> 1); s_out is a host array [d]. fold: rows

@@ -81,6 +81,8 @@ class Oracle:
                                               C.c_float, C.c_float, _f32p, _f32p]
         else:
             L.ref_gradcheck.argtypes = [C.c_uint64, C.c_int, C.c_double, C.POINTER(C.c_int)]
+            L.ref_ckpt_resave.argtypes = [C.c_char_p, C.c_char_p]
+            L.ref_ckpt_write.argtypes = [C.c_char_p, C.c_char_p, _i64p, _f32p]
             L.ref_moe_backward_full.argtypes = [_f32p, _f32p, _i64, _i64, _i64, _i64, _i64, _f32p, _f32p, _f32p,
                                                 C.c_float, C.c_float, _f32p, _f32p, _f32p, _f32p]
 
@@ -263,6 +265,47 @@ class Oracle:
         out = np.empty_like(x)
         self.lib.orc_round_bf16(x.ravel(), out.ravel(), x.size)
         return out
+
+    # ---- SPEC balance_calibration, restated over route() ----
+    def balance_calibration(self, base, pool, wr, k: int, tau: int):
+        """Counts of the routed base set, then pool tokens in order: a token is taken iff one of
+        its top-k experts is still below tau; stop once every expert reaches tau. Returns
+        (selected pool indices, final counts); raises OracleError naming the expert when the pool
+        runs out first. Pure-Python loop: small cases only."""
+        if tau < 1:
+            raise OracleError("balance_calibration: tau must be >= 1")
+        n = wr.shape[1]
+        cnt = np.zeros(n, np.int64)
+        if base is not None and len(base):
+            cnt += self.route(base, wr, k)["counts"]
+        sel = []
+        if pool is not None and len(pool) and (cnt < tau).any():
+            idx = self.route(pool, wr, k)["topk_idx"]
+            for j in range(idx.shape[0]):
+                if not (cnt < tau).any():
+                    break
+                if (cnt[idx[j]] < tau).any():
+                    cnt[idx[j]] += 1
+                    sel.append(j)
+        low = np.nonzero(cnt < tau)[0]
+        if len(low):
+            e = int(low[0])
+            raise OracleError(f"balance_calibration: token pool exhausted with expert {e} at {cnt[e]} < tau={tau}")
+        return np.array(sel, np.int64), cnt
+
+    # ---- reference checkpoint code (kind "reference" only) ----
+    def ckpt_resave(self, src: str, dst: str) -> None:
+        self._call("ckpt_resave", src.encode(), dst.encode())
+
+    def ckpt_write(self, path: str, tensors: dict) -> None:
+        names = "\n".join(tensors)
+        shapes, vals = [], []
+        for a in tensors.values():
+            a = np.ascontiguousarray(a, np.float32)
+            shapes += [a.ndim] + list(a.shape)
+            vals.append(a.ravel())
+        self._call("ckpt_write", path.encode(), names.encode(), np.array(shapes, np.int64),
+                   np.ascontiguousarray(np.concatenate(vals), np.float32))
 
     def gradcheck(self, seed=20260809, cases=100, tol=1e-4):
         n = C.c_int()

@@ -13,9 +13,11 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <map>
 #include <string>
 #include <vector>
 
+#include "compasslab/checkpoint.hpp"
 #include "compasslab/common.hpp"
 #include "compasslab/gradcheck.hpp"
 #include "compasslab/tensor.hpp"
@@ -260,6 +262,39 @@ int ref_moe_backward_full(const float* x, const float* wr, std::int64_t T, std::
 
 // The reference's own finite-difference gradient suite (gradcheck.cpp:610-656); returns the
 // number of failing ops (0 = all pass) and the number of ops checked in *n_ops.
+// The reference's own checkpoint code (proj/src/checkpoint.cpp): load `in_path`, save it again to
+// `out_path`. A file our writer made is byte-identical to its reference re-save iff the two
+// writers agree; a load failure surfaces the reference's validation message.
+int ref_ckpt_resave(const char* in_path, const char* out_path) {
+  return guarded([&] { compasslab::save_checkpoint(out_path, compasslab::load_checkpoint(in_path)); });
+}
+
+// Writes tensors with the reference's save_checkpoint: names joined by '\n', shapes as
+// (rank, dims...) int64 records, values concatenated in the same order.
+int ref_ckpt_write(const char* out_path, const char* names, const std::int64_t* shapes, const float* values) {
+  return guarded([&] {
+    std::map<std::string, Tensor> ts;
+    std::string all(names);
+    size_t pos = 0;
+    const std::int64_t* sp = shapes;
+    const float* vp = values;
+    while (pos <= all.size() && !all.empty()) {
+      const size_t nl = all.find('\n', pos);
+      const std::string name = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+      const std::int64_t rank = *sp++;
+      compasslab::Shape shape(sp, sp + rank);
+      sp += rank;
+      std::int64_t n = 1;
+      for (auto e : shape) n *= e;
+      ts.emplace(name, Tensor::from_values(shape, vec(vp, n)));
+      vp += n;
+      if (nl == std::string::npos) break;
+      pos = nl + 1;
+    }
+    compasslab::save_checkpoint(out_path, ts);
+  });
+}
+
 int ref_gradcheck(std::uint64_t seed, int cases, double tol, int* n_ops) {
   const auto res = compasslab::run_gradcheck(seed, cases, tol);
   int fails = 0;

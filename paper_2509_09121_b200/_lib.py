@@ -75,6 +75,10 @@ _PROTOS = {
     "cl_moe_version": (C.c_char_p, []),
     "cl_moe_create": (C.c_int, [C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]),
     "cl_moe_create_synthetic": (C.c_int, [C.POINTER(Config), C.c_uint64, C.POINTER(C.c_void_p)]),
+    "cl_moe_create_from_checkpoint": (C.c_int, [C.POINTER(Config), C.c_char_p, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "cl_moe_save_checkpoint": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
+    "cl_moe_balance_calibration": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64,
+                                             C.c_void_p, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p]),
     "cl_moe_destroy": (None, [C.c_void_p]),
     "cl_moe_last_error": (C.c_char_p, [C.c_void_p]),
     "cl_moe_synthetic_tokens": (C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]),

@@ -22,6 +22,7 @@
 #include "synth_pack.cuh"
 #include "ep.cuh"
 #include "bwd_kernels.cuh"
+#include "ckpt.hpp"
 
 using namespace cmoe;
 
@@ -987,6 +988,131 @@ cl_status cl_moe_backward_full(cl_moe* h, const void* d_out, float g_aux, float 
   });
 }
 
+// ---- reference checkpoint format (CLCKPT1, proj/include/compasslab/checkpoint.hpp:4-9) ----
+// Failures of the create entries (no handle exists yet) are kept per thread.
+static thread_local std::string g_create_error;
+
+cl_status cl_moe_create_from_checkpoint(const cl_moe_config* cfg, const char* path, const char* prefix, cl_moe** out) {
+  if (!out || !cfg) return CL_ERR_CONFIG;
+  *out = nullptr;
+  try {
+    if (!path) return CL_ERR_CONFIG;
+    const std::string pre = prefix ? prefix : "";
+    const Checkpoint c = Checkpoint::load(path);
+    const int ep = cfg->ep_size <= 0 ? 1 : cfg->ep_size;
+    if (cfg->n_experts < 1 || cfg->n_experts % ep) {
+      g_create_error = "n_experts must be a positive multiple of ep_size";
+      return CL_ERR_CONFIG;
+    }
+    const int64_t d = cfg->d_model, N = cfg->n_experts, f = cfg->d_ff, NL = N / ep, e0 = cfg->ep_rank * NL;
+    const std::vector<float> wr = c.get(pre + "router", {d, N});
+    std::vector<float> w_in((size_t)NL * d * 2 * f), w_out((size_t)NL * f * d);
+    for (int64_t e = 0; e < NL; ++e) {
+      const std::string ex = pre + "experts." + std::to_string(e0 + e) + ".";
+      std::memcpy(w_in.data() + e * d * 2 * f, c.get(ex + "w_in", {d, 2 * f}).data(), sizeof(float) * d * 2 * f);
+      std::memcpy(w_out.data() + e * f * d, c.get(ex + "w_out", {f, d}).data(), sizeof(float) * f * d);
+    }
+    return cl_moe_create(cfg, wr.data(), w_in.data(), w_out.data(), out);
+  } catch (const std::exception& e) {
+    g_create_error = std::string("cl_moe_create_from_checkpoint: ") + e.what();
+    return CL_ERR_RUN;
+  }
+}
+
+cl_status cl_moe_save_checkpoint(cl_moe* h, const char* path, const char* prefix) {
+  return guarded(h, [&] {
+    if (!path) throw ConfigErr("path is null");
+    CK(cudaSetDevice(h->cfg.device));
+    const std::string pre = prefix ? prefix : "";
+    const int64_t d = h->d, N = h->N, f = h->f, NL = h->n_local;
+    std::vector<float> wr(d * N), win((size_t)NL * d * 2 * f), wout((size_t)NL * f * d);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(wr.data(), h->wr, sizeof(float) * d * N, cudaMemcpyDeviceToHost));
+    // packed bf16 -> reference layouts on device, then widen on the host
+    __nv_bfloat16* tmp = dalloc<__nv_bfloat16>((size_t)d * 2 * f);
+    std::vector<uint16_t> hb((size_t)d * 2 * f);
+    auto widen = [&](const std::vector<uint16_t>& src, float* dst, size_t n) {
+      for (size_t i = 0; i < n; ++i) {
+        const uint32_t u = static_cast<uint32_t>(src[i]) << 16;
+        std::memcpy(dst + i, &u, 4);
+      }
+    };
+    for (int64_t e = 0; e < NL; ++e) {
+      transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
+          h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, tmp);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * d * 2 * f, cudaMemcpyDeviceToHost));
+      widen(hb, win.data() + e * d * 2 * f, (size_t)d * 2 * f);
+      transpose_weight_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)(f / 32)), 256>>>(
+          h->wout + (size_t)e * d * f, (int)d, (int)f, (int)f, tmp);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * f * d, cudaMemcpyDeviceToHost));
+      widen(hb, wout.data() + e * f * d, (size_t)f * d);
+    }
+    cudaFree(tmp);
+    std::map<std::string, std::pair<std::vector<int64_t>, const float*>> ts;
+    ts[pre + "router"] = {{d, N}, wr.data()};
+    for (int64_t e = 0; e < NL; ++e) {
+      const std::string ex = pre + "experts." + std::to_string(h->e0 + e) + ".";
+      ts[ex + "w_in"] = {{d, 2 * f}, win.data() + e * d * 2 * f};
+      ts[ex + "w_out"] = {{f, d}, wout.data() + e * f * d};
+    }
+    Checkpoint::save(path, ts);
+  });
+}
+
+// ---- balance_calibration ----
+cl_status cl_moe_balance_calibration(cl_moe* h, const void* base, int64_t T_base, const void* pool, int64_t P,
+                                     int64_t tau, int64_t* selected, int64_t* n_selected, int64_t* final_counts,
+                                     void* stream) {
+  return guarded(h, [&] {
+    if (tau < 1) throw ConfigErr("balance_calibration: tau must be >= 1");
+    if (!selected || !n_selected || !final_counts || (P > 0 && !pool)) throw ConfigErr("null argument");
+    CK(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t N = h->N, K = h->K, d = h->d;
+    std::vector<int64_t> cnt(N, 0);
+    std::vector<int32_t> c32(N);
+    if (base && T_base > 0) {
+      for (int64_t t0 = 0; t0 < T_base; t0 += h->cap) {
+        const int64_t t = std::min<int64_t>(h->cap, T_base - t0);
+        run_router(h, static_cast<const __nv_bfloat16*>(base) + t0 * d, t, st);
+        CK(cudaMemcpyAsync(c32.data(), h->rb.counts, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int64_t e = 0; e < N; ++e) cnt[e] += c32[e];
+      }
+    }
+    // pre-route the pool (router only) and greedily take tokens routed to a deficit expert
+    std::vector<int32_t> idx;
+    int64_t ns = 0;
+    auto deficit = [&]() {
+      for (int64_t e = 0; e < N; ++e)
+        if (cnt[e] < tau) return true;
+      return false;
+    };
+    for (int64_t t0 = 0; t0 < P && deficit(); t0 += h->cap) {
+      const int64_t t = std::min<int64_t>(h->cap, P - t0);
+      run_router(h, static_cast<const __nv_bfloat16*>(pool) + t0 * d, t, st);
+      idx.resize(t * K);
+      CK(cudaMemcpyAsync(idx.data(), h->rb.topk_idx, sizeof(int32_t) * t * K, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int64_t j = 0; j < t && deficit(); ++j) {
+        bool useful = false;
+        for (int64_t k = 0; k < K; ++k) useful |= cnt[idx[j * K + k]] < tau;
+        if (!useful) continue;
+        for (int64_t k = 0; k < K; ++k) cnt[idx[j * K + k]] += 1;
+        selected[ns++] = t0 + j;
+      }
+    }
+    *n_selected = ns;
+    for (int64_t e = 0; e < N; ++e) final_counts[e] = cnt[e];
+    for (int64_t e = 0; e < N; ++e)
+      if (cnt[e] < tau)
+        throw RunErr(fmt("balance_calibration: token pool exhausted with expert %lld at %lld < tau=%lld", (long long)e,
+                         (long long)cnt[e], (long long)tau));
+  });
+}
+
 cl_status cl_moe_ep_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank, int64_t* local_offsets,
                            int64_t* recv_piece, int64_t* recv_total) {
   if (!counts || !local_offsets || !recv_piece || R < 1 || N < R || N % R || rank < 0 || rank >= R)
@@ -999,7 +1125,7 @@ cl_status cl_moe_ep_layout(const int64_t* counts, int32_t R, int32_t N, int32_t 
 
 const char* cl_moe_version(void) { return "0.1.0-sm100a"; }
 
-const char* cl_moe_last_error(const cl_moe* h) { return h == nullptr ? "" : h->last_error.c_str(); }
+const char* cl_moe_last_error(const cl_moe* h) { return h == nullptr ? g_create_error.c_str() : h->last_error.c_str(); }
 
 static cl_status create_common(const cl_moe_config* cfg, cl_moe** out, const float* w_router, const float* w_in,
                                const float* w_out, bool synthetic, uint64_t seed) {
@@ -1044,7 +1170,7 @@ static cl_status create_common(const cl_moe_config* cfg, cl_moe** out, const flo
     build_maps(h, false);
   });
   if (st != CL_OK) {
-    std::fprintf(stderr, "cl_moe_create: %s\n", h->last_error.c_str());
+    g_create_error = h->last_error;
     delete h;
     return st;
   }

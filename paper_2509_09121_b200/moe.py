@@ -66,13 +66,16 @@ def _stream(device) -> C.c_void_p:
 class MoELayer:
     """One MoE layer (router + N gated experts) resident on one B200."""
 
-    def __init__(self, cfg: MoEConfig, w_router=None, w_in=None, w_out=None, seed: int | None = None):
+    def __init__(self, cfg: MoEConfig, w_router=None, w_in=None, w_out=None, seed: int | None = None,
+                 checkpoint: str | None = None, prefix: str = ""):
         self.cfg = cfg
         self.L = _lib.lib()
         self.h = C.c_void_p()
         self.device = torch.device("cuda", cfg.device)
         c = cfg.to_c()
-        if seed is not None:
+        if checkpoint is not None:
+            rc = self.L.cl_moe_create_from_checkpoint(C.byref(c), checkpoint.encode(), prefix.encode(), C.byref(self.h))
+        elif seed is not None:
             rc = self.L.cl_moe_create_synthetic(C.byref(c), seed, C.byref(self.h))
         else:
             wr = np.ascontiguousarray(w_router, np.float32)
@@ -81,7 +84,7 @@ class MoELayer:
             rc = self.L.cl_moe_create(C.byref(c), wr.ctypes.data, wi.ctypes.data, wo.ctypes.data, C.byref(self.h))
         if rc != _lib.CL_OK:
             cls = MoEConfigError if rc == _lib.CL_ERR_CONFIG else MoEError
-            raise cls(f"cl_moe_create failed with status {rc}")
+            raise cls(f"cl_moe_create failed with status {rc}: {self.L.cl_moe_last_error(None).decode()}")
 
     def close(self):
         if self.h:
@@ -199,6 +202,22 @@ class MoELayer:
             b = np.ascontiguousarray(act_scale_mid, np.float32)
             rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
         self._check(rc, "quantize_fp8")
+
+    def save_checkpoint(self, path: str, prefix: str = "") -> None:
+        self._check(self.L.cl_moe_save_checkpoint(self.h, path.encode(), prefix.encode()), "save_checkpoint")
+
+    def balance_calibration(self, base, pool, tau: int):
+        """SPEC balance_calibration: (selected pool row indices, final counts)."""
+        base = None if base is None else self._bf16(base)
+        pool = None if pool is None else self._bf16(pool)
+        p = 0 if pool is None else pool.shape[0]
+        sel = np.empty(max(p, 1), np.int64)
+        ns = C.c_int64()
+        fc = np.empty(self.cfg.n_experts, np.int64)
+        self._check(self.L.cl_moe_balance_calibration(self.h, _ptr(base), 0 if base is None else base.shape[0],
+                                                      _ptr(pool), p, tau, sel.ctypes.data, C.byref(ns), fc.ctypes.data,
+                                                      _stream(self.device)), "balance_calibration")
+        return sel[:ns.value], fc
 
     def compute_smoothing(self, alpha: float = 0.5) -> np.ndarray:
         s = np.empty(self.cfg.d_model, np.float32)
