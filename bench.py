@@ -208,6 +208,13 @@ def run_ours(args, cfg):
         dist.broadcast_object_list(obj, src=0)
         layer.ep_init(obj[0])
     train = bool(cfg.get("train"))
+    transport = "NCCL send/recv"
+    if world > 1 and not train and args.ep_transport == "peer":
+        try:
+            layer.ep_peer_init()
+            transport = "NVLink peer stores from the dispatch kernel and the GEMM2 epilogue; NCCL for counts"
+        except Exception as e:  # no P2P between the devices: keep the NCCL transport, say so
+            transport = f"NCCL send/recv (peer transport unavailable: {e})"
     if cfg.get("skew"):
         layer.synthetic_skew(cfg["skew"])
     x = layer.synthetic_tokens(T, SEED + rank, shift=1.0 if cfg.get("skew") else 0.0)
@@ -345,7 +352,7 @@ def run_ours(args, cfg):
             dtype="bf16" if args.precision == "bf16" else "e4m3 (fp32 accumulate, bf16 activations in/out)",
             data="synthetic (device-generated reference-PRNG tokens and random-init weights)",
             config=dict(workload=cfg["workload"], T=T, d=d, n_experts=N, top_k=K, d_ff=f,
-                        global_batch=T * world, parallelism=("ep%d (experts %d/rank, NCCL all-to-all)" % (world, N // world))
+                        global_batch=T * world, parallelism=("ep%d (experts %d/rank; rows: %s)" % (world, N // world, transport))
                         if world > 1 else "single",
                         gemm_ctas=args.gemm_ctas or "auto",
                         l2=(f"inputs larger than L2 (x {T * d * 2 / 1e6:.0f} MB, weights "
@@ -416,6 +423,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp8"])
     ap.add_argument("--tokens", type=int, default=0, help="override T (tokens per rank)")
+    ap.add_argument("--ep-transport", default="peer", choices=["peer", "nccl"],
+                    help="N>1 forward: rows over NVLink peer stores (dispatch kernel / GEMM2 epilogue) or NCCL p2p")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]

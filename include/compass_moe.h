@@ -237,6 +237,25 @@ cl_status cl_moe_ep_init(cl_moe* h, const uint8_t* id);
  * ep_size == 1 this runs the same exchange code in loopback). bf16 only. */
 cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
                             const cl_moe_decision* decision, void* stream);
+/* Switches an initialised EP handle to the peer-memory (NVLink) transport: collective over the
+ * ranks; maps every rank's receive buffer and return buffer into this process (CUDA IPC, handles
+ * exchanged over the communicator). Afterwards the forward moves rows with direct peer stores —
+ * the dispatch kernel writes into the owners' receive buffers and the GEMM2 epilogue writes each
+ * output row back into its source rank's buffer — and NCCL carries only the counts and two
+ * barriers. Training keeps the NCCL transport. Needs P2P access between the devices; if any
+ * rank cannot map its peers, every rank returns CL_ERR_RUN and keeps the NCCL transport. */
+cl_status cl_moe_ep_peer_init(cl_moe* h);
+/* Single-process, single-device emulation of an R-rank EP group (handles hs[r] created with
+ * ep_size = R, ep_rank = r on the same device, no communicator): runs the peer-transport forward
+ * for every rank, phase by phase, with the other handles' buffers as the "peer" addresses. */
+cl_status cl_moe_ep_group_forward(cl_moe* const* hs, int32_t R, const void* const* hidden,
+                                  const int64_t* T, void* const* out, void* stream);
+/* Pure host helper (no GPU): peer-transport layout of `rank` from counts[R][N]:
+ * dispatch_row[g] = first row of this rank's piece for expert g in the owner's receive buffer;
+ * return_row[e*R+s] = first row of piece (local expert e, source s) in s's permutation;
+ * local_offsets[N/R+1] as in cl_moe_ep_layout. */
+cl_status cl_moe_ep_peer_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank,
+                                int64_t* dispatch_row, int64_t* return_row, int64_t* local_offsets);
 /* Pure host helper (no GPU): receive layout of `rank` from the all-gathered count matrix
  * counts[R][N] (row = source rank). local_offsets[N/R+1], recv_piece[(N/R)*R] indexed
  * e*R + s = first receive row of (local expert e, source s); recv_total = rows received. */

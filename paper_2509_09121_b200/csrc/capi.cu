@@ -169,6 +169,17 @@ struct cl_moe {
   __nv_bfloat16* dYsrc = nullptr;       // EP training: source-order dY [cap*K][d]
   __nv_bfloat16* dXsrc = nullptr;       // EP training: source-order dX [cap*K][d]
   CUtensorMap mA1e[2], mA2e[2];
+  // peer-memory (NVLink) transport (ep.cuh): 0 = NCCL send/recv, 1 = direct peer stores
+  int ep_transport = 0;
+  char** peer_x_dev = nullptr;          // [R] every rank's x_recv, as mapped in this process
+  char** peer_y_dev = nullptr;          // [R] every rank's y (source-order return buffer)
+  float** peer_w_dev = nullptr;         // [R] every rank's w_recv
+  float* w_recv = nullptr;              // [recv_cap] combine weight of each received row
+  void** expert_dst = nullptr;          // [N] dispatch destinations of this rank's pieces
+  float** expert_dst_w = nullptr;       // [N] ... of their combine weights
+  void** row_ptr = nullptr;             // [recv_cap] return address of every received row
+  float* bar_buf = nullptr;             // [1] payload of the exchange barriers
+  std::vector<void*> ipc_opened;        // peers' buffers mapped through CUDA IPC
 
   // training (expert-FFN backward)
   bool train_ready = false;
@@ -206,8 +217,11 @@ struct cl_moe {
     for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
                     (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
                     (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
-                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter})
+                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
+                    (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
+                    (void*)row_ptr, (void*)bar_buf})
       if (p) cudaFree(p);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
     if (comm) NcclApi::get().CommDestroy(comm);
@@ -453,7 +467,7 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
 // GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
 void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
-               cudaStream_t st, __nv_bfloat16* h_save = nullptr) {
+               cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
@@ -488,6 +502,7 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g2.out = y;
   g2.ldo = static_cast<int>(h->d);
   g2.row_scale = row_w;
+  g2.row_ptr = row_ptr;
   g2.act_scale = h->sx_mid;
   g2.w_scale = h->ws_out;
   const int v = h->gemm_ctas == 2 ? 1 : 0;
@@ -646,9 +661,15 @@ void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStr
 // all-gather, (expert, source)-piece exchange, local grouped GEMMs, reverse exchange, weighted
 // combine. Requires cl_moe_ep_init. bf16 only in this round. `train` keeps H / A^T on the expert
 // side for cl_moe_backward.
+void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st);
+
 void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
   if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
   if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
+  if (h->ep_transport == 1 && !train) {
+    run_ep_peer(h, x, T, out, out_f32, st);
+    return;
+  }
   NcclApi& nc = NcclApi::get();
   const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
   const int rank = h->cfg.ep_rank;
@@ -700,6 +721,77 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
     h->train_T = T;
     h->cur_x = x;
   }
+}
+
+// ---- peer-memory transport (ep.cuh): phases shared by the multi-process path and the
+// single-process emulation group ----
+void ep_peer_alloc(cl_moe* h) {
+  if (h->row_ptr) return;
+  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  h->peer_x_dev = dalloc<char*>(R);
+  h->peer_y_dev = dalloc<char*>(R);
+  h->peer_w_dev = dalloc<float*>(R);
+  h->w_recv = dalloc<float>(h->recv_cap);
+  h->expert_dst = dalloc<void*>(h->N);
+  h->expert_dst_w = dalloc<float*>(h->N);
+  h->row_ptr = dalloc<void*>(h->recv_cap);
+  h->bar_buf = dalloc<float>(1);
+  CK(cudaMemset(h->bar_buf, 0, sizeof(float)));
+}
+
+void ep_peer_layout(cl_moe* h, cudaStream_t st) {
+  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  ep_peer_layout_kernel<<<h->n_local * R + 1, 256, 0, st>>>(h->ep_counts_dev, R, (int)h->N, h->cfg.ep_rank, h->recv_cap,
+                                                             h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
+                                                             h->expert_dst, h->expert_dst_w, h->ep_off_dev, h->row_ptr,
+                                                             h->rb.finite_flag);
+  CK(cudaGetLastError());
+}
+
+void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
+  const int blocks = static_cast<int>((T + 7) / 8);
+  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
+                                                 (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
+                                                 h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
+                                                 h->expert_dst_w);
+  CK(cudaGetLastError());
+  prof_mark(h, 2, st);
+}
+
+void ep_peer_experts(cl_moe* h, cudaStream_t st) {
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, h->w_recv, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st, nullptr,
+            h->row_ptr);
+  prof_mark(h, 4, st);
+}
+
+void ep_peer_combine(cl_moe* h, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  // rows arrive already scaled by their combine weight (GEMM2 epilogue), as on one GPU
+  if (out_f32)
+    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
+  else
+    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                  h->rb.finite_flag, st);
+  CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
+  h->last_rows = T * h->K;
+}
+
+// Multi-process forward over NVLink peer memory. NCCL carries only the R x N counts and two
+// one-float barriers; the rows move as direct stores of the dispatch kernel and of the GEMM2
+// epilogue. No host synchronisation: the layout is computed on the device.
+//   all-gather(counts) -> layout -> dispatch (stores into owners' x_recv) -> barrier
+//   -> GEMM1 -> GEMM2 (epilogue stores into sources' y) -> barrier -> combine
+// The first all-gather also orders this forward after every rank's previous use of x_recv / y.
+void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  NcclApi& nc = NcclApi::get();
+  NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)h->N, NcclApi::kInt32, h->comm, st));
+  ep_peer_layout(h, st);
+  ep_peer_dispatch(h, x, T, st);
+  NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+  ep_peer_experts(h, st);
+  NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+  ep_peer_combine(h, T, out, out_f32, st);
 }
 
 void ensure_training(cl_moe* h) {
@@ -940,6 +1032,132 @@ cl_status cl_moe_ep_init(cl_moe* h, const uint8_t* id) {
     NCK(NcclApi::get().CommInitRank(&h->comm, R, uid, h->cfg.ep_rank));
     ep_alloc(h);
   });
+}
+
+cl_status cl_moe_ep_peer_init(cl_moe* h) {
+  return guarded(h, [&] {
+    if (!h->comm) throw ConfigErr("cl_moe_ep_peer_init needs cl_moe_ep_init first");
+    CK(cudaSetDevice(h->cfg.device));
+    const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size, rank = h->cfg.ep_rank;
+    ep_peer_alloc(h);
+    // exchange the IPC handles of x_recv and y over the communicator
+    constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+    constexpr int kB = 3;  // x_recv, y, w_recv
+    void* const own[kB] = {h->x_recv, h->y, h->w_recv};
+    std::vector<uint8_t> mine(kB * kH), all(kB * kH * R);
+    for (int b = 0; b < kB; ++b) {
+      cudaIpcMemHandle_t hb;
+      CK(cudaIpcGetMemHandle(&hb, own[b]));
+      std::memcpy(mine.data() + b * kH, &hb, kH);
+    }
+    uint8_t* dbuf = dalloc<uint8_t>(kB * kH * (R + 1));
+    cudaStream_t st = nullptr;
+    CK(cudaMemcpy(dbuf, mine.data(), kB * kH, cudaMemcpyHostToDevice));
+    NCK(NcclApi::get().AllGather(dbuf, dbuf + kB * kH, kB * kH, NcclApi::kUint8, h->comm, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(all.data(), dbuf + kB * kH, kB * kH * R, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    std::vector<void*> peer[kB];
+    for (int b = 0; b < kB; ++b) peer[b].assign(R, nullptr);
+    std::string why;
+    for (int s = 0; s < R && why.empty(); ++s)
+      for (int b = 0; b < kB && why.empty(); ++b) {
+        if (s == rank) {
+          peer[b][s] = own[b];
+          continue;
+        }
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, all.data() + ((size_t)s * kB + b) * kH, kH);
+        void* p = nullptr;
+        const cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          why = fmt("rank %d cannot map rank %d's buffers: %s", rank, s, cudaGetErrorString(e));
+          break;
+        }
+        h->ipc_opened.push_back(p);
+        peer[b][s] = p;
+      }
+    // all ranks switch together or not at all
+    float* okf = dalloc<float>(1);
+    const float bad = why.empty() ? 0.f : 1.f;
+    CK(cudaMemcpy(okf, &bad, sizeof(float), cudaMemcpyHostToDevice));
+    NCK(NcclApi::get().AllReduce(okf, okf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+    CK(cudaStreamSynchronize(st));
+    float nbad = 0.f;
+    CK(cudaMemcpy(&nbad, okf, sizeof(float), cudaMemcpyDeviceToHost));
+    cudaFree(okf);
+    if (nbad > 0.f) {
+      for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
+      h->ipc_opened.clear();
+      throw RunErr(why.empty() ? fmt("peer transport unavailable on %d rank(s); keeping NCCL", (int)nbad) : why);
+    }
+    CK(cudaMemcpy(h->peer_x_dev, peer[0].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->peer_y_dev, peer[1].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->peer_w_dev, peer[2].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    h->ep_transport = 1;
+  });
+}
+
+// Single-process emulation of R expert-parallel ranks on one device (test and bring-up path):
+// the same layout / dispatch / GEMM / combine kernels with "peer" addresses that are the other
+// handles' buffers. Every phase runs for all ranks before the next one starts, in stream order,
+// so no kernel ever waits on another; the count all-gather becomes R x R device copies.
+cl_status cl_moe_ep_group_forward(cl_moe* const* hs, int32_t R, const void* const* hidden, const int64_t* T,
+                                  void* const* out, void* stream) {
+  if (!hs || R < 1 || !hidden || !T || !out) return CL_ERR_CONFIG;
+  for (int r = 0; r < R; ++r)
+    if (!hs[r]) return CL_ERR_CONFIG;
+  cl_moe* h0 = hs[0];
+  return guarded(h0, [&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = static_cast<int>(h0->N);
+    for (int r = 0; r < R; ++r) {
+      cl_moe* h = hs[r];
+      if (h->cfg.ep_size != R || h->cfg.ep_rank != r || h->N != N || h->d != h0->d || h->f != h0->f ||
+          h->K != h0->K || h->cfg.device != h0->cfg.device)
+        throw ConfigErr(fmt("handle %d is not rank %d of a matching %d-rank group", r, r, R));
+      if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
+      if (!hidden[r] || !out[r]) throw ConfigErr("null argument");
+    }
+    CK(cudaSetDevice(h0->cfg.device));
+    std::vector<char*> px(R), py(R);
+    std::vector<float*> pw(R);
+    for (int r = 0; r < R; ++r) {
+      ep_alloc(hs[r]);
+      ep_peer_alloc(hs[r]);
+      px[r] = reinterpret_cast<char*>(hs[r]->x_recv);
+      py[r] = reinterpret_cast<char*>(hs[r]->y);
+      pw[r] = hs[r]->w_recv;
+    }
+    for (int r = 0; r < R; ++r) {
+      CK(cudaMemcpyAsync(hs[r]->peer_x_dev, px.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(hs[r]->peer_y_dev, py.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(hs[r]->peer_w_dev, pw.data(), sizeof(float*) * R, cudaMemcpyHostToDevice, st));
+    }
+    for (int r = 0; r < R; ++r) run_router(hs[r], hidden[r], T[r], st);
+    for (int r = 0; r < R; ++r)
+      for (int s = 0; s < R; ++s)
+        CK(cudaMemcpyAsync(hs[r]->ep_counts_dev + (size_t)s * N, hs[s]->rb.counts, sizeof(int32_t) * N,
+                           cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < R; ++r) ep_peer_layout(hs[r], st);
+    for (int r = 0; r < R; ++r) ep_peer_dispatch(hs[r], hidden[r], T[r], st);
+    for (int r = 0; r < R; ++r) ep_peer_experts(hs[r], st);
+    for (int r = 0; r < R; ++r) ep_peer_combine(hs[r], T[r], out[r], false, st);
+    CK(cudaStreamSynchronize(st));  // the host pointer tables above must outlive their copies
+  });
+}
+
+cl_status cl_moe_ep_peer_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank, int64_t* dispatch_row,
+                                int64_t* return_row, int64_t* local_offsets) {
+  if (!counts || !dispatch_row || !return_row || !local_offsets || R < 1 || N < R || N % R || rank < 0 || rank >= R)
+    return CL_ERR_CONFIG;
+  const int NL = N / R;
+  for (int g = 0; g < N; ++g) dispatch_row[g] = ep_piece_row(counts, R, N, g / NL, g % NL, rank);
+  for (int e = 0; e < NL; ++e)
+    for (int s = 0; s < R; ++s) return_row[e * R + s] = ep_src_row(counts, N, s, rank * NL + e);
+  for (int e = 0; e <= NL; ++e) local_offsets[e] = ep_piece_row(counts, R, N, rank, e, 0);
+  return CL_OK;
 }
 
 cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
@@ -1331,6 +1549,7 @@ cl_status cl_moe_sync(cl_moe* h, void* stream) {
     CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
     if (flag) {
       CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
+      if (flag & 2) throw RunErr("expert-parallel receive buffer overflow");
       throw RunErr("non-finite value produced by op 'moe_forward'");
     }
   });

@@ -88,4 +88,81 @@ inline int64_t ep_layout(const int64_t* C, int R, int N, int rank, int64_t* loca
   return row;
 }
 
+// ---- peer-memory (NVLink) transport ----
+// With every rank's receive buffer x_recv and return buffer y mapped into every peer (CUDA IPC),
+// the two exchanges need no copy engine and no NCCL data movement:
+//   dispatch: the source's dispatch kernel stores each (token, k) row straight into the owner's
+//             x_recv at the row ep_piece_row(owner, e, source) + rank-within-expert, and its
+//             combine weight into the owner's w_recv (GEMM2 scales rows exactly as on one GPU,
+//             so the layer output is bit-identical for every EP degree);
+//   return:   the owner's GEMM2 epilogue stores each output row straight into the source's y at
+//             ep_src_row(source, g) + row-within-piece, so the return exchange overlaps GEMM2
+//             tile by tile.
+// All ranks evaluate these from the same all-gathered C, so the layout is consistent by
+// construction. The helpers below are shared by the host restatement (cl_moe_ep_peer_layout,
+// tested on the CPU) and the device layout kernel.
+template <typename CT>
+__host__ __device__ inline int64_t ep_piece_row(const CT* C, int R, int N, int owner, int e, int s) {
+  const int NL = N / R;
+  int64_t row = 0;
+  for (int e2 = 0; e2 < e; ++e2)
+    for (int s2 = 0; s2 < R; ++s2) row += C[(int64_t)s2 * N + owner * NL + e2];
+  for (int s2 = 0; s2 < s; ++s2) row += C[(int64_t)s2 * N + owner * NL + e];
+  return row;
+}
+
+// First row of global expert g's piece in source s's expert-major permutation.
+template <typename CT>
+__host__ __device__ inline int64_t ep_src_row(const CT* C, int N, int s, int g) {
+  int64_t row = 0;
+  for (int g2 = 0; g2 < g; ++g2) row += C[(int64_t)s * N + g2];
+  return row;
+}
+
+#ifdef __CUDACC__
+// Device layout for `rank` from the all-gathered counts C (R x N int32):
+//   expert_dst[g]   address of this rank's first row for expert g in the owner's x_recv
+//   expert_dst_w[g] the same row in the owner's w_recv (combine weight of each received row)
+//   ep_off[e]       (NL+1) local expert offsets in this rank's x_recv (GEMM row groups)
+//   row_ptr[r]      for every received row r: its return address in the source rank's y
+// Blocks 0..NL*R-1 fill row_ptr for one (local expert, source) piece each; the last block checks
+// every owner's receive total against recv_cap (the same verdict on all ranks) and on overflow
+// sets bit 2 of `flag`, nulls expert_dst and zeroes ep_off, so nothing is written anywhere.
+__global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __restrict__ C, int R, int N, int rank,
+                                                             int64_t recv_cap, int64_t row_bytes,
+                                                             char* const* __restrict__ peer_x,
+                                                             char* const* __restrict__ peer_y,
+                                                             float* const* __restrict__ peer_w, void** expert_dst,
+                                                             float** expert_dst_w, int32_t* ep_off, void** row_ptr,
+                                                             int32_t* flag) {
+  const int NL = N / R;
+  if (blockIdx.x < (unsigned)(NL * R)) {
+    const int e = blockIdx.x / R, s = blockIdx.x % R, g = rank * NL + e;
+    const int64_t start = ep_piece_row(C, R, N, rank, e, s);
+    const int64_t n = C[(int64_t)s * N + g];
+    char* dst = peer_y[s] + ep_src_row(C, N, s, g) * row_bytes;
+    for (int64_t j = threadIdx.x; j < n && start + j < recv_cap; j += blockDim.x)
+      row_ptr[start + j] = dst + j * row_bytes;
+    return;
+  }
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    int good = 1;
+    for (int o = 0; o < R; ++o)
+      if (ep_piece_row(C, R, N, o, NL, 0) > recv_cap) good = 0;
+    ok = good;
+    if (!good) atomicOr(flag, 2);
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < N; g += blockDim.x) {
+    const int o = g / NL, e = g % NL;
+    const int64_t row = ep_piece_row(C, R, N, o, e, rank);
+    expert_dst[g] = ok ? peer_x[o] + row * row_bytes : nullptr;
+    expert_dst_w[g] = ok ? peer_w[o] + row : nullptr;
+  }
+  for (int e = threadIdx.x; e <= NL; e += blockDim.x)
+    ep_off[e] = ok ? static_cast<int32_t>(ep_piece_row(C, R, N, rank, e, 0)) : 0;
+}
+#endif
+
 }  // namespace cmoe

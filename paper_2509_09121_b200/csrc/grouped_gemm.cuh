@@ -54,6 +54,7 @@ struct GemmArgs {
   void* aux_t;              // training: transposed copy of the output, bf16 [C][rp] (nullable)
   int64_t rp;               // row stride of aux_t (padded-row capacity)
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
+  void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
 };
 
 constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
@@ -128,6 +129,12 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v
   for (int i = 0; i < 4; ++i)
     st_global_v4_hint(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
                       pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]), pol);
+}
+__device__ __forceinline__ void store_bf16x32_plain(__nv_bfloat16* dst, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    st_global_v4(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                 pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
 }
 __device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* src, float* v) {
 #pragma unroll
@@ -407,7 +414,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               v[i] = __uint_as_float(a[i]) * rs;
               if constexpr (kFp8) v[i] *= ws[c * 32 + i];
             }
-            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32, v);
+            if (args.row_ptr)  // peer transport: the row returns to its source rank over NVLink
+              store_bf16x32_plain(static_cast<__nv_bfloat16*>(args.row_ptr[row]) + ti.nt * kBN + c * 32, v);
+            else
+              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32, v);
           }
         }
       } else if constexpr (kEpi == EPI_SWIGLU_BWD) {
@@ -490,6 +500,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
+  if constexpr (kEpi == EPI_ROWSCALE)
+    if (args.row_ptr && warp >= 4) __threadfence_system();  // peer rows visible before the exchange barrier
   tc_fence_before();
   if constexpr (kCtaGroup == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();

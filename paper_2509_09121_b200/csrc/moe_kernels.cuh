@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
         slog[tl * N4 + e] = z;
         if (tok < T && e < N) {
           rb.logits[(size_t)tok * N + e] = z;
-          if (!isfinite(z)) atomicExch(rb.finite_flag, 1);
+          if (!isfinite(z)) atomicOr(rb.finite_flag, 1);
         }
       }
     }
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
         slog[tl * N4 + e] = z;
         if (tok < T && e < N) {
           rb.logits[(size_t)tok * N + e] = z;
-          if (!isfinite(z)) atomicExch(rb.finite_flag, 1);
+          if (!isfinite(z)) atomicOr(rb.finite_flag, 1);
         }
       }
     }
@@ -515,18 +515,32 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
                                                        int K, int tpc, RouteBufs rb, const int32_t* __restrict__ idx,
                                                        const float* __restrict__ wts, void* __restrict__ xperm,
                                                        int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-                                                       float* __restrict__ row_w, const float* __restrict__ act_scale) {
+                                                       float* __restrict__ row_w, const float* __restrict__ act_scale,
+                                                       void* const* __restrict__ expert_dst = nullptr,
+                                                       float* const* __restrict__ expert_dst_w = nullptr) {
+  // expert_dst (peer transport, ep.cuh): row r of expert e goes to expert_dst[e] + (r - offsets[e])
+  // rows — the owner's receive buffer over NVLink — instead of xperm; null entries (overflow) skip.
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= T) return;
   const int tile = j / tpc;
   int rows[8];
   float sc[8];
+  void* dsts[8];
   for (int k = 0; k < K; ++k) {
     const size_t s = (size_t)j * K + k;
     const int e = idx[s];
     const int r = rb.offsets[e] + rb.tile_cnt[(size_t)tile * N + e] + rb.local_rank[s];
     rows[k] = r;
+    if constexpr (!kFp8) {
+      if (expert_dst) {
+        char* b = static_cast<char*>(expert_dst[e]);
+        dsts[k] = b ? b + (size_t)(r - rb.offsets[e]) * d * 2 : nullptr;
+        if (lane == 0 && b) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
+      } else {
+        dsts[k] = reinterpret_cast<__nv_bfloat16*>(xperm) + (size_t)r * d;
+      }
+    }
     if constexpr (kFp8) sc[k] = act_scale[e];
     if (lane == 0) {
       inv[s] = r;
@@ -543,12 +557,14 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
       for (int u = 0; u < 4; ++u)
         if (v0 + u * 32 < nvec) buf[u] = ld_nc_v4(src + v0 + u * 32);
       for (int k = 0; k < K; ++k) {
-        int4* dst = reinterpret_cast<int4*>(reinterpret_cast<__nv_bfloat16*>(xperm) + (size_t)rows[k] * d);
+        int4* dst = static_cast<int4*>(dsts[k]);
+        if (!dst) continue;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (v0 + u * 32 < nvec) st_na_v4(dst + v0 + u * 32, buf[u]);
       }
     }
+    if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
   } else {
     for (int v = lane; v < nvec; v += 32) {
       const int4 raw = ld_nc_v4(src + v);
@@ -631,7 +647,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
       }
     }
   }
-  if (!fin) atomicExch(finite_flag, 1);
+  if (!fin) atomicOr(finite_flag, 1);
 }
 
 template <typename OutT>

@@ -307,6 +307,10 @@ class MoELayer:
         buf = (C.c_uint8 * 128).from_buffer_copy(uid)
         self._check(self.L.cl_moe_ep_init(self.h, buf), "ep_init")
 
+    def ep_peer_init(self):
+        """Collective: switch to the NVLink peer-memory transport (cl_moe_ep_peer_init)."""
+        self._check(self.L.cl_moe_ep_peer_init(self.h), "ep_peer_init")
+
     def ep_forward(self, hidden: torch.Tensor) -> torch.Tensor:
         hidden = self._bf16(hidden)
         out = torch.empty_like(hidden)
@@ -373,3 +377,34 @@ def ep_layout(counts: np.ndarray, rank: int):
     if rc != _lib.CL_OK:
         raise MoEConfigError("ep_layout: bad arguments")
     return loc, piece.reshape(nl, r), tot.value
+
+
+def ep_peer_layout(counts: np.ndarray, rank: int):
+    """Peer-transport layout of `rank` (pure host): (dispatch_row [N], return_row [N/R x R],
+    local_offsets [N/R+1]); see cl_moe_ep_peer_layout."""
+    counts = np.ascontiguousarray(counts, np.int64)
+    r, n = counts.shape
+    nl = n // r
+    disp = np.empty(n, np.int64)
+    ret = np.empty(nl * r, np.int64)
+    loc = np.empty(nl + 1, np.int64)
+    rc = _lib.lib().cl_moe_ep_peer_layout(counts.ctypes.data, r, n, rank, disp.ctypes.data, ret.ctypes.data,
+                                          loc.ctypes.data)
+    if rc != _lib.CL_OK:
+        raise MoEConfigError("ep_peer_layout: bad arguments")
+    return disp, ret.reshape(nl, r), loc
+
+
+def ep_group_forward(layers, hidden):
+    """Single-device emulation of an R-rank expert-parallel group over the peer transport:
+    layers[r] holds rank r's experts (ep_size = R, ep_rank = r); hidden[r] is rank r's batch."""
+    R = len(layers)
+    hidden = [lay._bf16(x) for lay, x in zip(layers, hidden)]
+    outs = [torch.empty_like(x) for x in hidden]
+    hs = (C.c_void_p * R)(*[lay.h.value for lay in layers])
+    xs = (C.c_void_p * R)(*[x.data_ptr() for x in hidden])
+    os_ = (C.c_void_p * R)(*[o.data_ptr() for o in outs])
+    ts = (C.c_int64 * R)(*[x.shape[0] for x in hidden])
+    _lib.check(_lib.lib().cl_moe_ep_group_forward(hs, R, xs, ts, os_, _stream(layers[0].device)), layers[0].h,
+               "ep_group_forward")
+    return outs

@@ -264,3 +264,111 @@ def test_ep_gloo_backward_matches_single_process_oracle(tmp_path, world, n, k):
             if cnt:
                 assert np.array_equal(p_["dwi"][e], rdwi[i * nl + e]), (i, e)
                 assert np.array_equal(p_["dwo"][e], rdwo[i * nl + e]), (i, e)
+
+
+# ---- peer-memory (NVLink) transport: layout consistency and a gloo restatement of the one-sided
+# stores (cl_moe_ep_peer_layout / ep_peer_layout_kernel, csrc/ep.cuh) ----
+
+def test_peer_layout_agrees_across_ranks():
+    """Every source's independently computed dispatch row equals the owner's receive-piece start;
+    every owner's return row equals the piece start in the source's permutation."""
+    from paper_2509_09121_b200.moe import ep_peer_layout
+    rng = np.random.default_rng(3)
+    for world, n in ((1, 8), (2, 8), (4, 16), (8, 16), (8, 64)):
+        nl = n // world
+        counts = rng.integers(0, 40, (world, n))
+        counts[rng.random((world, n)) < 0.2] = 0  # empty pieces
+        recv = [ep_layout(counts, o) for o in range(world)]
+        peer = [ep_peer_layout(counts, r) for r in range(world)]
+        for s in range(world):
+            disp, _, _ = peer[s]
+            src_off = np.concatenate([[0], np.cumsum(counts[s])])
+            for g in range(n):
+                o, e = divmod(g, nl)
+                assert disp[g] == recv[o][1][e, s]
+        for o in range(world):
+            _, ret, loc = peer[o]
+            assert np.array_equal(loc, recv[o][0])
+            for e in range(nl):
+                for s in range(world):
+                    assert ret[e, s] == np.cumsum(np.concatenate([[0], counts[s]]))[o * nl + e]
+
+
+def _ep_peer_worker(rank, world, port, t, d, n, k, f, result_dir):
+    """One-sided stores restated over gloo: each writer computes the destination rows itself
+    (from ep_peer_layout) and ships (rows, data); the target only scatters. A layout mismatch
+    would overwrite or leave holes, caught by the hole check and the bit-exact comparison."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle, make_inputs
+    from paper_2509_09121_b200.moe import ep_peer_layout
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    nl = n // world
+    xs = full["x"][rank * t:(rank + 1) * t]
+    r = o.route(xs, full["w_router"], k)
+    idx, w = r["topk_idx"], r["combine_weights"]
+    offsets, perm, inv = o.plan(idx, n)
+    counts = np.diff(offsets).astype(np.int64)
+    allc = [torch.zeros(n, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, torch.from_numpy(counts))
+    cmat = torch.stack(allc).numpy()
+    disp, ret, loc = ep_peer_layout(cmat, rank)
+
+    def one_sided(stores, rows):
+        """stores[dst] = (row indices, data); returns this rank's buffer after everyone's stores."""
+        sent = [None] * world
+        dist.all_gather_object(sent, stores)
+        buf = np.full((rows, d), np.nan, np.float32)
+        for s in range(world):
+            ridx, data = sent[s][rank]
+            assert np.isnan(buf[ridx]).all(), "two writers hit the same row"
+            buf[ridx] = data
+        return buf
+
+    # dispatch: row r of expert g (rank-in-expert r - offsets[g]) -> owner row disp[g] + that rank
+    stores = [([], []) for _ in range(world)]
+    for g in range(n):
+        for j in range(offsets[g], offsets[g + 1]):
+            stores[g // nl][0].append(disp[g] + j - offsets[g])
+            stores[g // nl][1].append(xs[perm[j] // k])
+    stores = [(np.array(a, np.int64), np.array(b, np.float32).reshape(-1, d)) for a, b in stores]
+    recv = one_sided(stores, loc[-1])
+    assert not np.isnan(recv).any(), "receive buffer has holes"
+    # experts, then the GEMM2-epilogue stores: received row loc-piece (e, s) + j -> s's row ret[e, s] + j
+    yrecv = np.zeros_like(recv)
+    for e in range(nl):
+        a, b = loc[e], loc[e + 1]
+        if b > a:
+            _, yrecv[a:b] = o.expert_ffn(recv[a:b], full["w_in"][rank * nl + e], full["w_out"][rank * nl + e])
+    stores = [([], []) for _ in range(world)]
+    row = 0
+    for e in range(nl):
+        for s in range(world):
+            cnt = cmat[s, rank * nl + e]
+            stores[s][0].extend(range(ret[e, s], ret[e, s] + cnt))
+            stores[s][1].extend(yrecv[row:row + cnt])
+            row += cnt
+    stores = [(np.array(a, np.int64), np.array(b, np.float32).reshape(-1, d)) for a, b in stores]
+    y = one_sided(stores, t * k)
+    assert not np.isnan(y).any(), "return buffer has holes"
+    out = np.zeros((t, d), np.float32)
+    order = np.argsort(idx, axis=1, kind="stable")
+    for j in range(t):
+        for kk in order[j]:
+            out[j] = out[j] + (y[inv[j * k + kk]] * w[j, kk]).astype(np.float32)
+    np.save(os.path.join(result_dir, f"out{rank}.npy"), out)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,k", [(2, 8, 2), (4, 16, 4)])
+def test_ep_peer_transport_gloo_matches_single_process_oracle(tmp_path, world, n, k):
+    t, d, f = 40, 64, 32
+    mp.spawn(_ep_peer_worker, args=(world, _free_port(), t, d, n, k, f, str(tmp_path)), nprocs=world, join=True)
+    from oracle.oracle import Oracle, make_inputs
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    r = o.route(full["x"], full["w_router"], k)
+    ref = o.moe_forward(full["x"], full["w_in"], full["w_out"], r["topk_idx"], r["combine_weights"])
+    got = np.concatenate([np.load(tmp_path / f"out{i}.npy") for i in range(world)])
+    assert np.array_equal(got, ref)

@@ -1,0 +1,106 @@
+"""Peer-memory (NVLink) expert-parallel transport on one GPU.
+
+* R-rank groups emulated in one process (cl_moe_ep_group_forward): the production layout,
+  dispatch (stores into the owners' receive buffers) and GEMM2 epilogue (stores into the sources'
+  return buffers) kernels, with the other handles' buffers as peer addresses, phase by phase so no
+  kernel waits on another. Output must be bit-identical to the single-GPU layer on each rank's
+  batch (a row's GEMM result does not depend on which rows share its tile).
+* ep_size = 1 through cl_moe_ep_peer_init with a real 1-rank communicator (NCCL counts
+  all-gather and barriers, self "peer" = local buffers)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+from oracle.oracle import Oracle, make_inputs  # noqa: E402
+
+JOBS = os.cpu_count() or 1
+
+
+def _dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16).contiguous()
+
+
+@pytest.mark.parametrize("R,n,k,ts,gemm_ctas", [(2, 8, 2, (300, 517), 1), (2, 8, 2, (1024, 900), 2),
+                                                 (4, 16, 4, (300, 1, 517, 64), 1), (4, 16, 2, (640, 640, 3, 700), 2),
+                                                 (8, 16, 2, (128,) * 8, 1)])
+def test_group_forward_bit_identical_to_single_gpu(R, n, k, ts, gemm_ctas):
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer, ep_group_forward
+    d, f = 512, 256
+    T = sum(ts)
+    inp = make_inputs(T, d, n, f)
+    nl = n // R
+    cap = max(ts)
+    full = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=cap, gemm_ctas=gemm_ctas),
+                    inp["w_router"], inp["w_in"], inp["w_out"])
+    ranks = [MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=cap, gemm_ctas=gemm_ctas,
+                                ep_size=R, ep_rank=r),
+                      inp["w_router"], inp["w_in"][r * nl:(r + 1) * nl], inp["w_out"][r * nl:(r + 1) * nl])
+             for r in range(R)]
+    xs, a = [], 0
+    for t in ts:
+        xs.append(_dev(inp["x"][a:a + t]))
+        a += t
+    outs = ep_group_forward(ranks, xs)
+    for r in range(R):
+        ranks[r].sync()
+        assert torch.equal(outs[r], full.forward(xs[r])), f"rank {r}"
+    # twice: buffers are reused across forwards
+    outs2 = ep_group_forward(ranks, xs)
+    assert all(torch.equal(a_, b_) for a_, b_ in zip(outs, outs2))
+    if R == 2:
+        o = Oracle("port")
+        rr = o.route(inp["x"][:ts[0]], inp["w_router"], k)
+        ref = o.moe_forward(inp["x"][:ts[0]], inp["w_in"], inp["w_out"], rr["topk_idx"], rr["combine_weights"],
+                            jobs=JOBS)
+        dl = outs[0].float().cpu().numpy().astype(np.float64) - ref
+        assert np.linalg.norm(dl) / np.linalg.norm(ref) <= 1e-2
+
+
+def test_group_forward_skewed_routing():
+    """One expert (owned by rank 0) receives most rows from every rank."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer, ep_group_forward
+    R, n, k, d, f, t = 4, 16, 2, 256, 256, 400
+    inp = make_inputs(R * t, d, n, f, skew=2.0)
+    nl = n // R
+    full = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                    inp["w_router"], inp["w_in"], inp["w_out"])
+    ranks = [MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t, ep_size=R, ep_rank=r),
+                      inp["w_router"], inp["w_in"][r * nl:(r + 1) * nl], inp["w_out"][r * nl:(r + 1) * nl])
+             for r in range(R)]
+    xs = [_dev(inp["x"][r * t:(r + 1) * t]) for r in range(R)]
+    outs = ep_group_forward(ranks, xs)
+    for r in range(R):
+        assert torch.equal(outs[r], full.forward(xs[r]))
+
+
+def test_group_forward_rejects_mismatched_group():
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer, MoEConfigError, ep_group_forward
+    d, n, f = 256, 8, 256
+    inp = make_inputs(8, d, n, f)
+    a = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=2, d_ff=f, max_tokens=8, ep_size=2, ep_rank=0),
+                 inp["w_router"], inp["w_in"][:4], inp["w_out"][:4])
+    b = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=2, d_ff=f, max_tokens=8, ep_size=2, ep_rank=0),
+                 inp["w_router"], inp["w_in"][:4], inp["w_out"][:4])
+    with pytest.raises(MoEConfigError):
+        ep_group_forward([a, b], [_dev(inp["x"]), _dev(inp["x"])])
+
+
+def test_peer_transport_single_rank_nccl():
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 700, 512, 8, 2, 256
+    inp = make_inputs(t, d, n, f)
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    ref = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    lay.ep_init(MoELayer.ep_unique_id())
+    lay.ep_peer_init()
+    x = _dev(inp["x"])
+    for _ in range(2):
+        out = lay.ep_forward(x)
+        lay.sync()
+        assert torch.equal(out, ref.forward(x))
