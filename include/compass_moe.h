@@ -201,6 +201,11 @@ cl_status cl_moe_compute_smoothing(cl_moe* h, float alpha, float* s_out);
 cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s);
 cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
 /* Host copies of the FP8 scales in use: [N_local], [N_local], [N_local x 2f], [N_local x d]. */
+/* collect_calibration statistics accumulated by cl_moe_calibrate since the last reset (any
+ * pointer may be NULL): counts[N] routing counts (sum = tokens x K), x_max[N_local] / mid_max
+ * [N_local] per-expert max |GEMM1 input| / |SwiGLU output|, ch_max[d] per-channel max |hidden|.
+ * An empty calibration set (T = 0) leaves them unchanged (zero after a reset). */
+cl_status cl_moe_calibration_stats(cl_moe* h, int64_t* counts, float* x_max, float* mid_max, float* ch_max);
 cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,
                                 float* w_out_scale);
 

@@ -119,6 +119,7 @@ struct cl_moe {
   float* sx_mid = nullptr;             // [n_local]
   float* calib = nullptr;              // [2][n_local] running maxima
   float* calib_ch = nullptr;           // [d] per-channel max |hidden| over calibration tokens
+  long long* calib_counts = nullptr;   // [N] routing counts over calibration tokens
   float* smooth = nullptr;             // [d] scratch for fold_smoothing
   bool fp8_ready = false;
 
@@ -206,7 +207,7 @@ struct cl_moe {
   bool maps_q = false;
 
   ~cl_moe() {
-    void* ptrs[] = {calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
+    void* ptrs[] = {calib_counts, calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
                     sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
                     inv,    row_w,   slot[0].x, slot[0].xf, slot[0].out, slot[1].x, slot[1].xf, slot[1].out,
                     io_out, rb.logits,    rb.probs,
@@ -376,6 +377,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
   h->calib_ch = dalloc<float>(h->d);
   CK(cudaMemset(h->calib_ch, 0, sizeof(float) * h->d));
+  h->calib_counts = dalloc<long long>(h->N);
+  CK(cudaMemset(h->calib_counts, 0, sizeof(long long) * h->N));
   h->smooth = dalloc<float>(h->d);
 
   using namespace cmoe;
@@ -1618,13 +1621,16 @@ cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls) {
 
 cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream) {
   return guarded(h, [&] {
-    if (!hidden) throw ConfigErr("hidden is null");
+    if (!hidden && T != 0) throw ConfigErr("hidden is null");
     CK(cudaSetDevice(h->cfg.device));
     cudaStream_t st = (cudaStream_t)stream;
     if (reset) {
       CK(cudaMemsetAsync(h->calib, 0, sizeof(float) * 2 * h->n_local, st));
       CK(cudaMemsetAsync(h->calib_ch, 0, sizeof(float) * h->d, st));
+      CK(cudaMemsetAsync(h->calib_counts, 0, sizeof(long long) * h->N, st));
     }
+    if (T == 0) return;  // empty calibration set: statistics unchanged
+    if (T < 0) throw ConfigErr("T must be >= 0");
     col_absmax_kernel<<<dim3((unsigned)((h->d + 255) / 256), (unsigned)((T + 255) / 256)), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(hidden), T, (int)h->d, 256, h->calib_ch);
     const int saved = h->precision;
@@ -1633,12 +1639,24 @@ cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t res
     if (!h->io_out) h->io_out = dalloc<__nv_bfloat16>(h->cap * h->d);
     run_experts(h, hidden, T, h->io_out, false, st);
     h->precision = saved;
+    add_counts_kernel<<<1, 128, 0, st>>>(h->rb.counts, (int)h->N, h->calib_counts);
     const int64_t rows = T * h->K;
     segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)h->d,
                                                                  h->rb.offsets, h->n_local, h->calib);
     segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)h->f,
                                                                  h->rb.offsets, h->n_local, h->calib + h->n_local);
     CK(cudaGetLastError());
+  });
+}
+
+cl_status cl_moe_calibration_stats(cl_moe* h, int64_t* counts, float* x_max, float* mid_max, float* ch_max) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaDeviceSynchronize());
+    if (counts) CK(cudaMemcpy(counts, h->calib_counts, sizeof(int64_t) * h->N, cudaMemcpyDeviceToHost));
+    if (x_max) CK(cudaMemcpy(x_max, h->calib, sizeof(float) * h->n_local, cudaMemcpyDeviceToHost));
+    if (mid_max) CK(cudaMemcpy(mid_max, h->calib + h->n_local, sizeof(float) * h->n_local, cudaMemcpyDeviceToHost));
+    if (ch_max) CK(cudaMemcpy(ch_max, h->calib_ch, sizeof(float) * h->d, cudaMemcpyDeviceToHost));
   });
 }
 

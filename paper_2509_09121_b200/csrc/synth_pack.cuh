@@ -126,6 +126,11 @@ __global__ void segment_absmax_kernel(const __nv_bfloat16* __restrict__ m, int c
 
 // Per-column max |value| of a row-major bf16 matrix [rows][cols] into out[cols] (atomicMax on the
 // bit patterns of non-negative floats). Grid (cols/256, row chunks).
+// Calibration routing counts: acc[e] += counts[e] (collect_calibration).
+__global__ void add_counts_kernel(const int32_t* __restrict__ counts, int n, long long* __restrict__ acc) {
+  for (int e = threadIdx.x; e < n; e += blockDim.x) acc[e] += counts[e];
+}
+
 __global__ void col_absmax_kernel(const __nv_bfloat16* __restrict__ m, int64_t rows, int cols, int rows_per_block,
                                   float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;

@@ -203,6 +203,15 @@ class MoELayer:
             rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
         self._check(rc, "quantize_fp8")
 
+    def calibration_stats(self):
+        """collect_calibration statistics: dict(counts [N], x_max [N_local], mid_max [N_local], ch_max [d])."""
+        nl = self.cfg.n_experts // self.cfg.ep_size
+        out = dict(counts=np.zeros(self.cfg.n_experts, np.int64), x_max=np.zeros(nl, np.float32),
+                   mid_max=np.zeros(nl, np.float32), ch_max=np.zeros(self.cfg.d_model, np.float32))
+        self._check(self.L.cl_moe_calibration_stats(self.h, *(v.ctypes.data for v in out.values())),
+                    "calibration_stats")
+        return out
+
     def save_checkpoint(self, path: str, prefix: str = "") -> None:
         self._check(self.L.cl_moe_save_checkpoint(self.h, path.encode(), prefix.encode()), "save_checkpoint")
 

@@ -134,3 +134,23 @@ def test_checkpoint_expert_shard(oracle_ref, tmp_path):
                                                         for w in ("w_in", "w_out")])
     for e in range(4, 8):
         assert np.array_equal(got[f"{PREFIX}experts.{e}.w_in"], inp["w_in"][e])
+
+
+def test_collect_calibration_counts(oracle_port):
+    """SPEC.md:532-536 collect_calibration: counts sum = B*K, equal to the oracle's routing counts
+    accumulated over batches (skewed router included); an empty token set gives zero counts."""
+    n, k, d = 16, 4, 256
+    inp = make_inputs(900, d, n, 256, skew=1.8)
+    lay = _layer(inp, k, 512)
+    x = inp["x"]
+    lay.calibrate(_dev(x[:0]), reset=True)
+    st = lay.calibration_stats()
+    assert st["counts"].sum() == 0 and st["x_max"].max() == 0
+    lay.calibrate(_dev(x[:500]), reset=True)
+    lay.calibrate(_dev(x[500:]), reset=False)
+    st = lay.calibration_stats()
+    ref = oracle_port.route(x, inp["w_router"], k)["counts"]
+    assert st["counts"].sum() == 900 * k
+    assert np.array_equal(st["counts"], ref)
+    assert np.array_equal(st["ch_max"], np.abs(x).max(0))
+    assert ref[0] / ref.sum() > 2.0 / n  # the injected skew is visible in the statistics
