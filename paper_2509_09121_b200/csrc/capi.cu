@@ -506,6 +506,7 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g2.ldo = static_cast<int>(h->d);
   g2.row_scale = row_w;
   g2.row_ptr = row_ptr;
+  g1.half_tail = g2.half_tail = 1;  // 2-CTA: tail m-tiles of <= 128 rows as M=128 pair MMAs
   g2.act_scale = h->sx_mid;
   g2.w_scale = h->ws_out;
   const int v = h->gemm_ctas == 2 ? 1 : 0;

@@ -55,6 +55,8 @@ struct GemmArgs {
   int64_t rp;               // row stride of aux_t (padded-row capacity)
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
   void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
+  int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
+                            // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
 };
 
 constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
@@ -73,8 +75,12 @@ struct GemmCfg {
   static constexpr int kStageB = kBRowsPerCta * kBKBytes;
   static constexpr int kStageBytes = kStageA + kStageB;
   static constexpr int kStages = kCtaGroup == 1 ? 4 : 6;
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ +
-                               (kMaxExperts + 1) * 4;
+  // half tiles (2-CTA): gate/up exchange between TMEM lane halves, [64 rows][129 fp32] (padded)
+  static constexpr int kXStride = 129;
+  static constexpr int kXBytes = kCtaGroup == 2 ? 64 * kXStride * 4 : 0;
+  static constexpr int kSmemCtl = 1024 /*align*/ + 256 /*barriers*/ + (kMaxExperts + 1) * 4;
+  static constexpr int kSmem = kStages * kStageBytes + kSmemCtl + kXBytes;
+  static_assert(kSmem <= 232448, "shared memory budget");
 };
 
 struct TileInfo {
@@ -83,6 +89,7 @@ struct TileInfo {
   int b_row;     // first B row of the tile
   int row_end;   // row-grouped: end of the expert segment (epilogue mask)
   int kb0, nkb;  // k-block range
+  bool half;     // 2-CTA tail tile run as M=128 (64 rows per CTA)
 };
 
 // Row-grouped decode: tiles of expert e = mtiles(e) x n_tiles_n, m fastest.
@@ -100,6 +107,7 @@ __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, cons
   ti.row_end = a.offsets[e + 1];
   ti.kb0 = 0;
   ti.nkb = a.num_kb;
+  ti.half = a.half_tail && ti.row_end - ti.a_row <= bm / 2;
   return true;
 }
 
@@ -118,6 +126,7 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, i
   ti.row_end = 1 << 30;
   ti.kb0 = a.kb_off[e];
   ti.nkb = a.kb_off[e + 1] - a.kb_off[e];
+  ti.half = false;
   return true;
 }
 
@@ -162,6 +171,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kUmmaKBytes = 32;                    // 16 bf16 or 32 e4m3 per MMA
   constexpr int kMmaPerKb = kBKBytes / kUmmaKBytes;  // 4
   constexpr uint32_t kIdesc = idesc_f32acc<kFp8>(Cfg::kBM, kBN);
+  constexpr uint32_t kIdescHalf = idesc_f32acc<kFp8>(128, kBN);  // 2-CTA tail tiles
   constexpr int kElemBytes = kFp8 ? 1 : 2;
   constexpr int kBKElems = kBKBytes / kElemBytes;
   // Row-grouped: the A rows of an expert are re-read for every n-block -> keep them in L2.
@@ -180,6 +190,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   int* tile_ring = reinterpret_cast<int*>(tfree + kTileSlots);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
   int* mt_prefix = reinterpret_cast<int*>(smem + S * Cfg::kStageBytes + 256);
+  float* xbuf = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + Cfg::kSmemCtl - 1024);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -267,7 +278,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           free_tile(i);
         }
         if (tile >= total_tiles || !decode(tile, ti)) break;
-        const int a_row = ti.a_row + cta_rank * Cfg::kRowsPerCta;
+        const bool half_t = kCtaGroup == 2 && ti.half;
+        const int a_row = ti.a_row + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -300,6 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
+        const uint32_t idesc = (kCtaGroup == 2 && ti.half) ? kIdescHalf : kIdesc;
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kMmaPerKb; ++k) {
             const uint64_t koff = static_cast<uint64_t>((k * kUmmaKBytes) >> 4);
-            mma_ss<kCtaGroup, kFp8>(d_tmem, adesc + koff, bdesc + koff, kIdesc, (kb | k) != 0);
+            mma_ss<kCtaGroup, kFp8>(d_tmem, adesc + koff, bdesc + koff, idesc, (kb | k) != 0);
           }
           mma_commit<kCtaGroup>(&empty[s]);
           if (++s == S) { s = 0; ph ^= 1; }
@@ -351,73 +364,126 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           wsu = wsg + kBN / 2;
         }
         if constexpr (kOutFp8) so = 1.0f / args.out_scale[ti.e];  // act / s_mid as a multiply
-#pragma unroll 1
-        for (int c = half * (kBN / 64 / 2); c < (half + 1) * (kBN / 64 / 2); ++c) {
-          uint32_t g[32], u[32];
-          tmem_ld32(t_row + c * 32, g);
-          tmem_ld32(t_row + kBN / 2 + c * 32, u);
-          tmem_ld_wait();
-          float v[32], gv[32], uv[32];
+        // stores of one 32-channel chunk of one row: A_act (bf16 / e4m3), training H and A^T
+        auto emit = [&](int row, int64_t prow, int col, const float* v, const float* gv, const float* uv) {
+          if constexpr (kOutFp8) {
+            uint32_t p[8];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            gv[i] = __uint_as_float(g[i]) * sg;
-            uv[i] = __uint_as_float(u[i]) * su;
-            if constexpr (kFp8) {
-              gv[i] *= wsg[c * 32 + i];
-              uv[i] *= wsu[c * 32 + i];
+            for (int i = 0; i < 8; ++i) {
+              const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                  make_float2(v[4 * i] * so, v[4 * i + 1] * so), __NV_SATFINITE, __NV_E4M3);
+              const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                  make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
+              p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
             }
-            v[i] = silu_f(gv[i]) * uv[i];
+            uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;
+            st_global_v4(dst, p[0], p[1], p[2], p[3]);
+            st_global_v4(dst + 16, p[4], p[5], p[6], p[7]);
+          } else {
+            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
+            if (args.aux) {  // training: keep H = [G | U] for the SwiGLU backward
+              __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
+              store_bf16x32(hrow + col, gv);
+              store_bf16x32(hrow + args.ffn + col, uv);
+            }
+            if (args.aux_t)  // training: A^T (padded K-major) for the dW_out gradient GEMM
+              store_t_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)col * args.rp + prow, args.rp, v);
           }
-          if (valid) {
-            const int col = ti.nt * (kBN / 2) + c * 32;
-            if constexpr (kOutFp8) {
-              uint32_t p[8];
+        };
+        if (kCtaGroup == 2 && ti.half) {
+          // M=128 pair tile: TMEM lane r (< 64) holds gate channels of row r, lane 64 + r the up
+          // channels of the same row (same columns). Up-lane warps pass their (scaled) values
+          // through shared memory; gate-lane warps finish the SwiGLU and store.
+          const int r64 = row_in_cta & 63;
+          const int hrow = ti.a_row + cta_rank * 64 + r64;
+          const bool hvalid = hrow < ti.row_end;
+          const int64_t hprow = args.aux_t ? (int64_t)args.poff[ti.e] + (hrow - args.offsets[ti.e]) : 0;
+          if (q >= 2) {
+#pragma unroll 1
+            for (int c = half * 2; c < half * 2 + 2; ++c) {
+              uint32_t u[32];
+              tmem_ld32(t_row + c * 32, u);
+              tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-                    make_float2(v[4 * i] * so, v[4 * i + 1] * so), __NV_SATFINITE, __NV_E4M3);
-                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-                    make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
-                p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+              for (int i = 0; i < 32; ++i) {
+                float uv = __uint_as_float(u[i]) * su;
+                if constexpr (kFp8) uv *= wsu[c * 32 + i];
+                xbuf[r64 * Cfg::kXStride + c * 32 + i] = uv;
               }
-              uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;
-              st_global_v4(dst, p[0], p[1], p[2], p[3]);
-              st_global_v4(dst + 16, p[4], p[5], p[6], p[7]);
-            } else {
-              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
-              if (args.aux) {  // training: keep H = [G | U] for the SwiGLU backward
-                __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
-                store_bf16x32(hrow + col, gv);
-                store_bf16x32(hrow + args.ffn + col, uv);
-              }
-              if (args.aux_t)  // training: A^T (padded K-major) for the dW_out gradient GEMM
-                store_t_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)col * args.rp + prow, args.rp, v);
             }
+          }
+          named_bar_sync(1, kEpiWarps * 32);
+          if (q < 2) {
+#pragma unroll 1
+            for (int c = half * 2; c < half * 2 + 2; ++c) {
+              uint32_t g[32];
+              tmem_ld32(t_row + c * 32, g);
+              tmem_ld_wait();
+              float v[32], gv[32], uv[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                gv[i] = __uint_as_float(g[i]) * sg;
+                if constexpr (kFp8) gv[i] *= wsg[c * 32 + i];
+                uv[i] = xbuf[r64 * Cfg::kXStride + c * 32 + i];
+                v[i] = silu_f(gv[i]) * uv[i];
+              }
+              if (hvalid) emit(hrow, hprow, ti.nt * (kBN / 2) + c * 32, v, gv, uv);
+            }
+          }
+          named_bar_sync(1, kEpiWarps * 32);  // xbuf free for the next half tile
+        } else {
+#pragma unroll 1
+          for (int c = half * (kBN / 64 / 2); c < (half + 1) * (kBN / 64 / 2); ++c) {
+            uint32_t g[32], u[32];
+            tmem_ld32(t_row + c * 32, g);
+            tmem_ld32(t_row + kBN / 2 + c * 32, u);
+            tmem_ld_wait();
+            float v[32], gv[32], uv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              gv[i] = __uint_as_float(g[i]) * sg;
+              uv[i] = __uint_as_float(u[i]) * su;
+              if constexpr (kFp8) {
+                gv[i] *= wsg[c * 32 + i];
+                uv[i] *= wsu[c * 32 + i];
+              }
+              v[i] = silu_f(gv[i]) * uv[i];
+            }
+            if (valid) emit(row, prow, ti.nt * (kBN / 2) + c * 32, v, gv, uv);
           }
         }
       } else if constexpr (kEpi == EPI_ROWSCALE) {
-        float rs = valid ? (args.row_scale ? args.row_scale[row] : 1.0f) : 0.0f;
+        // M=128 pair tile: lane r (< 64) holds columns [0,128) of row r, lane 64 + r columns
+        // [128,256) of the same row, both in TMEM columns [0,128).
+        const bool ht = kCtaGroup == 2 && ti.half;
+        const int erow = ht ? ti.a_row + cta_rank * 64 + (row_in_cta & 63) : row;
+        const bool evalid = erow < ti.row_end;
+        const int col0 = ht ? (q >= 2 ? kBN / 2 : 0) : 0;
+        const int c_lo = ht ? half * 2 : half * (kBN / 64);
+        const int c_hi = ht ? half * 2 + 2 : (half + 1) * (kBN / 64);
+        float rs = evalid ? (args.row_scale ? args.row_scale[erow] : 1.0f) : 0.0f;
         const float* ws = nullptr;
         if constexpr (kFp8) {
           rs *= args.act_scale[ti.e];
-          ws = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN;
+          ws = args.w_scale + (size_t)ti.e * args.b_rows_per_expert + ti.nt * kBN + col0;
         }
 #pragma unroll 1
-        for (int c = half * (kBN / 64); c < (half + 1) * (kBN / 64); ++c) {
+        for (int c = c_lo; c < c_hi; ++c) {
           uint32_t a[32];
           tmem_ld32(t_row + c * 32, a);
           tmem_ld_wait();
-          if (valid) {
+          if (evalid) {
             float v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               v[i] = __uint_as_float(a[i]) * rs;
               if constexpr (kFp8) v[i] *= ws[c * 32 + i];
             }
+            const int col = ti.nt * kBN + col0 + c * 32;
             if (args.row_ptr)  // peer transport: the row returns to its source rank over NVLink
-              store_bf16x32_plain(static_cast<__nv_bfloat16*>(args.row_ptr[row]) + ti.nt * kBN + c * 32, v);
+              store_bf16x32_plain(static_cast<__nv_bfloat16*>(args.row_ptr[erow]) + col, v);
             else
-              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + ti.nt * kBN + c * 32, v);
+              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)erow * args.ldo + col, v);
           }
         }
       } else if constexpr (kEpi == EPI_SWIGLU_BWD) {

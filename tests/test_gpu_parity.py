@@ -315,3 +315,26 @@ def test_device_skew_construction_matches_oracle():
     assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), r["topk_idx"])
     assert dec.counts.cpu().numpy().max() > 0.25 * t * k  # hot expert
     lay.close()
+
+
+@pytest.mark.parametrize("precision", ["bf16", "fp8"])
+def test_pair_tail_tiles_match_single_cta(precision):
+    """2-CTA kernels run an expert's last m-tile with <= 128 rows as an M=128 pair MMA (64 rows per
+    CTA, gate/up exchanged through shared memory in the SwiGLU epilogue). The 1-CTA kernels use
+    plain M=128 tiles; both accumulate every output element in the same K order, so the layer
+    outputs must agree bit for bit. Many experts give tail sizes across 1..255."""
+    t, d, n, k, f = 12000, 256, 64, 4, 256
+    inp = make_inputs(t, d, n, f)
+    x = _x_dev(inp["x"])
+    outs = []
+    for g in (1, 2):
+        lay = _layer(inp, t, k, gemm_ctas=g)
+        if precision == "fp8":
+            lay.calibrate(x)
+            lay.quantize_fp8()
+        outs.append(lay.forward(x))
+        lay.sync()
+    counts = Oracle("port").route(inp["x"], inp["w_router"], k)["counts"]
+    tails = counts % 256
+    assert ((tails > 0) & (tails <= 128)).sum() >= 10 and (tails > 128).sum() >= 5
+    assert torch.equal(outs[0], outs[1])
