@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -396,11 +397,22 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
 }
 
+// m-tiles per L2-resident group for a row-grouped GEMM whose A rows are k_bytes long (decode_tile).
+int m_group_for(int64_t k_bytes, int bm) {
+  static const int64_t budget = [] {
+    const char* e = std::getenv("CL_MOE_L2_GROUP_MB");
+    return (int64_t)(e ? std::atoi(e) : 32) << 20;
+  }();
+  if (budget <= 0) return 0;
+  return static_cast<int>(std::max<int64_t>(1, budget / (k_bytes * bm)));
+}
+
 template <int G, int EPI, bool F8, bool OF8, bool WG = false>
 void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st) {
   if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
   GemmArgs args = args_in;
   args.tile_counter = h->tile_counter;
+  if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
   CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((h->num_sms / G) * G);

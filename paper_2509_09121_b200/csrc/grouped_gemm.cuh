@@ -55,6 +55,7 @@ struct GemmArgs {
   int64_t rp;               // row stride of aux_t (padded-row capacity)
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
   void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
+  int32_t m_group;          // row-grouped tile order: m-tiles per group (0 = all), see decode_tile
   int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
                             // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
 };
@@ -92,16 +93,23 @@ struct TileInfo {
   bool half;     // 2-CTA tail tile run as M=128 (64 rows per CTA)
 };
 
-// Row-grouped decode: tiles of expert e = mtiles(e) x n_tiles_n, m fastest.
+// Row-grouped decode: tiles of expert e = mtiles(e) x n_tiles_n. The expert's m-tiles are taken
+// in groups of m_group; inside a group m is fastest and the group sweeps every n-block before the
+// next group starts. The group's A rows stay resident in L2 while the weight n-blocks stream past
+// (an expert whose rows exceed L2 would otherwise re-stream its rows for every n-block).
 __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, const GemmArgs& a, int bm, TileInfo& ti) {
   if (tile >= mt_prefix[a.n_experts] * a.n_tiles_n) return false;
   int e = 0;
   while (tile >= mt_prefix[e + 1] * a.n_tiles_n) ++e;
   const int local = tile - mt_prefix[e] * a.n_tiles_n;
   const int mtiles = mt_prefix[e + 1] - mt_prefix[e];
+  const int gm = (a.m_group > 0 && a.m_group < mtiles) ? a.m_group : mtiles;
+  const int g = local / (gm * a.n_tiles_n);
+  const int within = local - g * gm * a.n_tiles_n;
+  const int gsz = min(gm, mtiles - g * gm);
   ti.e = e;
-  ti.nt = local / mtiles;
-  ti.mt = local - ti.nt * mtiles;
+  ti.nt = within / gsz;
+  ti.mt = g * gm + (within - ti.nt * gsz);
   ti.a_row = a.offsets[e] + ti.mt * bm;
   ti.b_row = e * a.b_rows_per_expert + ti.nt * kBN;
   ti.row_end = a.offsets[e + 1];
@@ -135,9 +143,12 @@ __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
   const uint64_t pol = l2_policy_evict_first();
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    st_global_v4_hint(dst + 8 * i, pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
-                      pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]), pol);
+  for (int i = 0; i < 2; ++i) {
+    uint32_t p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = pack_bf16(v[16 * i + 2 * j], v[16 * i + 2 * j + 1]);
+    st_global_v8_hint(dst + 16 * i, p, pol);
+  }
 }
 __device__ __forceinline__ void store_bf16x32_plain(__nv_bfloat16* dst, const float* v) {
 #pragma unroll
@@ -376,9 +387,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   make_float2(v[4 * i + 2] * so, v[4 * i + 3] * so), __NV_SATFINITE, __NV_E4M3);
               p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
             }
-            uint8_t* dst = reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col;
-            st_global_v4(dst, p[0], p[1], p[2], p[3]);
-            st_global_v4(dst + 16, p[4], p[5], p[6], p[7]);
+            st_global_v8(reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col, p);
           } else {
             store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
             if (args.aux) {  // training: keep H = [G | U] for the SwiGLU backward
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           float* dst = base + c * 32;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) st_global_v4(dst + 4 * i, a[4 * i], a[4 * i + 1], a[4 * i + 2], a[4 * i + 3]);
+          for (int i = 0; i < 4; ++i) st_global_v8(dst + 8 * i, a + 8 * i);
         }
       }
       tc_fence_before();
