@@ -342,7 +342,7 @@ def run_ours(args, cfg):
     tp = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(f"{T}x{d}x{N}x{K}x{f}")
+            traffic = json.load(fh).get(f"{T}x{d}x{N}x{K}x{f}") if args.precision == "bf16" else None
 
     if rank == 0:
         line = dict(

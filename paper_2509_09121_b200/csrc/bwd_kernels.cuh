@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(256) transpose_pad_kernel(const __nv_bfloat16*
                                                             const int32_t* __restrict__ offsets,
                                                             const int32_t* __restrict__ poff, int n,
                                                             __nv_bfloat16* __restrict__ dst, int64_t rp_cap) {
-  __shared__ __nv_bfloat16 tile[64][66];
+  // 16-byte global accesses both ways; the smem row pitch of 72 bf16 (144 B) keeps the 8-row
+  // column gathers of the store phase on distinct banks.
+  __shared__ __align__(16) __nv_bfloat16 tile[64][72];
   const int c0 = blockIdx.x * 64;
   const int p0 = blockIdx.y * 64;
   if (p0 >= poff[n]) return;
@@ -80,38 +82,37 @@ __global__ void __launch_bounds__(256) transpose_pad_kernel(const __nv_bfloat16*
   const int cnt = offsets[e + 1] - offsets[e];
   const int base_row = offsets[e] + (p0 - poff[e]);
   const int valid_p = min(64, cnt - (p0 - poff[e]));  // may be <= 0 in a pure padding block
-  // load: 64 rows (p) x 64 cols (c); thread handles 2 consecutive columns
-  for (int i = threadIdx.x; i < 64 * 32; i += 256) {
-    const int pr = i / 32, cc = (i % 32) * 2;
-    __nv_bfloat162 v = __floats2bfloat162_rn(0.0f, 0.0f);
-    if (pr < valid_p && c0 + cc < C)
-      v = *reinterpret_cast<const __nv_bfloat162*>(src + (size_t)(base_row + pr) * C + c0 + cc);
-    tile[pr][cc] = v.x;
-    tile[pr][cc + 1] = v.y;
+  // load: 64 rows (p) x 64 cols (c), 8 columns (16 B) per thread and step
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int pr = i >> 3, cc = (i & 7) * 8;
+    int4 v = make_int4(0, 0, 0, 0);
+    if (pr < valid_p) v = ld_nc_v4(src + (size_t)(base_row + pr) * C + c0 + cc);
+    *reinterpret_cast<int4*>(&tile[pr][cc]) = v;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 64 * 32; i += 256) {
-    const int cr = i / 32, pp = (i % 32) * 2;
-    if (c0 + cr < C) {
-      __nv_bfloat162 v;
-      v.x = tile[pp][cr];
-      v.y = tile[pp + 1][cr];
-      *reinterpret_cast<__nv_bfloat162*>(dst + (size_t)(c0 + cr) * rp_cap + p0 + pp) = v;
-    }
+  // store: column c of the tile = 64 consecutive p, 8 of them (16 B) per thread and step
+  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
+    const int cr = i >> 3, pp = (i & 7) * 8;
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = tile[pp + j][cr];
+    *reinterpret_cast<int4*>(dst + (size_t)(c0 + cr) * rp_cap + p0 + pp) = *reinterpret_cast<const int4*>(v);
   }
 }
 
 // Zero the padding columns [poff[e] + cnt_e, poff[e+1]) of a transposed buffer [C][rp] whose data
 // columns are written by a GEMM epilogue. Grid: (C / 256, n_experts), 256 threads.
-__global__ void zero_pad_cols_kernel(__nv_bfloat16* __restrict__ buf, int C, int64_t rp,
-                                     const int32_t* __restrict__ offsets, const int32_t* __restrict__ poff) {
+__global__ void __launch_bounds__(256) zero_pad_cols_kernel(__nv_bfloat16* __restrict__ buf, int C, int64_t rp,
+                                                            const int32_t* __restrict__ offsets,
+                                                            const int32_t* __restrict__ poff) {
+  // one warp per row c: the < 64 padding entries of expert e are contiguous in the row
   const int e = blockIdx.y;
-  const int c = blockIdx.x * 256 + threadIdx.x;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (c >= C) return;
   const int64_t start = poff[e] + (offsets[e + 1] - offsets[e]);
   const int64_t end = poff[e + 1];
   __nv_bfloat16* row = buf + (size_t)c * rp;
-  for (int64_t k = start; k < end; ++k) row[k] = __float2bfloat16_rn(0.0f);
+  for (int64_t k = start + (threadIdx.x & 31); k < end; k += 32) row[k] = __float2bfloat16_rn(0.0f);
 }
 
 // dst[i][j] = src[rowmap(j)][i]: src [rows_src][cols_src] bf16 -> dst [cols_src][rows_src].

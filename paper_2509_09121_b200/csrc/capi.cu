@@ -981,9 +981,9 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
                                                                      es_off, h->poff, NL, h->XT, h->rp_cap);
   transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT,
                                                                      h->rp_cap);
-  zero_pad_cols_kernel<<<dim3((unsigned)((f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
+  zero_pad_cols_kernel<<<dim3((unsigned)((f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
                                                                                         h->poff);
-  zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 255) / 256), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
+  zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
                                                                                             h->rp_cap, es_off, h->poff);
   CK(cudaGetLastError());
   prof_mark(h, 4, st);
