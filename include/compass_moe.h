@@ -178,7 +178,11 @@ cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls);
  * the bf16 layer on `hidden` and accumulates per-expert activation maxima of the GEMM1 input and
  * the SwiGLU output; quantize then sets per-expert activation scales = max/448 and per-(expert,
  * output channel) weight scales = channel absmax/448 and switches the
- * handle's precision. act_scale_* may be given explicitly (host arrays [N_local]) instead. */
+ * handle's precision. act_scale_* may be given explicitly instead: act_scale_in [N] (every
+ * expert's GEMM1-input scale; under expert parallelism the source quantizes each dispatched row
+ * with its owner's scale, so all ranks need the same global table) and act_scale_mid [N_local].
+ * Under expert parallelism, calibration keeps the GEMM1-input maxima per global expert at the
+ * source and quantize all-reduces them (max) over the ranks. */
 cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t reset, void* stream);
 cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float* act_scale_mid);
 /* balance_calibration: with the expert counts of the routed `base` tokens

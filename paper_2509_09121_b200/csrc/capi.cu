@@ -117,6 +117,9 @@ struct cl_moe {
   float* ws_in = nullptr;              // [n_local][2f]
   float* ws_out = nullptr;             // [n_local][d]
   float* sx_in = nullptr;              // [n_local]
+  float* sx_in_all = nullptr;          // [N] GEMM1-input scales of every expert (EP: the source
+                                       //     quantizes a row with its owner's scale)
+  float* calib_all = nullptr;          // [N] EP calibration: source-side max |x| per global expert
   float* sx_mid = nullptr;             // [n_local]
   float* calib = nullptr;              // [2][n_local] running maxima
   float* calib_ch = nullptr;           // [d] per-channel max |hidden| over calibration tokens
@@ -171,6 +174,8 @@ struct cl_moe {
   __nv_bfloat16* dYsrc = nullptr;       // EP training: source-order dY [cap*K][d]
   __nv_bfloat16* dXsrc = nullptr;       // EP training: source-order dX [cap*K][d]
   CUtensorMap mA1e[2], mA2e[2];
+  CUtensorMap mA1eq[2], mA2eq[2];       // e4m3 views of x_recv / act_recv
+  bool maps_eq = false;
   // peer-memory (NVLink) transport (ep.cuh): 0 = NCCL send/recv, 1 = direct peer stores
   int ep_transport = 0;
   char** peer_x_dev = nullptr;          // [R] every rank's x_recv, as mapped in this process
@@ -208,7 +213,7 @@ struct cl_moe {
   bool maps_q = false;
 
   ~cl_moe() {
-    void* ptrs[] = {calib_counts, calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
+    void* ptrs[] = {sx_in_all, calib_all, calib_counts, calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
                     sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
                     inv,    row_w,   slot[0].x, slot[0].xf, slot[0].out, slot[1].x, slot[1].xf, slot[1].out,
                     io_out, rb.logits,    rb.probs,
@@ -373,6 +378,9 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);
+  h->sx_in_all = dalloc<float>(h->N);
+  h->calib_all = dalloc<float>(h->N);
+  CK(cudaMemset(h->calib_all, 0, sizeof(float) * h->N));
   h->sx_mid = dalloc<float>(h->n_local);
   h->calib = dalloc<float>(2 * h->n_local);
   CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
@@ -553,6 +561,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
     run_ep(h, x, T, out, out_f32, st);
     return;
   }
+  if (h->cfg.ep_size > 1) throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_forward)");
   const int N = static_cast<int>(h->N);
   const int tpc = h->tpc_cur;
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
@@ -607,6 +616,15 @@ void ensure_fp8_storage(cl_moe* h) {
   build_maps(h, true);
 }
 
+void ep_fp8_maps(cl_moe* h) {
+  if (h->maps_eq) return;
+  for (int v = 0; v < 2; ++v) {
+    h->mA1eq[v] = make_map(h->x_recv, true, h->d, h->recv_cap, 128);
+    h->mA2eq[v] = make_map(h->act_recv, true, h->f, h->recv_cap, 128);
+  }
+  h->maps_eq = true;
+}
+
 void ep_alloc(cl_moe* h) {
   if (h->x_recv) return;
   const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
@@ -633,12 +651,12 @@ void ep_alloc(cl_moe* h) {
 // One direction of the expert-parallel row exchange (layout of the last EP forward).
 // to_experts: rows of this rank's source permutation `src` (piece g at my_off[g]) go to the
 // owner of expert g, landing at its (local expert, source) slot of `dst`; otherwise the reverse.
-void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStream_t st) {
+void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStream_t st, size_t row_b = 0) {
   NcclApi& nc = NcclApi::get();
   const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
   const int rank = h->cfg.ep_rank;
   const int N = static_cast<int>(h->N), NL = h->n_local;
-  const size_t row_b = static_cast<size_t>(h->d) * 2;
+  if (row_b == 0) row_b = static_cast<size_t>(h->d) * 2;
   const auto& C = h->ep_C;
   const auto& piece = h->ep_piece;
   const auto& my_off = h->ep_myoff;
@@ -681,7 +699,9 @@ void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
 
 void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
   if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
-  if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  if (fp8 && train) throw ConfigErr("training runs in bf16 (set_precision(BF16) first)");
+  if (fp8) ep_fp8_maps(h);
   if (h->ep_transport == 1 && !train) {
     run_ep_peer(h, x, T, out, out_f32, st);
     return;
@@ -692,9 +712,14 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   const int N = static_cast<int>(h->N), NL = h->n_local;
   const int tpc = h->tpc_cur;
   const int blocks = static_cast<int>((T + 7) / 8);
-  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
-                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
-                                                 h->inv, h->row_w, nullptr);
+  if (fp8)  // rows quantized with their owner's GEMM1-input scale (global table)
+    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                  (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
+                                                  h->perm, h->inv, h->row_w, h->sx_in_all);
+  else
+    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
+                                                   h->perm, h->inv, h->row_w, nullptr);
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
   // ---- counts exchange ----
@@ -712,13 +737,13 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   for (int e = 0; e <= NL; ++e) h->ep_off_host[e] = static_cast<int32_t>(loc[e]);
   CK(cudaMemcpyAsync(h->ep_off_dev, h->ep_off_host, sizeof(int32_t) * (NL + 1), cudaMemcpyHostToDevice, st));
   // ---- dispatch exchange: piece (dest r, expert g) -> r's (local expert, source) slot ----
-  ep_exchange(h, h->xperm, h->x_recv, true, st);
+  ep_exchange(h, h->xperm, h->x_recv, true, st, (size_t)h->d * (fp8 ? 1 : 2));
   // ---- local experts ----
   if (train) {
     pad_plan_kernel<<<1, 32, 0, st>>>(h->ep_off_dev, NL, h->poff, h->kb_off);
     CK(cudaGetLastError());
   }
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st,
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1eq, h->mA2eq, st,
             train ? h->Hbuf : nullptr);
   prof_mark(h, 4, st);
   // ---- reverse exchange into this rank's permutation slots ----
@@ -757,8 +782,9 @@ void ep_peer_alloc(cl_moe* h) {
 
 void ep_peer_layout(cl_moe* h, cudaStream_t st) {
   const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+  const int64_t xrb = h->d * (h->precision == CL_MOE_FP8_E4M3 ? 1 : 2);
   ep_peer_layout_kernel<<<h->n_local * R + 1, 256, 0, st>>>(h->ep_counts_dev, R, (int)h->N, h->cfg.ep_rank, h->recv_cap,
-                                                             h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
+                                                             xrb, h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
                                                              h->expert_dst, h->expert_dst_w, h->ep_off_dev, h->row_ptr,
                                                              h->rb.finite_flag);
   CK(cudaGetLastError());
@@ -766,16 +792,23 @@ void ep_peer_layout(cl_moe* h, cudaStream_t st) {
 
 void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int blocks = static_cast<int>((T + 7) / 8);
-  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
-                                                 (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
-                                                 h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
-                                                 h->expert_dst_w);
+  if (h->precision == CL_MOE_FP8_E4M3)
+    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
+                                                  (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
+                                                  h->xperm, h->perm, h->inv, h->row_w, h->sx_in_all, h->expert_dst,
+                                                  h->expert_dst_w);
+  else
+    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
+                                                   (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
+                                                   h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
+                                                   h->expert_dst_w);
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
 }
 
 void ep_peer_experts(cl_moe* h, cudaStream_t st) {
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, h->w_recv, h->mA1e, h->mA2e, h->mA1e, h->mA2e, st, nullptr,
+  if (h->precision == CL_MOE_FP8_E4M3) ep_fp8_maps(h);
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, h->w_recv, h->mA1e, h->mA2e, h->mA1eq, h->mA2eq, st, nullptr,
             h->row_ptr);
   prof_mark(h, 4, st);
 }
@@ -1133,7 +1166,7 @@ cl_status cl_moe_ep_group_forward(cl_moe* const* hs, int32_t R, const void* cons
       if (h->cfg.ep_size != R || h->cfg.ep_rank != r || h->N != N || h->d != h0->d || h->f != h0->f ||
           h->K != h0->K || h->cfg.device != h0->cfg.device)
         throw ConfigErr(fmt("handle %d is not rank %d of a matching %d-rank group", r, r, R));
-      if (h->precision != CL_MOE_BF16) throw ConfigErr("expert-parallel FP8 is not supported yet");
+      if (h->precision != h0->precision) throw ConfigErr("all ranks of a group need the same precision");
       if (!hidden[r] || !out[r]) throw ConfigErr("null argument");
     }
     CK(cudaSetDevice(h0->cfg.device));
@@ -1641,6 +1674,7 @@ cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t res
       CK(cudaMemsetAsync(h->calib, 0, sizeof(float) * 2 * h->n_local, st));
       CK(cudaMemsetAsync(h->calib_ch, 0, sizeof(float) * h->d, st));
       CK(cudaMemsetAsync(h->calib_counts, 0, sizeof(long long) * h->N, st));
+      CK(cudaMemsetAsync(h->calib_all, 0, sizeof(float) * h->N, st));
     }
     if (T == 0) return;  // empty calibration set: statistics unchanged
     if (T < 0) throw ConfigErr("T must be >= 0");
@@ -1654,10 +1688,19 @@ cl_status cl_moe_calibrate(cl_moe* h, const void* hidden, int64_t T, int32_t res
     h->precision = saved;
     add_counts_kernel<<<1, 128, 0, st>>>(h->rb.counts, (int)h->N, h->calib_counts);
     const int64_t rows = T * h->K;
-    segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm), (int)h->d,
-                                                                 h->rb.offsets, h->n_local, h->calib);
-    segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)h->f,
-                                                                 h->rb.offsets, h->n_local, h->calib + h->n_local);
+    if (h->comm) {
+      // expert parallel: GEMM1-input maxima at the source for every global expert (all-reduced
+      // over the ranks by quantize_fp8), SwiGLU-output maxima at the owner (receive layout)
+      route_absmax_kernel<<<(int)((T + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(hidden), (int)T,
+                                                              (int)h->d, (int)h->K, h->rb.topk_idx, h->calib_all);
+      segment_absmax_kernel<<<(int)((h->recv_cap + 7) / 8), 256, 0, st>>>(h->act_recv, (int)h->f, h->ep_off_dev,
+                                                                           h->n_local, h->calib + h->n_local);
+    } else {
+      segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->xperm),
+                                                                   (int)h->d, h->rb.offsets, h->n_local, h->calib);
+      segment_absmax_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(h->act), (int)h->f,
+                                                                   h->rb.offsets, h->n_local, h->calib + h->n_local);
+    }
     CK(cudaGetLastError());
   });
 }
@@ -1731,26 +1774,43 @@ cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float*
   return guarded(h, [&] {
     CK(cudaSetDevice(h->cfg.device));
     ensure_fp8_storage(h);
-    std::vector<float> sin(h->n_local), smid(h->n_local);
+    const int N = static_cast<int>(h->N), NL = h->n_local;
+    const bool ep = h->cfg.ep_size > 1;
+    std::vector<float> sin_all(N), smid(NL);
     if (act_scale_in && act_scale_mid) {
-      std::copy(act_scale_in, act_scale_in + h->n_local, sin.begin());
-      std::copy(act_scale_mid, act_scale_mid + h->n_local, smid.begin());
+      std::copy(act_scale_in, act_scale_in + N, sin_all.begin());  // [N]: every expert's (EP: global table)
+      std::copy(act_scale_mid, act_scale_mid + NL, smid.begin());
     } else {
-      std::vector<float> c(2 * h->n_local);
+      std::vector<float> c(2 * NL), call(N);
       CK(cudaDeviceSynchronize());
-      CK(cudaMemcpy(c.data(), h->calib, sizeof(float) * 2 * h->n_local, cudaMemcpyDeviceToHost));
-      for (int e = 0; e < h->n_local; ++e) {
-        if (!(c[e] > 0.0f) || !(c[h->n_local + e] > 0.0f))
-          throw RunErr(fmt("quantize_model: missing calibration for expert %d", h->e0 + e));
-        sin[e] = c[e] / 448.0f;
-        smid[e] = c[h->n_local + e] / 448.0f;
+      CK(cudaMemcpy(c.data(), h->calib, sizeof(float) * 2 * NL, cudaMemcpyDeviceToHost));
+      if (ep && !h->comm) throw ConfigErr("expert-parallel calibration needs cl_moe_ep_init (or explicit scales)");
+      if (h->comm) {  // calibrated through the EP path: source-side maxima of every global expert
+        cudaStream_t st = nullptr;
+        NCK(NcclApi::get().AllReduce(h->calib_all, h->calib_all, (size_t)N, NcclApi::kFloat32, NcclApi::kMax, h->comm,
+                                     st));
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMemcpy(call.data(), h->calib_all, sizeof(float) * N, cudaMemcpyDeviceToHost));
+      } else {
+        std::copy(c.begin(), c.begin() + NL, call.begin());
+      }
+      for (int g = 0; g < N; ++g) {
+        if (!(call[g] > 0.0f)) throw RunErr(fmt("quantize_model: missing calibration for expert %d", g));
+        sin_all[g] = call[g] / 448.0f;
+      }
+      for (int e = 0; e < NL; ++e) {
+        if (!(c[NL + e] > 0.0f)) throw RunErr(fmt("quantize_model: missing calibration for expert %d", h->e0 + e));
+        smid[e] = c[NL + e] / 448.0f;
       }
     }
-    for (int e = 0; e < h->n_local; ++e)
-      if (!(sin[e] > 0.0f) || !(smid[e] > 0.0f)) throw ConfigErr("activation scales must be > 0");
-    CK(cudaMemcpy(h->sx_in, sin.data(), sizeof(float) * h->n_local, cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->sx_mid, smid.data(), sizeof(float) * h->n_local, cudaMemcpyHostToDevice));
-    const int64_t r1 = (int64_t)h->n_local * 2 * h->f, r2 = (int64_t)h->n_local * h->d;
+    for (int g = 0; g < N; ++g)
+      if (!(sin_all[g] > 0.0f)) throw ConfigErr("activation scales must be > 0");
+    for (int e = 0; e < NL; ++e)
+      if (!(smid[e] > 0.0f)) throw ConfigErr("activation scales must be > 0");
+    CK(cudaMemcpy(h->sx_in_all, sin_all.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sx_in, sin_all.data() + h->e0, sizeof(float) * NL, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sx_mid, smid.data(), sizeof(float) * NL, cudaMemcpyHostToDevice));
+    const int64_t r1 = (int64_t)NL * 2 * h->f, r2 = (int64_t)NL * h->d;
     quantize_rows_e4m3_kernel<<<(int)((r1 + 7) / 8), 256>>>(h->win, r1, (int)h->d, h->win8, h->ws_in);
     quantize_rows_e4m3_kernel<<<(int)((r2 + 7) / 8), 256>>>(h->wout, r2, (int)h->f, h->wout8, h->ws_out);
     CK(cudaGetLastError());

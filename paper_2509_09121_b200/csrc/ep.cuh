@@ -28,7 +28,7 @@ struct NcclApi {
     char internal[128];
   };
   enum DataType { kUint8 = 1, kInt32 = 2, kFloat32 = 7 };
-  enum RedOp { kSum = 0 };
+  enum RedOp { kSum = 0, kMax = 2 };
   int (*GetUniqueId)(UniqueId*) = nullptr;
   int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
   int (*CommDestroy)(Comm) = nullptr;
@@ -120,7 +120,8 @@ __host__ __device__ inline int64_t ep_src_row(const CT* C, int N, int s, int g) 
 }
 
 #ifdef __CUDACC__
-// Device layout for `rank` from the all-gathered counts C (R x N int32):
+// Device layout for `rank` from the all-gathered counts C (R x N int32); x rows are x_row_bytes
+// long (bf16 or e4m3), returned rows row_bytes (bf16):
 //   expert_dst[g]   address of this rank's first row for expert g in the owner's x_recv
 //   expert_dst_w[g] the same row in the owner's w_recv (combine weight of each received row)
 //   ep_off[e]       (NL+1) local expert offsets in this rank's x_recv (GEMM row groups)
@@ -129,7 +130,7 @@ __host__ __device__ inline int64_t ep_src_row(const CT* C, int N, int s, int g) 
 // every owner's receive total against recv_cap (the same verdict on all ranks) and on overflow
 // sets bit 2 of `flag`, nulls expert_dst and zeroes ep_off, so nothing is written anywhere.
 __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __restrict__ C, int R, int N, int rank,
-                                                             int64_t recv_cap, int64_t row_bytes,
+                                                             int64_t recv_cap, int64_t x_row_bytes, int64_t row_bytes,
                                                              char* const* __restrict__ peer_x,
                                                              char* const* __restrict__ peer_y,
                                                              float* const* __restrict__ peer_w, void** expert_dst,
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __re
   for (int g = threadIdx.x; g < N; g += blockDim.x) {
     const int o = g / NL, e = g % NL;
     const int64_t row = ep_piece_row(C, R, N, o, e, rank);
-    expert_dst[g] = ok ? peer_x[o] + row * row_bytes : nullptr;
+    expert_dst[g] = ok ? peer_x[o] + row * x_row_bytes : nullptr;
     expert_dst_w[g] = ok ? peer_w[o] + row : nullptr;
   }
   for (int e = threadIdx.x; e <= NL; e += blockDim.x)

@@ -532,14 +532,13 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     const int e = idx[s];
     const int r = rb.offsets[e] + rb.tile_cnt[(size_t)tile * N + e] + rb.local_rank[s];
     rows[k] = r;
-    if constexpr (!kFp8) {
-      if (expert_dst) {
-        char* b = static_cast<char*>(expert_dst[e]);
-        dsts[k] = b ? b + (size_t)(r - rb.offsets[e]) * d * 2 : nullptr;
-        if (lane == 0 && b) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
-      } else {
-        dsts[k] = reinterpret_cast<__nv_bfloat16*>(xperm) + (size_t)r * d;
-      }
+    constexpr int kRowElemBytes = kFp8 ? 1 : 2;
+    if (expert_dst) {
+      char* b = static_cast<char*>(expert_dst[e]);
+      dsts[k] = b ? b + (size_t)(r - rb.offsets[e]) * d * kRowElemBytes : nullptr;
+      if (lane == 0 && b) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
+    } else {
+      dsts[k] = static_cast<char*>(xperm) + (size_t)r * d * kRowElemBytes;
     }
     if constexpr (kFp8) sc[k] = act_scale[e];
     if (lane == 0) {
@@ -564,7 +563,6 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
           if (v0 + u * 32 < nvec) st_na_v4(dst + v0 + u * 32, buf[u]);
       }
     }
-    if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
   } else {
     for (int v = lane; v < nvec; v += 32) {
       const int4 raw = ld_nc_v4(src + v);
@@ -583,11 +581,13 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
               make_float2(__fdiv_rn(f[4 * i + 2], sc[k]), __fdiv_rn(f[4 * i + 3], sc[k])), __NV_SATFINITE, __NV_E4M3);
           p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
         }
-        uint2* dst = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(xperm) + (size_t)rows[k] * d) + v;
+        if (!dsts[k]) continue;
+        uint2* dst = static_cast<uint2*>(dsts[k]) + v;
         *dst = make_uint2(p[0], p[1]);
       }
     }
   }
+  if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
 }
 
 // ---------------------------------------------------------------------------------------

@@ -124,13 +124,27 @@ __global__ void segment_absmax_kernel(const __nv_bfloat16* __restrict__ m, int c
   if (lane == 0) atomicMax(reinterpret_cast<int*>(out) + e, __float_as_int(mx));
 }
 
-// Per-column max |value| of a row-major bf16 matrix [rows][cols] into out[cols] (atomicMax on the
-// bit patterns of non-negative floats). Grid (cols/256, row chunks).
 // Calibration routing counts: acc[e] += counts[e] (collect_calibration).
 __global__ void add_counts_kernel(const int32_t* __restrict__ counts, int n, long long* __restrict__ acc) {
   for (int e = threadIdx.x; e < n; e += blockDim.x) acc[e] += counts[e];
 }
 
+// Source-side calibration under expert parallelism: out[g] = max |x_j| over the tokens j routed to
+// global expert g (one warp per token; atomicMax on non-negative float bit patterns).
+__global__ void route_absmax_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int K,
+                                    const int32_t* __restrict__ idx, float* __restrict__ out) {
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= T) return;
+  float mx = 0.0f;
+  const __nv_bfloat16* src = x + (size_t)j * d;
+  for (int i = lane; i < d; i += 32) mx = fmaxf(mx, fabsf(__bfloat162float(src[i])));
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane < K) atomicMax(reinterpret_cast<int*>(out) + idx[(size_t)j * K + lane], __float_as_int(mx));
+}
+
+// Per-column max |value| of a row-major bf16 matrix [rows][cols] into out[cols] (atomicMax on the
+// bit patterns of non-negative floats). Grid (cols/256, row chunks).
 __global__ void col_absmax_kernel(const __nv_bfloat16* __restrict__ m, int64_t rows, int cols, int rows_per_block,
                                   float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;

@@ -198,8 +198,10 @@ class MoELayer:
         if act_scale_in is None:
             rc = self.L.cl_moe_quantize_fp8(self.h, None, None)
         else:
-            a = np.ascontiguousarray(act_scale_in, np.float32)
-            b = np.ascontiguousarray(act_scale_mid, np.float32)
+            a = np.ascontiguousarray(act_scale_in, np.float32)  # [N]: every expert (EP: global table)
+            b = np.ascontiguousarray(act_scale_mid, np.float32)  # [N_local]
+            if a.size != self.cfg.n_experts or b.size != self.cfg.n_experts // self.cfg.ep_size:
+                raise MoEConfigError("act_scale_in needs n_experts entries, act_scale_mid n_experts/ep_size")
             rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
         self._check(rc, "quantize_fp8")
 

@@ -104,3 +104,64 @@ def test_peer_transport_single_rank_nccl():
         out = lay.ep_forward(x)
         lay.sync()
         assert torch.equal(out, ref.forward(x))
+
+
+@pytest.mark.parametrize("R,n,k,ts", [(2, 8, 2, (300, 517)), (4, 16, 4, (256, 1, 700, 64))])
+def test_group_forward_fp8_bit_identical_to_single_gpu(R, n, k, ts):
+    """Expert-parallel FP8: the source quantizes each dispatched row with its owner's GEMM1-input
+    scale (global table), owners run the e4m3 GEMMs; bit-identical to the single-GPU FP8 layer."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer, ep_group_forward
+    d, f = 512, 256
+    inp = make_inputs(sum(ts), d, n, f)
+    nl = n // R
+    cap = max(ts)
+    full = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=sum(ts)),
+                    inp["w_router"], inp["w_in"], inp["w_out"])
+    xall = _dev(inp["x"])
+    full.calibrate(xall)
+    full.quantize_fp8()
+    s_in, s_mid, _, _ = full.fp8_scales()
+    ranks = []
+    for r in range(R):
+        lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=cap, ep_size=R, ep_rank=r),
+                       inp["w_router"], inp["w_in"][r * nl:(r + 1) * nl], inp["w_out"][r * nl:(r + 1) * nl])
+        lay.quantize_fp8(s_in, s_mid[r * nl:(r + 1) * nl])
+        ranks.append(lay)
+    xs, a = [], 0
+    for t in ts:
+        xs.append(_dev(inp["x"][a:a + t]))
+        a += t
+    outs = ep_group_forward(ranks, xs)
+    for r in range(R):
+        assert torch.equal(outs[r], full.forward(xs[r])), f"rank {r}"
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_ep_fp8_calibration_single_rank_nccl(peer):
+    """EP calibration (source-side per-expert maxima, all-reduced by quantize) gives the same scales
+    as the single-GPU calibration; the FP8 EP forward then matches the single-GPU FP8 layer
+    (bit-identical over the peer transport, within bf16 rounding of the combine over NCCL)."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 600, 512, 8, 2, 256
+    inp = make_inputs(t, d, n, f)
+    x = _dev(inp["x"])
+    ref = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    ref.calibrate(x)
+    ref.quantize_fp8()
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    lay.ep_init(MoELayer.ep_unique_id())
+    if peer:
+        lay.ep_peer_init()
+    lay.calibrate(x)
+    lay.quantize_fp8()
+    for a_, b_ in zip(lay.fp8_scales(), ref.fp8_scales()):
+        assert np.array_equal(a_, b_)
+    out, want = lay.ep_forward(x), ref.forward(x)
+    lay.sync()
+    if peer:
+        assert torch.equal(out, want)
+    else:
+        dl = (out.float() - want.float()).abs().max().item()
+        assert dl <= 2e-2 * want.float().abs().max().item()
