@@ -138,7 +138,8 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, i
   return true;
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// SiLU with the MUFU exp2 / reciprocal pair (2 ulp in fp32; the result is rounded to bf16 / e4m3)
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
   const uint64_t pol = l2_policy_evict_first();
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const float da = __uint_as_float(a[i]);
-              const float s = 1.0f / (1.0f + __expf(-g[i]));
+              const float s = __fdividef(1.0f, 1.0f + __expf(-g[i]));
               du[i] = da * (g[i] * s);
               dg[i] = da * u[i] * (s * (1.0f + g[i] * (1.0f - s)));
             }
