@@ -444,8 +444,13 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int N = static_cast<int>(h->N);
   // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
+  static const int force = [] {
+    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "small" or "big"
+    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : 0) : 0;
+  }();
   const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
-  const bool big = (T + tpc_big - 1) / tpc_big >= h->num_sms && RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  const bool big_ok = RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
   const bool small = !big && router_smem_bytes(N, 32, 8) <= 220 * 1024;
   const int tpc = big ? tpc_big : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;

@@ -1,0 +1,27 @@
+"""Subprocess helper for tests/test_gpu_router_variants.py: route one batch on the GPU with the
+router variant forced by CL_MOE_ROUTER (read once per process) and compare with the oracle."""
+import sys
+
+import numpy as np
+import torch
+
+from oracle.oracle import Oracle, make_inputs
+from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+
+
+def main(t, d, n, k):
+    inp = make_inputs(t, d, n, 128, experts=False)
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=128, max_tokens=t), inp["w_router"],
+                   np.zeros((n, d, 256), np.float32), np.zeros((n, 128, d), np.float32))
+    dec = lay.route_tokens(torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16))
+    lay.sync()
+    ref = Oracle("port").route(inp["x"], inp["w_router"], k)
+    ok = (np.array_equal(dec.logits.cpu().numpy(), ref["logits"]) and
+          np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), ref["topk_idx"]) and
+          np.array_equal(dec.counts.cpu().numpy(), ref["counts"]))
+    print("ok" if ok else "MISMATCH")
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main(*map(int, sys.argv[1:5])))

@@ -1,0 +1,21 @@
+"""Both K1 router variants (small 1x4 with a deep prefetch ring, big 4x4), forced through
+CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
+including ragged last tiles and shapes where the automatic choice would pick another variant."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("variant", ["small", "big"])
+@pytest.mark.parametrize("t,d,n,k", [(333, 256, 16, 2), (1000, 512, 8, 2), (257, 256, 32, 4), (70, 1024, 4, 1)])
+def test_router_variant_bit_exact(variant, t, d, n, k):
+    env = dict(os.environ, CL_MOE_ROUTER=variant, PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "helpers", "route_check.py"), str(t), str(d), str(n),
+                        str(k)], env=env, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
