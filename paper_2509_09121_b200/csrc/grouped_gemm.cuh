@@ -138,6 +138,18 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, i
   return true;
 }
 
+// 32 consecutive per-column scales as 8 vector loads (FP8 epilogues; read-only, L1-cached)
+__device__ __forceinline__ void load_f32x32(const float* __restrict__ p, float* v) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p) + i);
+    v[4 * i] = t.x;
+    v[4 * i + 1] = t.y;
+    v[4 * i + 2] = t.z;
+    v[4 * i + 3] = t.w;
+  }
+}
+
 // SiLU with the MUFU exp2 / reciprocal pair (2 ulp in fp32; the result is rounded to bf16 / e4m3)
 __device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
@@ -412,12 +424,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
             for (int c = half * 2; c < half * 2 + 2; ++c) {
               uint32_t u[32];
+              float wu[32];
+              if constexpr (kFp8) load_f32x32(wsu + c * 32, wu);
               tmem_ld32(t_row + c * 32, u);
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 float uv = __uint_as_float(u[i]) * su;
-                if constexpr (kFp8) uv *= wsu[c * 32 + i];
+                if constexpr (kFp8) uv *= wu[i];
                 xbuf[r64 * Cfg::kXStride + c * 32 + i] = uv;
               }
             }
@@ -427,13 +441,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
             for (int c = half * 2; c < half * 2 + 2; ++c) {
               uint32_t g[32];
+              float wg[32];
+              if constexpr (kFp8) load_f32x32(wsg + c * 32, wg);
               tmem_ld32(t_row + c * 32, g);
               tmem_ld_wait();
               float v[32], gv[32], uv[32];
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 gv[i] = __uint_as_float(g[i]) * sg;
-                if constexpr (kFp8) gv[i] *= wsg[c * 32 + i];
+                if constexpr (kFp8) gv[i] *= wg[i];
                 uv[i] = xbuf[r64 * Cfg::kXStride + c * 32 + i];
                 v[i] = silu_f(gv[i]) * uv[i];
               }
@@ -445,6 +461,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
           for (int c = half * (kBN / 64 / 2); c < (half + 1) * (kBN / 64 / 2); ++c) {
             uint32_t g[32], u[32];
+            float wg[32], wu[32];
+            if constexpr (kFp8) {
+              load_f32x32(wsg + c * 32, wg);
+              load_f32x32(wsu + c * 32, wu);
+            }
             tmem_ld32(t_row + c * 32, g);
             tmem_ld32(t_row + kBN / 2 + c * 32, u);
             tmem_ld_wait();
@@ -454,8 +475,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               gv[i] = __uint_as_float(g[i]) * sg;
               uv[i] = __uint_as_float(u[i]) * su;
               if constexpr (kFp8) {
-                gv[i] *= wsg[c * 32 + i];
-                uv[i] *= wsu[c * 32 + i];
+                gv[i] *= wg[i];
+                uv[i] *= wu[i];
               }
               v[i] = silu_f(gv[i]) * uv[i];
             }
@@ -480,6 +501,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
         for (int c = c_lo; c < c_hi; ++c) {
           uint32_t a[32];
+          float wv[32];
+          if constexpr (kFp8) load_f32x32(ws + c * 32, wv);
           tmem_ld32(t_row + c * 32, a);
           tmem_ld_wait();
           if (evalid) {
@@ -487,7 +510,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               v[i] = __uint_as_float(a[i]) * rs;
-              if constexpr (kFp8) v[i] *= ws[c * 32 + i];
+              if constexpr (kFp8) v[i] *= wv[i];
             }
             const int col = ti.nt * kBN + col0 + c * 32;
             if (args.row_ptr)  // peer transport: the row returns to its source rank over NVLink
