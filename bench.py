@@ -209,10 +209,11 @@ def run_ours(args, cfg):
         layer.ep_init(obj[0])
     train = bool(cfg.get("train"))
     transport = "NCCL send/recv"
-    if world > 1 and not train and args.ep_transport == "peer":
+    if world > 1 and args.ep_transport == "peer":
         try:
             layer.ep_peer_init()
-            transport = "NVLink peer stores from the dispatch kernel and the GEMM2 epilogue; NCCL for counts"
+            transport = ("NVLink peer stores: dispatch kernel + GEMM2 epilogue" +
+                         (", combine-backward kernel + dgrad-2 epilogue" if train else "") + "; NCCL for counts/barriers")
         except Exception as e:  # no P2P between the devices: keep the NCCL transport, say so
             transport = f"NCCL send/recv (peer transport unavailable: {e})"
     if cfg.get("skew"):

@@ -251,7 +251,8 @@ cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
  * exchanged over the communicator). Afterwards the forward moves rows with direct peer stores —
  * the dispatch kernel writes into the owners' receive buffers and the GEMM2 epilogue writes each
  * output row back into its source rank's buffer — and NCCL carries only the counts and two
- * barriers. Training keeps the NCCL transport. Needs P2P access between the devices; if any
+ * barriers; training too (the combine-backward kernel stores dY rows into the owners' buffers,
+ * the dgrad-2 epilogue stores dX rows back). Needs P2P access between the devices; if any
  * rank cannot map its peers, every rank returns CL_ERR_RUN and keeps the NCCL transport. */
 cl_status cl_moe_ep_peer_init(cl_moe* h);
 /* Single-process, single-device emulation of an R-rank EP group (handles hs[r] created with
@@ -259,6 +260,14 @@ cl_status cl_moe_ep_peer_init(cl_moe* h);
  * for every rank, phase by phase, with the other handles' buffers as the "peer" addresses. */
 cl_status cl_moe_ep_group_forward(cl_moe* const* hs, int32_t R, const void* const* hidden,
                                   const int64_t* T, void* const* out, void* stream);
+/* Training step of an emulated single-device group (see cl_moe_ep_group_forward): forward_train
+ * and the expert-FFN backward (cl_moe_backward semantics) of every rank, with the backward's row
+ * exchanges as peer stores (combine-backward kernel into the owners' dY buffers, dgrad-2 epilogue
+ * into the sources' dX buffers). Per-rank arrays of R pointers. */
+cl_status cl_moe_ep_group_train_step(cl_moe* const* hs, int32_t R, const void* const* hidden,
+                                     const int64_t* T, void* const* out, const void* const* d_out,
+                                     void* const* d_hidden, float* const* d_combine_w,
+                                     float* const* dw_in, float* const* dw_out, void* stream);
 /* Pure host helper (no GPU): peer-transport layout of `rank` from counts[R][N]:
  * dispatch_row[g] = first row of this rank's piece for expert g in the owner's receive buffer;
  * return_row[e*R+s] = first row of piece (local expert e, source s) in s's permutation;

@@ -16,7 +16,12 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* _
                                                           const __nv_bfloat16* __restrict__ y,
                                                           const int32_t* __restrict__ perm,
                                                           const float* __restrict__ cw, int rows, int d, int K,
-                                                          __nv_bfloat16* __restrict__ dy, float* __restrict__ d_cw) {
+                                                          __nv_bfloat16* __restrict__ dy, float* __restrict__ d_cw,
+                                                          void* const* __restrict__ expert_dst = nullptr,
+                                                          const int32_t* __restrict__ idx = nullptr,
+                                                          const int32_t* __restrict__ offsets = nullptr) {
+  // expert_dst (EP peer transport): the dY row of expert g goes straight into the owner's dYbuf at
+  // expert_dst[g] + (r - offsets[g]) rows instead of dy[r].
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -26,6 +31,11 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* _
   const int4* g = reinterpret_cast<const int4*>(d_out + (size_t)j * d);
   const int4* yr = reinterpret_cast<const int4*>(y + (size_t)r * d);
   int4* o = reinterpret_cast<int4*>(dy + (size_t)r * d);
+  if (expert_dst) {
+    const int e = idx[s];
+    char* b = static_cast<char*>(expert_dst[e]);
+    o = b ? reinterpret_cast<int4*>(b + (size_t)(r - offsets[e]) * d * 2) : nullptr;
+  }
   float acc = 0.0f;
   for (int v = lane; v < d / 8; v += 32) {
     const int4 gv = ld_nc_v4(g + v);
@@ -44,10 +54,11 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* _
     ov.y = pack_bf16(f[2], f[3]);
     ov.z = pack_bf16(f[4], f[5]);
     ov.w = pack_bf16(f[6], f[7]);
-    st_na_v4(o + v, ov);
+    if (o) st_na_v4(o + v, ov);
   }
   for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   if (lane == 0) d_cw[s] = acc;
+  if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
 }
 
 // poff[e] = 64-aligned first padded row of expert e; kb_off[e] = poff[e] / 64 (k-blocks of the

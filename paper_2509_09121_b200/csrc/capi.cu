@@ -185,6 +185,11 @@ struct cl_moe {
   void** expert_dst = nullptr;          // [N] dispatch destinations of this rank's pieces
   float** expert_dst_w = nullptr;       // [N] ... of their combine weights
   void** row_ptr = nullptr;             // [recv_cap] return address of every received row
+  char** peer_dy_dev = nullptr;         // [R] every rank's dYbuf (training: dY rows to the owners)
+  char** peer_dx_dev = nullptr;         // [R] every rank's dXsrc (training: dX rows back)
+  void** expert_dst_dy = nullptr;       // [N] this rank's dY pieces in the owners' dYbuf
+  void** row_ptr_dx = nullptr;          // [recv_cap] source address of every received row's dX
+  bool ep_group = false;                // member of a single-process EP group (cl_moe_ep_group_*)
   float* bar_buf = nullptr;             // [1] payload of the exchange barriers
   std::vector<void*> ipc_opened;        // peers' buffers mapped through CUDA IPC
 
@@ -226,7 +231,8 @@ struct cl_moe {
                     (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
                     (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
-                    (void*)row_ptr, (void*)bar_buf})
+                    (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
+                    (void*)row_ptr_dx})
       if (p) cudaFree(p);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
@@ -700,15 +706,15 @@ void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStr
 // all-gather, (expert, source)-piece exchange, local grouped GEMMs, reverse exchange, weighted
 // combine. Requires cl_moe_ep_init. bf16 only in this round. `train` keeps H / A^T on the expert
 // side for cl_moe_backward.
-void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st);
+void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train);
 
 void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
   if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   if (fp8 && train) throw ConfigErr("training runs in bf16 (set_precision(BF16) first)");
   if (fp8) ep_fp8_maps(h);
-  if (h->ep_transport == 1 && !train) {
-    run_ep_peer(h, x, T, out, out_f32, st);
+  if (h->ep_transport == 1) {
+    run_ep_peer(h, x, T, out, out_f32, st, train);
     return;
   }
   NcclApi& nc = NcclApi::get();
@@ -781,6 +787,14 @@ void ep_peer_alloc(cl_moe* h) {
   h->expert_dst = dalloc<void*>(h->N);
   h->expert_dst_w = dalloc<float*>(h->N);
   h->row_ptr = dalloc<void*>(h->recv_cap);
+  h->peer_dy_dev = dalloc<char*>(R);
+  h->peer_dx_dev = dalloc<char*>(R);
+  h->expert_dst_dy = dalloc<void*>(h->N);
+  h->row_ptr_dx = dalloc<void*>(h->recv_cap);
+  if (h->f % 256 == 0) {  // training-capable: the two backward exchange targets, mapped by peers
+    if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
+    if (!h->dXsrc) h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * h->d);
+  }
   h->bar_buf = dalloc<float>(1);
   CK(cudaMemset(h->bar_buf, 0, sizeof(float)));
 }
@@ -791,7 +805,8 @@ void ep_peer_layout(cl_moe* h, cudaStream_t st) {
   ep_peer_layout_kernel<<<h->n_local * R + 1, 256, 0, st>>>(h->ep_counts_dev, R, (int)h->N, h->cfg.ep_rank, h->recv_cap,
                                                              xrb, h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
                                                              h->expert_dst, h->expert_dst_w, h->ep_off_dev, h->row_ptr,
-                                                             h->rb.finite_flag);
+                                                             h->rb.finite_flag, h->peer_dy_dev, h->peer_dx_dev,
+                                                             h->expert_dst_dy, h->row_ptr_dx);
   CK(cudaGetLastError());
 }
 
@@ -811,20 +826,32 @@ void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   prof_mark(h, 2, st);
 }
 
-void ep_peer_experts(cl_moe* h, cudaStream_t st) {
+void ep_peer_experts(cl_moe* h, cudaStream_t st, bool train = false) {
   if (h->precision == CL_MOE_FP8_E4M3) ep_fp8_maps(h);
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, h->w_recv, h->mA1e, h->mA2e, h->mA1eq, h->mA2eq, st, nullptr,
-            h->row_ptr);
+  if (train) {  // padded row plan of the receive layout for the weight-gradient GEMMs
+    pad_plan_kernel<<<1, 32, 0, st>>>(h->ep_off_dev, h->n_local, h->poff, h->kb_off);
+    CK(cudaGetLastError());
+  }
+  // inference: rows return weighted (as on one GPU); training keeps Y unweighted for the backward
+  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, train ? nullptr : h->w_recv, h->mA1e, h->mA2e, h->mA1eq,
+            h->mA2eq, st, train ? h->Hbuf : nullptr, h->row_ptr);
   prof_mark(h, 4, st);
 }
 
-void ep_peer_combine(cl_moe* h, int64_t T, void* out, bool out_f32, cudaStream_t st) {
-  // rows arrive already scaled by their combine weight (GEMM2 epilogue), as on one GPU
+void ep_peer_combine(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st,
+                     bool train = false) {
+  // inference: rows arrive already scaled by their combine weight (GEMM2 epilogue), as on one GPU
+  const float* w = train ? h->rb.combine_w : nullptr;
   if (out_f32)
-    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
+    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
+                          w);
   else
     launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
-                                  h->rb.finite_flag, st);
+                                  h->rb.finite_flag, st, w);
+  if (train) {
+    h->train_T = T;
+    h->cur_x = x;
+  }
   CK(cudaGetLastError());
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
@@ -837,34 +864,35 @@ void ep_peer_combine(cl_moe* h, int64_t T, void* out, bool out_f32, cudaStream_t
 //   all-gather(counts) -> layout -> dispatch (stores into owners' x_recv) -> barrier
 //   -> GEMM1 -> GEMM2 (epilogue stores into sources' y) -> barrier -> combine
 // The first all-gather also orders this forward after every rank's previous use of x_recv / y.
-void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
   NcclApi& nc = NcclApi::get();
   NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)h->N, NcclApi::kInt32, h->comm, st));
   ep_peer_layout(h, st);
   ep_peer_dispatch(h, x, T, st);
   NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-  ep_peer_experts(h, st);
+  ep_peer_experts(h, st, train);
   NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-  ep_peer_combine(h, T, out, out_f32, st);
+  ep_peer_combine(h, x, T, out, out_f32, st, train);
 }
 
 void ensure_training(cl_moe* h) {
   if (h->train_ready) return;
   if (h->f % 256) throw ConfigErr("training needs d_ff to be a multiple of 256");
-  if (h->cfg.ep_size > 1 && !h->comm) throw ConfigErr("expert-parallel training needs cl_moe_ep_init first");
-  const bool ep = h->comm != nullptr;
+  if (h->cfg.ep_size > 1 && !h->comm && !h->ep_group)
+    throw ConfigErr("expert-parallel training needs cl_moe_ep_init first");
+  const bool ep = h->comm != nullptr || h->ep_group;
   // expert-side rows: the receive buffer under expert parallelism
   const int64_t rows = ep ? h->recv_cap : h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
   if (!h->win_ref) {  // buffers and descriptors: once per handle
     if (ep) {
       h->dYsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
-      h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
+      if (!h->dXsrc) h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
     }
     h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
     h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
     h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
     h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-    h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
+    if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
     h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
     h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
     h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
@@ -901,6 +929,8 @@ void ensure_training(cl_moe* h) {
 // combine (fp32) so the backward can form d(combine_w) = <dOut, Y>.
 void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStream_t st) {
   if (h->precision != CL_MOE_BF16) throw ConfigErr("training runs in bf16");
+  if (h->cfg.ep_size > 1 && !h->comm)
+    throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_train_step)");
   ensure_training(h);
   if (h->comm) {
     run_ep(h, x, T, out, false, st, true);
@@ -928,25 +958,52 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
 }
 
 // Expert-FFN backward of the last training forward.
-void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, float* dw_in, float* dw_out,
-                  cudaStream_t st, float* dw_router = nullptr, float g_aux = 0.0f, float g_z = 0.0f) {
+// Backward phases (shared by the single-handle call and the single-process EP group):
+//   A  combine backward (+ dY rows to the experts' owners)
+//   B  dgrad GEMMs on the expert side (+ dX rows back to their sources)
+//   C  dispatch backward (+ router backward)
+//   D  transposes and weight-gradient GEMMs
+// Under the peer transport, A's kernel stores dY rows straight into the owners' dYbuf and B's
+// dgrad-2 epilogue stores dX rows straight into the sources' dXsrc; the caller puts a barrier
+// between A/B and B/C (NCCL all-reduce of one float, or phase order in the group).
+struct BwdArgs {
+  const void* d_out;
+  void* d_hidden;
+  float* d_cw;
+  float* dw_in;
+  float* dw_out;
+  float* dw_router;
+  float g_aux, g_z;
+};
+
+bool ep_mode(const cl_moe* h) { return h->comm != nullptr || h->ep_group; }
+bool ep_peer_mode(const cl_moe* h) { return h->ep_group || (h->comm && h->ep_transport == 1); }
+
+void bwd_check(cl_moe* h) {
   if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
-  const int64_t T = h->train_T, rows = T * h->K, d = h->d, f = h->f;
-  const int NL = h->n_local;
-  const bool ep = h->comm != nullptr;
-  // expert-side views: the receive buffers under expert parallelism
-  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
-  const void* es_x = ep ? static_cast<const void*>(h->x_recv) : h->xperm;
+}
+
+void bwd_phase_a(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
+  const int64_t T = h->train_T, rows = T * h->K, d = h->d;
+  const bool ep = ep_mode(h), peer = ep_peer_mode(h);
   __nv_bfloat16* dY_src = ep ? h->dYsrc : h->dYbuf;
-  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
   prof_begin(h, st, 1);
   // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
-  combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(d_out), h->y, h->perm,
+  combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.d_out), h->y, h->perm,
                                                            h->rb.combine_w, (int)rows, (int)d, (int)h->K, dY_src,
-                                                           d_cw);
+                                                           a.d_cw, peer ? h->expert_dst_dy : nullptr, h->rb.topk_idx,
+                                                           h->rb.offsets);
   CK(cudaGetLastError());
-  if (ep) ep_exchange(h, dY_src, h->dYbuf, true, st);  // dY rows to the experts' owners
+  if (ep && !peer) ep_exchange(h, dY_src, h->dYbuf, true, st);  // dY rows to the experts' owners
   prof_mark(h, 0, st);
+}
+
+void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
+  const int64_t d = h->d, f = h->f;
+  const int NL = h->n_local;
+  const bool ep = ep_mode(h), peer = ep_peer_mode(h);
+  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
+  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
   const int v = h->gemm_ctas == 2 ? 1 : 0;  // same variant the training forward chose
   // 2. dA = dY W_out^T fused with the SwiGLU backward -> dH
   GemmArgs a1{};
@@ -961,7 +1018,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   a1.aux_t = h->dHT;  // dH^T straight from the epilogue (dW_in GEMM operand)
   a1.rp = h->rp_cap;
   a1.poff = h->poff;
-  // 3. dX = dH W_in^T
+  // 3. dX = dH W_in^T (peer transport: each row straight back into its source's dXsrc)
   GemmArgs a2{};
   a2.offsets = es_off;
   a2.n_experts = NL;
@@ -970,6 +1027,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   a2.b_rows_per_expert = static_cast<int>(d);
   a2.out = h->dXbuf;
   a2.ldo = static_cast<int>(d);
+  a2.row_ptr = peer ? h->row_ptr_dx : nullptr;
   if (v) {
     launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
     prof_mark(h, 1, st);
@@ -979,37 +1037,52 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
     prof_mark(h, 1, st);
     launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
   }
-  if (ep) ep_exchange(h, h->dXbuf, dX_src, false, st);  // dX rows back to their tokens' ranks
+  if (ep && !peer) ep_exchange(h, h->dXbuf, dX_src, false, st);  // dX rows back to their tokens' ranks
   prof_mark(h, 2, st);
+}
+
+void bwd_phase_c(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
+  const int64_t T = h->train_T, d = h->d;
+  const bool ep = ep_mode(h);
+  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
   // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]  (+ router term)
-  if (dw_router) {
+  if (a.dw_router) {
     const int N = static_cast<int>(h->N);
     if (!h->rdz) {
       h->rdz = dalloc<float>(h->cap * h->N);
       h->rpart = dalloc<float>(((h->cap + kRwTokens - 1) / kRwTokens) * h->d * h->N);
     }
-    router_bwd_dz_kernel<<<(int)((T + 127) / 128), 128, 0, st>>>(h->rb.probs, h->rb.logits, h->rb.topk_idx, d_cw,
-                                                                h->rb.counts, (int)T, N, (int)h->K, g_aux, g_z, h->rdz);
+    router_bwd_dz_kernel<<<(int)((T + 127) / 128), 128, 0, st>>>(h->rb.probs, h->rb.logits, h->rb.topk_idx, a.d_cw,
+                                                                h->rb.counts, (int)T, N, (int)h->K, a.g_aux, a.g_z,
+                                                                h->rdz);
     const int chunks = static_cast<int>((T + kRwTokens - 1) / kRwTokens);
     router_wgrad_partial_kernel<<<dim3((unsigned)(d / 64), (unsigned)chunks, (unsigned)((N + 15) / 16)), 256, 0, st>>>(
         static_cast<const __nv_bfloat16*>(h->cur_x), h->rdz, (int)T, (int)d, N, h->rpart);
-    router_wgrad_reduce_kernel<<<(int)((d * N + 255) / 256), 256, 0, st>>>(h->rpart, chunks, (int)(d * N), dw_router);
+    router_wgrad_reduce_kernel<<<(int)((d * N + 255) / 256), 256, 0, st>>>(h->rpart, chunks, (int)(d * N), a.dw_router);
     // the router is replicated: its gradient is the sum over the data-parallel ranks
-    if (ep) NCK(NcclApi::get().AllReduce(dw_router, dw_router, (size_t)(d * N), NcclApi::kFloat32, NcclApi::kSum,
-                                         h->comm, st));
+    if (h->comm) NCK(NcclApi::get().AllReduce(a.dw_router, a.dw_router, (size_t)(d * N), NcclApi::kFloat32,
+                                              NcclApi::kSum, h->comm, st));
     const int blocks = static_cast<int>((T + 7) / 8);
     switch (h->K) {
-      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
-      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
-      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(d_hidden)); break;
+      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
+      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
+      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
       default: throw ConfigErr("router backward supports top_k in {1, 2, 4}");
     }
   } else {
-    launch_combine<__nv_bfloat16>(dX_src, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(d_hidden),
+    launch_combine<__nv_bfloat16>(dX_src, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(a.d_hidden),
                                   h->rb.finite_flag, st);
   }
   CK(cudaGetLastError());
   prof_mark(h, 3, st);
+}
+
+void bwd_phase_d(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
+  const int64_t d = h->d, f = h->f;
+  const int NL = h->n_local;
+  const bool ep = ep_mode(h);
+  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
+  const void* es_x = ep ? static_cast<const void*>(h->x_recv) : h->xperm;
   // 5. weight gradients over each expert's rows (variable K): padded K-major transposes, then
   //    dW_out[e] = A_e^T dY_e ([f x d]) and dW_in[e] = X_e^T dH_e ([d x 2f]), fp32.
   //    (A^T and dH^T were written by the GEMM1 / dgrad-1 epilogues; only their padding columns
@@ -1020,9 +1093,9 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT,
                                                                      h->rp_cap);
   zero_pad_cols_kernel<<<dim3((unsigned)((f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
-                                                                                        h->poff);
+                                                                                    h->poff);
   zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
-                                                                                            h->rp_cap, es_off, h->poff);
+                                                                                        h->rp_cap, es_off, h->poff);
   CK(cudaGetLastError());
   prof_mark(h, 4, st);
   const int gw = (f % 256 == 0) ? 2 : 1;
@@ -1031,7 +1104,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   wo.kb_off = h->kb_off;
   wo.m_tiles = static_cast<int>(f / (128 * gw));
   wo.n_tiles_n = static_cast<int>(d / kBN);
-  wo.out = dw_out;
+  wo.out = a.dw_out;
   wo.ldo = static_cast<int>(d);
   wo.out_estride = f * d;
   GemmArgs wi{};
@@ -1039,7 +1112,7 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   wi.kb_off = h->kb_off;
   wi.m_tiles = static_cast<int>(d / (128 * gw));
   wi.n_tiles_n = static_cast<int>(2 * f / kBN);
-  wi.out = dw_in;
+  wi.out = a.dw_in;
   wi.ldo = static_cast<int>(2 * f);
   wi.out_estride = d * 2 * f;
   if (gw == 2) {
@@ -1053,6 +1126,25 @@ void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, flo
   }
   prof_mark(h, 6, st);
   h->cur_ev = nullptr;
+}
+
+// One float all-reduce on the communicator: orders every rank's preceding peer stores before
+// anything this rank issues next (the stores were fenced with __threadfence_system).
+void ep_barrier(cl_moe* h, cudaStream_t st) {
+  NCK(NcclApi::get().AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+}
+
+void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, float* dw_in, float* dw_out,
+                  cudaStream_t st, float* dw_router = nullptr, float g_aux = 0.0f, float g_z = 0.0f) {
+  bwd_check(h);
+  const BwdArgs a{d_out, d_hidden, d_cw, dw_in, dw_out, dw_router, g_aux, g_z};
+  const bool peer = h->comm && h->ep_transport == 1;
+  bwd_phase_a(h, a, st);
+  if (peer) ep_barrier(h, st);
+  bwd_phase_b(h, a, st);
+  if (peer) ep_barrier(h, st);
+  bwd_phase_c(h, a, st);
+  bwd_phase_d(h, a, st);
 }
 
 }  // namespace
@@ -1096,10 +1188,11 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     ep_peer_alloc(h);
     // exchange the IPC handles of x_recv and y over the communicator
     constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-    constexpr int kB = 3;  // x_recv, y, w_recv
-    void* const own[kB] = {h->x_recv, h->y, h->w_recv};
-    std::vector<uint8_t> mine(kB * kH), all(kB * kH * R);
+    constexpr int kB = 5;  // x_recv, y, w_recv, and for training dYbuf, dXsrc
+    void* const own[kB] = {h->x_recv, h->y, h->w_recv, h->dYbuf, h->dXsrc};
+    std::vector<uint8_t> mine(kB * kH, 0), all(kB * kH * R);
     for (int b = 0; b < kB; ++b) {
+      if (!own[b]) continue;  // not training-capable (d_ff % 256): an all-zero handle
       cudaIpcMemHandle_t hb;
       CK(cudaIpcGetMemHandle(&hb, own[b]));
       std::memcpy(mine.data() + b * kH, &hb, kH);
@@ -1120,6 +1213,7 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
           peer[b][s] = own[b];
           continue;
         }
+        if (!own[b]) continue;  // same on every rank (same configuration)
         cudaIpcMemHandle_t hd;
         std::memcpy(&hd, all.data() + ((size_t)s * kB + b) * kH, kH);
         void* p = nullptr;
@@ -1149,8 +1243,63 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     CK(cudaMemcpy(h->peer_x_dev, peer[0].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_y_dev, peer[1].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_w_dev, peer[2].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->peer_dy_dev, peer[3].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->peer_dx_dev, peer[4].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     h->ep_transport = 1;
   });
+}
+
+// Single-process emulation of R expert-parallel ranks on one device (test and bring-up path):
+// the same layout / dispatch / GEMM / combine kernels with "peer" addresses that are the other
+// handles' buffers. Every phase runs for all ranks before the next one starts, in stream order,
+// so no kernel ever waits on another; the count all-gather becomes R x R device copies.
+static void group_check(cl_moe* const* hs, int R) {
+  cl_moe* h0 = hs[0];
+  for (int r = 0; r < R; ++r) {
+    cl_moe* h = hs[r];
+    if (h->cfg.ep_size != R || h->cfg.ep_rank != r || h->N != h0->N || h->d != h0->d || h->f != h0->f ||
+        h->K != h0->K || h->cfg.device != h0->cfg.device)
+      throw ConfigErr(fmt("handle %d is not rank %d of a matching %d-rank group", r, r, R));
+    if (h->precision != h0->precision) throw ConfigErr("all ranks of a group need the same precision");
+    if (h->comm) throw ConfigErr("group handles must not have a communicator");
+  }
+}
+
+// Forward of every rank, phase by phase (see cl_moe_ep_group_forward).
+static void group_forward(cl_moe* const* hs, int R, const void* const* hidden, const int64_t* T, void* const* out,
+                          cudaStream_t st, bool train) {
+  const int N = static_cast<int>(hs[0]->N);
+  std::vector<char*> px(R), py(R), pdy(R), pdx(R);
+  std::vector<float*> pw(R);
+  for (int r = 0; r < R; ++r) {
+    cl_moe* h = hs[r];
+    h->ep_group = true;
+    ep_alloc(h);
+    ep_peer_alloc(h);
+    if (train) ensure_training(h);
+    px[r] = reinterpret_cast<char*>(h->x_recv);
+    py[r] = reinterpret_cast<char*>(h->y);
+    pw[r] = h->w_recv;
+    pdy[r] = reinterpret_cast<char*>(h->dYbuf);
+    pdx[r] = reinterpret_cast<char*>(h->dXsrc);
+  }
+  for (int r = 0; r < R; ++r) {
+    CK(cudaMemcpyAsync(hs[r]->peer_x_dev, px.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(hs[r]->peer_y_dev, py.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(hs[r]->peer_w_dev, pw.data(), sizeof(float*) * R, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(hs[r]->peer_dy_dev, pdy.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(hs[r]->peer_dx_dev, pdx.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+  }
+  for (int r = 0; r < R; ++r) run_router(hs[r], hidden[r], T[r], st);
+  for (int r = 0; r < R; ++r)
+    for (int s = 0; s < R; ++s)
+      CK(cudaMemcpyAsync(hs[r]->ep_counts_dev + (size_t)s * N, hs[s]->rb.counts, sizeof(int32_t) * N,
+                         cudaMemcpyDeviceToDevice, st));
+  for (int r = 0; r < R; ++r) ep_peer_layout(hs[r], st);
+  for (int r = 0; r < R; ++r) ep_peer_dispatch(hs[r], hidden[r], T[r], st);
+  for (int r = 0; r < R; ++r) ep_peer_experts(hs[r], st, train);
+  for (int r = 0; r < R; ++r) ep_peer_combine(hs[r], hidden[r], T[r], out[r], false, st, train);
+  CK(cudaStreamSynchronize(st));  // the host pointer tables above must outlive their copies
 }
 
 // Single-process emulation of R expert-parallel ranks on one device (test and bring-up path):
@@ -1162,43 +1311,45 @@ cl_status cl_moe_ep_group_forward(cl_moe* const* hs, int32_t R, const void* cons
   if (!hs || R < 1 || !hidden || !T || !out) return CL_ERR_CONFIG;
   for (int r = 0; r < R; ++r)
     if (!hs[r]) return CL_ERR_CONFIG;
-  cl_moe* h0 = hs[0];
-  return guarded(h0, [&] {
-    cudaStream_t st = (cudaStream_t)stream;
-    const int N = static_cast<int>(h0->N);
-    for (int r = 0; r < R; ++r) {
-      cl_moe* h = hs[r];
-      if (h->cfg.ep_size != R || h->cfg.ep_rank != r || h->N != N || h->d != h0->d || h->f != h0->f ||
-          h->K != h0->K || h->cfg.device != h0->cfg.device)
-        throw ConfigErr(fmt("handle %d is not rank %d of a matching %d-rank group", r, r, R));
-      if (h->precision != h0->precision) throw ConfigErr("all ranks of a group need the same precision");
-      if (!hidden[r] || !out[r]) throw ConfigErr("null argument");
-    }
-    CK(cudaSetDevice(h0->cfg.device));
-    std::vector<char*> px(R), py(R);
-    std::vector<float*> pw(R);
-    for (int r = 0; r < R; ++r) {
-      ep_alloc(hs[r]);
-      ep_peer_alloc(hs[r]);
-      px[r] = reinterpret_cast<char*>(hs[r]->x_recv);
-      py[r] = reinterpret_cast<char*>(hs[r]->y);
-      pw[r] = hs[r]->w_recv;
-    }
-    for (int r = 0; r < R; ++r) {
-      CK(cudaMemcpyAsync(hs[r]->peer_x_dev, px.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(hs[r]->peer_y_dev, py.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(hs[r]->peer_w_dev, pw.data(), sizeof(float*) * R, cudaMemcpyHostToDevice, st));
-    }
-    for (int r = 0; r < R; ++r) run_router(hs[r], hidden[r], T[r], st);
+  return guarded(hs[0], [&] {
+    group_check(hs, R);
     for (int r = 0; r < R; ++r)
-      for (int s = 0; s < R; ++s)
-        CK(cudaMemcpyAsync(hs[r]->ep_counts_dev + (size_t)s * N, hs[s]->rb.counts, sizeof(int32_t) * N,
-                           cudaMemcpyDeviceToDevice, st));
-    for (int r = 0; r < R; ++r) ep_peer_layout(hs[r], st);
-    for (int r = 0; r < R; ++r) ep_peer_dispatch(hs[r], hidden[r], T[r], st);
-    for (int r = 0; r < R; ++r) ep_peer_experts(hs[r], st);
-    for (int r = 0; r < R; ++r) ep_peer_combine(hs[r], T[r], out[r], false, st);
-    CK(cudaStreamSynchronize(st));  // the host pointer tables above must outlive their copies
+      if (!hidden[r] || !out[r]) throw ConfigErr("null argument");
+    CK(cudaSetDevice(hs[0]->cfg.device));
+    group_forward(hs, R, hidden, T, out, (cudaStream_t)stream, false);
+  });
+}
+
+// Training step of an emulated group: forward_train + expert-FFN backward of every rank, with
+// the backward's two row exchanges as peer stores (combine-backward kernel -> owners' dYbuf,
+// dgrad-2 epilogue -> sources' dXsrc), phase by phase.
+cl_status cl_moe_ep_group_train_step(cl_moe* const* hs, int32_t R, const void* const* hidden, const int64_t* T,
+                                     void* const* out, const void* const* d_out, void* const* d_hidden,
+                                     float* const* d_combine_w, float* const* dw_in, float* const* dw_out,
+                                     void* stream) {
+  if (!hs || R < 1 || !hidden || !T || !out || !d_out || !d_hidden || !d_combine_w || !dw_in || !dw_out)
+    return CL_ERR_CONFIG;
+  for (int r = 0; r < R; ++r)
+    if (!hs[r]) return CL_ERR_CONFIG;
+  return guarded(hs[0], [&] {
+    group_check(hs, R);
+    for (int r = 0; r < R; ++r) {
+      if (!hidden[r] || !out[r] || !d_out[r] || !d_hidden[r] || !d_combine_w[r] || !dw_in[r] || !dw_out[r])
+        throw ConfigErr("null argument");
+      if (hs[r]->precision != CL_MOE_BF16) throw ConfigErr("training runs in bf16");
+    }
+    CK(cudaSetDevice(hs[0]->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    group_forward(hs, R, hidden, T, out, st, true);
+    std::vector<BwdArgs> a(R);
+    for (int r = 0; r < R; ++r) {
+      bwd_check(hs[r]);
+      a[r] = BwdArgs{d_out[r], d_hidden[r], d_combine_w[r], dw_in[r], dw_out[r], nullptr, 0.0f, 0.0f};
+    }
+    for (int r = 0; r < R; ++r) bwd_phase_a(hs[r], a[r], st);
+    for (int r = 0; r < R; ++r) bwd_phase_b(hs[r], a[r], st);
+    for (int r = 0; r < R; ++r) bwd_phase_c(hs[r], a[r], st);
+    for (int r = 0; r < R; ++r) bwd_phase_d(hs[r], a[r], st);
   });
 }
 

@@ -126,6 +126,8 @@ __host__ __device__ inline int64_t ep_src_row(const CT* C, int N, int s, int g) 
 //   expert_dst_w[g] the same row in the owner's w_recv (combine weight of each received row)
 //   ep_off[e]       (NL+1) local expert offsets in this rank's x_recv (GEMM row groups)
 //   row_ptr[r]      for every received row r: its return address in the source rank's y
+// and, for training (peer_dy / peer_dx mapped): expert_dst_dy[g] (this rank's dY piece in the
+// owner's dYbuf) and row_ptr_dx[r] (the received row's dX slot in the source's dXsrc)
 // Blocks 0..NL*R-1 fill row_ptr for one (local expert, source) piece each; the last block checks
 // every owner's receive total against recv_cap (the same verdict on all ranks) and on overflow
 // sets bit 2 of `flag`, nulls expert_dst and zeroes ep_off, so nothing is written anywhere.
@@ -135,15 +137,21 @@ __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __re
                                                              char* const* __restrict__ peer_y,
                                                              float* const* __restrict__ peer_w, void** expert_dst,
                                                              float** expert_dst_w, int32_t* ep_off, void** row_ptr,
-                                                             int32_t* flag) {
+                                                             int32_t* flag, char* const* __restrict__ peer_dy,
+                                                             char* const* __restrict__ peer_dx, void** expert_dst_dy,
+                                                             void** row_ptr_dx) {
   const int NL = N / R;
   if (blockIdx.x < (unsigned)(NL * R)) {
     const int e = blockIdx.x / R, s = blockIdx.x % R, g = rank * NL + e;
     const int64_t start = ep_piece_row(C, R, N, rank, e, s);
     const int64_t n = C[(int64_t)s * N + g];
-    char* dst = peer_y[s] + ep_src_row(C, N, s, g) * row_bytes;
-    for (int64_t j = threadIdx.x; j < n && start + j < recv_cap; j += blockDim.x)
+    const int64_t src_row = ep_src_row(C, N, s, g);
+    char* dst = peer_y[s] + src_row * row_bytes;
+    char* dxb = peer_dx ? peer_dx[s] : nullptr;
+    for (int64_t j = threadIdx.x; j < n && start + j < recv_cap; j += blockDim.x) {
       row_ptr[start + j] = dst + j * row_bytes;
+      if (dxb) row_ptr_dx[start + j] = dxb + (src_row + j) * row_bytes;
+    }
     return;
   }
   __shared__ int ok;
@@ -160,6 +168,8 @@ __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __re
     const int64_t row = ep_piece_row(C, R, N, o, e, rank);
     expert_dst[g] = ok ? peer_x[o] + row * x_row_bytes : nullptr;
     expert_dst_w[g] = ok ? peer_w[o] + row : nullptr;
+    char* dyb = peer_dy ? peer_dy[o] : nullptr;
+    expert_dst_dy[g] = (ok && dyb) ? dyb + row * row_bytes : nullptr;
   }
   for (int e = threadIdx.x; e <= NL; e += blockDim.x)
     ep_off[e] = ok ? static_cast<int32_t>(ep_piece_row(C, R, N, rank, e, 0)) : 0;

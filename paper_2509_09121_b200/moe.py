@@ -419,3 +419,28 @@ def ep_group_forward(layers, hidden):
     _lib.check(_lib.lib().cl_moe_ep_group_forward(hs, R, xs, ts, os_, _stream(layers[0].device)), layers[0].h,
                "ep_group_forward")
     return outs
+
+
+def ep_group_train_step(layers, hidden, d_out):
+    """Single-device emulation of an R-rank EP training step over the peer transport:
+    returns per rank (out, d_hidden, d_combine_w, dw_in, dw_out) (cl_moe_backward semantics)."""
+    R = len(layers)
+    hidden = [lay._bf16(x) for lay, x in zip(layers, hidden)]
+    d_out = [lay._bf16(g) for lay, g in zip(layers, d_out)]
+    outs = [torch.empty_like(x) for x in hidden]
+    dhs = [torch.empty_like(x) for x in hidden]
+    cfg = layers[0].cfg
+    nl, d, f, k = cfg.n_experts // cfg.ep_size, cfg.d_model, cfg.d_ff, cfg.top_k
+    dev = layers[0].device
+    dcw = [torch.empty(x.shape[0], k, dtype=torch.float32, device=dev) for x in hidden]
+    dwi = [torch.empty(nl, d, 2 * f, dtype=torch.float32, device=dev) for _ in range(R)]
+    dwo = [torch.empty(nl, f, d, dtype=torch.float32, device=dev) for _ in range(R)]
+
+    def arr(ts):
+        return (C.c_void_p * R)(*[t.data_ptr() for t in ts])
+    hs = (C.c_void_p * R)(*[lay.h.value for lay in layers])
+    ts = (C.c_int64 * R)(*[x.shape[0] for x in hidden])
+    _lib.check(_lib.lib().cl_moe_ep_group_train_step(hs, R, arr(hidden), ts, arr(outs), arr(d_out), arr(dhs), arr(dcw),
+                                                     arr(dwi), arr(dwo), _stream(dev)), layers[0].h,
+               "ep_group_train_step")
+    return [(outs[r], dhs[r], dcw[r], dwi[r], dwo[r]) for r in range(R)]

@@ -165,3 +165,60 @@ def test_ep_fp8_calibration_single_rank_nccl(peer):
     else:
         dl = (out.float() - want.float()).abs().max().item()
         assert dl <= 2e-2 * want.float().abs().max().item()
+
+
+@pytest.mark.parametrize("R,n,k,t", [(2, 8, 2, 300), (4, 16, 2, 200)])
+def test_group_train_step_bit_identical_to_single_gpu(R, n, k, t):
+    """EP training over the peer transport (emulated group): forward_train + expert-FFN backward.
+    Ranks hold consecutive token slices, so each expert's receive layout is the single-GPU row
+    order of the concatenated batch: outputs, d_hidden, d_combine_w AND the weight gradients are
+    bit-identical to the single-GPU layer on the whole batch."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer, ep_group_train_step
+    d, f = 256, 256
+    inp = make_inputs(R * t, d, n, f)
+    g = make_inputs(R * t, d, 1, f, seed=99, experts=False)["x"]
+    nl = n // R
+    full = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=R * t, gemm_ctas=2),
+                    inp["w_router"], inp["w_in"], inp["w_out"])
+    out_f = full.forward_train(_dev(inp["x"]))
+    dh_f, dcw_f, dwi_f, dwo_f = full.backward(_dev(g))
+    full.sync()
+    ranks = [MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t, gemm_ctas=2, ep_size=R,
+                                ep_rank=r),
+                      inp["w_router"], inp["w_in"][r * nl:(r + 1) * nl], inp["w_out"][r * nl:(r + 1) * nl])
+             for r in range(R)]
+    res = ep_group_train_step(ranks, [_dev(inp["x"][r * t:(r + 1) * t]) for r in range(R)],
+                              [_dev(g[r * t:(r + 1) * t]) for r in range(R)])
+    for r in range(R):
+        out, dh, dcw, dwi, dwo = res[r]
+        sl = slice(r * t, (r + 1) * t)
+        assert torch.equal(out, out_f[sl]), f"out rank {r}"
+        assert torch.equal(dh, dh_f[sl]), f"d_hidden rank {r}"
+        assert torch.equal(dcw, dcw_f[sl]), f"d_combine_w rank {r}"
+        assert torch.equal(dwi, dwi_f[r * nl:(r + 1) * nl]), f"dW_in rank {r}"
+        assert torch.equal(dwo, dwo_f[r * nl:(r + 1) * nl]), f"dW_out rank {r}"
+
+
+def test_peer_transport_training_single_rank_nccl():
+    """ep_size = 1 with a real communicator over the peer transport: training matches the
+    single-GPU layer bit for bit (full backward incl. the router, dW_r all-reduced)."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoELayer
+    t, d, n, k, f = 400, 256, 8, 2, 256
+    inp = make_inputs(t, d, n, f)
+    g = make_inputs(t, d, 1, f, seed=5, experts=False)["x"]
+    ref = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t),
+                   inp["w_router"], inp["w_in"], inp["w_out"])
+    lay.ep_init(MoELayer.ep_unique_id())
+    lay.ep_peer_init()
+    x, gd = _dev(inp["x"]), _dev(g)
+    for _ in range(2):
+        a = lay.forward_train(x)
+        ga = lay.backward_full(gd, 0.01, 0.001)
+        b = ref.forward_train(x)
+        gb = ref.backward_full(gd, 0.01, 0.001)
+        lay.sync()
+        assert torch.equal(a, b)
+        for u, v in zip(ga, gb):
+            assert torch.equal(u, v)
