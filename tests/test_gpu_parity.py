@@ -338,3 +338,23 @@ def test_pair_tail_tiles_match_single_cta(precision):
     tails = counts % 256
     assert ((tails > 0) & (tails <= 128)).sum() >= 10 and (tails > 128).sum() >= 5
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("gemm_ctas", [1, 2])
+@pytest.mark.parametrize("t,d,n,k,f", [(1, 256, 128, 8, 128), (7, 256, 1, 1, 128), (5, 512, 128, 1, 256),
+                                       (64, 8192, 4, 2, 128), (1000, 256, 64, 8, 128), (2, 256, 2, 2, 384)])
+def test_layer_forward_edge_shapes(gemm_ctas, t, d, n, k, f):
+    """Limits of the configuration space: one token, one expert, N = 128 with K = 8 (most experts
+    empty), the widest hidden size at a tiny batch, f not a multiple of 256."""
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, f)
+    r = o.route(inp["x"], inp["w_router"], k)
+    ref = o.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], jobs=JOBS)
+    lay = _layer(inp, t, k, gemm_ctas=gemm_ctas)
+    out, dec = lay.forward(_x_dev(inp["x"]), want_decision=True)
+    lay.sync()
+    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), r["topk_idx"])
+    assert np.array_equal(dec.counts.cpu().numpy(), r["counts"])
+    rf, rm = _rel(out.float().cpu().numpy(), ref)
+    assert rf <= 1e-2 and rm <= 3e-2, (rf, rm)
+    lay.close()
