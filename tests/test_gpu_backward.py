@@ -24,7 +24,8 @@ def _rel(a, b):
 
 
 @pytest.mark.parametrize("gemm_ctas", [1, 2])
-@pytest.mark.parametrize("t,d,n,k,f", [(300, 256, 4, 2, 256), (1100, 512, 8, 2, 512), (37, 256, 8, 1, 256)])
+@pytest.mark.parametrize("t,d,n,k,f", [(300, 256, 4, 2, 256), (1100, 512, 8, 2, 512), (37, 256, 8, 1, 256),
+                                       (1, 256, 8, 2, 256), (20, 256, 64, 2, 256), (9, 256, 128, 8, 256)])
 def test_backward_vs_oracle(gemm_ctas, t, d, n, k, f):
     from paper_2509_09121_b200.moe import MoEConfig, MoELayer
     o = Oracle("port")
