@@ -275,10 +275,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     else mbar_wait(&tfill[slot], ph);
     return *reinterpret_cast<volatile int*>(&tile_ring[slot]);
   };
-  auto free_tile = [&](int i) {
+  // `tile` is the value just read from the slot: the arrive is control-dependent on that read, so
+  // a relaxed arrive cannot overtake it (the producer rewrites the slot once every consumer freed it).
+  auto free_tile = [&](int i, int tile) {
     const int slot = i % kTileSlots;
-    if (kCtaGroup == 1 || cta_rank == 0) mbar_arrive(&tfree[slot]);
-    else mbar_arrive_cluster(&tfree[slot], 0);
+    if (tile < 0) return;
+    if (kCtaGroup == 1 || cta_rank == 0) mbar_arrive_relaxed(&tfree[slot]);
+    else mbar_arrive_cluster_relaxed(&tfree[slot], 0);
   };
 
   if (warp == 0) {
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if constexpr (kCtaGroup == 2) mbar_arrive_cluster(&tfill[slot], 1);
         } else {
           tile = take_tile(i, true);
-          free_tile(i);
+          free_tile(i, tile);
         }
         if (tile >= total_tiles || !decode(tile, ti)) break;
         const bool half_t = kCtaGroup == 2 && ti.half;
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       TileInfo ti;
       for (int i = 0;; ++i) {
         const int tile = take_tile(i, false);
-        free_tile(i);
+        free_tile(i, tile);
         if (tile >= total_tiles || !decode(tile, ti)) break;
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0;; ++i) {
       const int tile = take_tile(i, kCtaGroup == 2 && cta_rank != 0);
       __syncwarp();
-      if (lane == 0) free_tile(i);
+      if (lane == 0) free_tile(i, tile);
       if (tile >= total_tiles || !decode(tile, ti)) break;
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
@@ -592,8 +595,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (kCtaGroup == 1) mbar_arrive(&tempty[acc]);
-        else mbar_arrive_cluster(&tempty[acc], 0);
+        // relaxed: the tcgen05 fence above orders the TMEM reads; the tile's global stores need
+        // not be complete before the accumulator is reused
+        if constexpr (kCtaGroup == 1) mbar_arrive_relaxed(&tempty[acc]);
+        else mbar_arrive_cluster_relaxed(&tempty[acc], 0);
       }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
