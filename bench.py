@@ -343,7 +343,7 @@ def run_ours(args, cfg):
     tp = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
-            traffic = json.load(fh).get(f"{T}x{d}x{N}x{K}x{f}") if args.precision == "bf16" else None
+            traffic = json.load(fh).get(f"{T}x{d}x{N}x{K}x{f}" + ("-fp8" if args.precision == "fp8" else ""))
 
     if rank == 0:
         line = dict(
@@ -372,7 +372,7 @@ def run_ours(args, cfg):
                       if (args.precision == "bf16" and T * K >= 256 * nl * 4) else
                       dict(bound="tensor", kernel="grouped GEMM1 + SwiGLU (tcgen05 kind::f8f6f4, e4m3)", achieved=g1_tf,
                            peak=fp8_peak()[0], unit="TFLOP/s", frac=g1_tf / fp8_peak()[0], peak_kind=fp8_peak()[1],
-                           traffic=None, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
+                           traffic=traffic, flop_per_launch=g1_flop, ms_per_launch=per["gemm1"])
                       if T * K >= 256 * nl * 4 else
                       dict(bound="hbm", kernel="grouped GEMM1+GEMM2 weight streaming (tcgen05)",
                            achieved=stream_gbs, peak=peaks["hbm"], unit="GB/s", frac=stream_gbs / peaks["hbm"],
