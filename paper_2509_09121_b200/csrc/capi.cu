@@ -349,8 +349,9 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   }
 
   const int64_t rows = h->cap * h->K;
-  const int tpc = std::min(router_tokens_per_cta(static_cast<int>(h->N), 32),
-                           RouterBigSmem(static_cast<int>(h->N), 32, 3).tpc);  // smallest tile of any variant
+  const int tpc = std::min({router_tokens_per_cta(static_cast<int>(h->N), 32),
+                            RouterBigSmem(static_cast<int>(h->N), 32, 3).tpc,
+                            RouterLatSmem<3, 64>(static_cast<int>(h->N)).tpc});  // smallest tile of any variant
   h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
   RouteBufs& rb = h->rb;
   rb.logits = dalloc<float>(h->cap * h->N);
@@ -381,6 +382,9 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);
@@ -450,20 +454,35 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int N = static_cast<int>(h->N);
   // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
+  // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
   static const int force = [] {
-    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "small" or "big"
-    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : 0) : 0;
+    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "lat", "small" or "big"
+    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : 0) : 0;
   }();
   const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
   const bool big_ok = RouterBigSmem(N, 32, 3).total <= 220 * 1024;
   const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
-  const bool small = !big && router_smem_bytes(N, 32, 8) <= 220 * 1024;
-  const int tpc = big ? tpc_big : router_tokens_per_cta(N, small ? 32 : 128);
+  // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
+  const int N4r = (N + 3) / 4 * 4;
+  const int lat_chunk = N4r <= 16 ? 256 : N4r <= 32 ? 128 : 64;
+  const int tpc_lat = RouterLatSmem<3, 64>(N).tpc;
+  const bool lat = !big && (force == 3 || (force == 0 && (T + tpc_lat - 1) / tpc_lat <= h->num_sms));
+  const bool small = !big && !lat && router_smem_bytes(N, 32, 8) <= 220 * 1024;
+  const int tpc = big ? tpc_big : lat ? tpc_lat : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   prof_begin(h, st);
-  if (big)
+  if (lat && lat_chunk == 256)
+    router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (lat && lat_chunk == 128)
+    router_lat_kernel<3, 128><<<n_tiles, 128, RouterLatSmem<3, 128>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (lat)
+    router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (big)
     router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   else if (small)

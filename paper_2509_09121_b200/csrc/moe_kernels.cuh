@@ -281,6 +281,138 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
 }
 
 // ---------------------------------------------------------------------------------------
+// K1, latency variant (decode-size batches): one thread per (token, expert) chain. A 4096-long
+// fp64 chain costs 4096 x 8.7 cycles of DFMA latency whatever the blocking, so at small T the
+// only lever is parallelism: 128-thread CTAs of (128 / N4) tokens x N4 experts, x and W chunks
+// through a cp.async ring. The x chunk is widened to fp64 once per CTA (not once per expert:
+// F2F runs at 15/clk/SM), then the operands of 32 steps are loaded ahead of their 32 dependent
+// DFMAs. Chunks are 256 steps for N <= 16 (128 / 64 for more experts) so the per-chunk barrier and
+// refill overhead is amortised over a long chain segment. Same ascending-l order per chain.
+template <int kStages, int kChunk>
+struct RouterLatSmem {
+  int tpc, N4;
+  size_t rx, sw, xd, slog, sidx, slse, total;
+  __host__ __device__ RouterLatSmem(int n_experts) {
+    N4 = (n_experts + 3) / 4 * 4;
+    tpc = N4 >= 128 ? 1 : 128 / N4;
+    rx = 0;                                                          // [stages][tpc][chunk] bf16
+    sw = rx + ((size_t)kStages * tpc * kChunk * 2 + 15) / 16 * 16;  // [stages][chunk][N4] fp64
+    xd = sw + (size_t)kStages * sizeof(double) * kChunk * N4;       // [tpc][chunk] fp64
+    slog = xd + sizeof(double) * tpc * kChunk;
+    sidx = slog + sizeof(float) * tpc * N4;
+    slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
+    total = slse + sizeof(double) * tpc;
+  }
+};
+
+template <int kStages, int kChunk>
+__global__ void __launch_bounds__(128) router_lat_kernel(const __nv_bfloat16* __restrict__ x,
+                                                         const double* __restrict__ wr64, int T, int d, int N, int K,
+                                                         RouteBufs rb) {
+  constexpr int kThreads = 128;
+  const RouterLatSmem<kStages, kChunk> L(N);
+  const int N4 = L.N4, tpc = L.tpc;
+  const int tile = blockIdx.x;
+  const int tok0 = tile * tpc;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* rawx = reinterpret_cast<__nv_bfloat16*>(smem_raw + L.rx);
+  double* sw = reinterpret_cast<double*>(smem_raw + L.sw);
+  double* xd = reinterpret_cast<double*>(smem_raw + L.xd);
+  float* slog = reinterpret_cast<float*>(smem_raw + L.slog);
+  int* sidx = reinterpret_cast<int*>(smem_raw + L.sidx);
+  double* slse = reinterpret_cast<double*>(smem_raw + L.slse);
+  const int tl = threadIdx.x / N4;  // token of this chain
+  const int e = threadIdx.x % N4;   // expert of this chain
+  const bool worker = tl < tpc;
+  double acc = 0.0;
+
+  const int nchunks = d / kChunk;
+  const int xpieces = tpc * (kChunk / 8);
+  const int wpieces = kChunk * N4 / 2;
+  auto issue = [&](int c, int buf) {
+    const int c0 = c * kChunk;
+    for (int i = threadIdx.x; i < xpieces; i += kThreads) {
+      const int r = i / (kChunk / 8), q = i % (kChunk / 8);
+      const bool ok = tok0 + r < T;
+      const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
+      cp_async16(rawx + ((size_t)buf * tpc + r) * kChunk + q * 8, src, ok);
+    }
+    const double* wsrc = wr64 + (size_t)c0 * N4;
+    for (int i = threadIdx.x; i < wpieces; i += kThreads)
+      cp_async16(sw + (size_t)buf * kChunk * N4 + i * 2, wsrc + i * 2, true);
+    cp_async_commit();
+  };
+  for (int c = 0; c < kStages - 1; ++c) {
+    if (c < nchunks) issue(c, c);
+    else cp_async_commit();
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c % kStages;
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
+    else cp_async_commit();
+    // widen the chunk's x once for all experts
+    const __nv_bfloat16* rx = rawx + (size_t)buf * tpc * kChunk;
+    for (int i = threadIdx.x * 8; i < tpc * kChunk; i += kThreads * 8) {  // 8 values per thread and pass
+      const int4 raw = *reinterpret_cast<const int4*>(rx + i);
+      const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+      double v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = static_cast<double>(__bfloat162float(hv[j]));
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) *reinterpret_cast<double2*>(xd + i + j) = make_double2(v[j], v[j + 1]);
+    }
+    __syncthreads();
+    if (worker) {
+      // 32 steps' operands are loaded before their 32 dependent DFMAs: one shared-memory round
+      // trip (~30 cycles) per 32 x 8-cycle chain segment. (Interleaving loads with the chain lets
+      // ptxas schedule each load right before its use, exposing the latency on every step.)
+      const double* xr = xd + (size_t)tl * kChunk;
+      const double* wc = sw + (size_t)buf * kChunk * N4 + e;
+      // Register double buffer across a NON-unrolled loop: the loads of block b+1 are issued at
+      // the top of iteration b and consumed only in the next iteration, so ptxas cannot sink
+      // them next to their uses; each 16-step FMA segment (~128 cycles) covers the round trip.
+      constexpr int kB = 16;
+      double xa[kB], wa[kB], xb[kB], wb[kB];
+      auto ld = [&](double (&xv)[kB], double (&w)[kB], int base) {
+#pragma unroll
+        for (int i = 0; i < kB; i += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(xr + base + i);
+          xv[i] = t.x;
+          xv[i + 1] = t.y;
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) w[i] = wc[(base + i) * N4];
+      };
+      ld(xa, wa, 0);
+#pragma unroll 1
+      for (int hb = 0; hb < kChunk; hb += 2 * kB) {
+        ld(xb, wb, hb + kB);
+#pragma unroll
+        for (int i = 0; i < kB; ++i) acc = fma(xa[i], wa[i], acc);
+        if (hb + 2 * kB < kChunk) ld(xa, wa, hb + 2 * kB);
+#pragma unroll
+        for (int i = 0; i < kB; ++i) acc = fma(xb[i], wb[i], acc);
+      }
+    }
+    __syncthreads();  // xd is rewritten by the next chunk
+  }
+  __syncthreads();
+  if (worker) {
+    const int tok = tok0 + tl;
+    const float z = static_cast<float>(acc);
+    slog[tl * N4 + e] = z;
+    if (tok < T && e < N) {
+      rb.logits[(size_t)tok * N + e] = z;
+      if (!isfinite(z)) atomicOr(rb.finite_flag, 1);
+    }
+  }
+  __syncthreads();
+  router_finish(tile, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb, kThreads);
+}
+
+// ---------------------------------------------------------------------------------------
 // K1, large-batch variant: one thread owns 4 tokens x 4 experts (16 independent fp64 chains, each
 // still summed over l in ascending order — bit-identical to the reference gemm_nn). x rows stay
 // raw bf16 in shared memory (16-byte chunks XOR-swizzled by token group so the per-token 16-byte

@@ -1,4 +1,4 @@
-"""Both K1 router variants (small 1x4 with a deep prefetch ring, big 4x4), forced through
+"""Every K1 router variant (lat 1x1 chains, small 1x4 with a deep prefetch ring, big 4x4), forced through
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
 including ragged last tiles and shapes where the automatic choice would pick another variant."""
 import os
@@ -12,8 +12,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("variant", ["small", "big"])
-@pytest.mark.parametrize("t,d,n,k", [(333, 256, 16, 2), (1000, 512, 8, 2), (257, 256, 32, 4), (70, 1024, 4, 1)])
+@pytest.mark.parametrize("variant", ["small", "big", "lat"])
+@pytest.mark.parametrize("t,d,n,k", [(333, 256, 16, 2), (1000, 512, 8, 2), (257, 256, 32, 4), (70, 1024, 4, 1), (5, 256, 128, 8)])
 def test_router_variant_bit_exact(variant, t, d, n, k):
     env = dict(os.environ, CL_MOE_ROUTER=variant, PYTHONPATH=ROOT)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "helpers", "route_check.py"), str(t), str(d), str(n),
