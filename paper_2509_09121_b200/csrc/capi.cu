@@ -597,11 +597,11 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   const int blocks = static_cast<int>((T + 7) / 8);
   if (fp8)
-    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
                                                   tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
                                                   h->inv, h->row_w, h->sx_in);
   else
-    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
                                                    (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
                                                    h->perm, h->inv, h->row_w, nullptr);
   CK(cudaGetLastError());
@@ -743,11 +743,11 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   const int tpc = h->tpc_cur;
   const int blocks = static_cast<int>((T + 7) / 8);
   if (fp8)  // rows quantized with their owner's GEMM1-input scale (global table)
-    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
                                                   h->perm, h->inv, h->row_w, h->sx_in_all);
   else
-    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
                                                    (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
                                                    h->perm, h->inv, h->row_w, nullptr);
   CK(cudaGetLastError());
@@ -832,12 +832,12 @@ void ep_peer_layout(cl_moe* h, cudaStream_t st) {
 void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int blocks = static_cast<int>((T + 7) / 8);
   if (h->precision == CL_MOE_FP8_E4M3)
-    dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
+    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
                                                   (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
                                                   h->xperm, h->perm, h->inv, h->row_w, h->sx_in_all, h->expert_dst,
                                                   h->expert_dst_w);
   else
-    dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
+    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
                                                    (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
                                                    h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
                                                    h->expert_dst_w);
@@ -958,7 +958,7 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   const int N = static_cast<int>(h->N);
   const int tpc = h->tpc_cur;
   const int blocks = static_cast<int>((T + 7) / 8);
-  dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+  dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
                                                  h->inv, h->row_w, nullptr);
   pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, h->n_local, h->poff, h->kb_off);

@@ -1,6 +1,7 @@
 // Router (K1), dispatch plan (K2), fused permute/dispatch (K3) and weighted combine (K6)
 // kernels of the MoE layer. All are memory- or latency-bound; see DESIGN.md for their rooflines.
 #pragma once
+#include <algorithm>
 #include <cuda_fp8.h>
 
 #include "ptx.cuh"
@@ -668,21 +669,25 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     if (expert_dst) {
       char* b = static_cast<char*>(expert_dst[e]);
       dsts[k] = b ? b + (size_t)(r - rb.offsets[e]) * d * kRowElemBytes : nullptr;
-      if (lane == 0 && b) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
+      if (lane == 0 && b && blockIdx.y == 0) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
     } else {
       dsts[k] = static_cast<char*>(xperm) + (size_t)r * d * kRowElemBytes;
     }
     if constexpr (kFp8) sc[k] = act_scale[e];
-    if (lane == 0) {
+    if (lane == 0 && blockIdx.y == 0) {
       inv[s] = r;
       perm[r] = static_cast<int32_t>(s);
       row_w[r] = wts[s];
     }
   }
   const int4* src = reinterpret_cast<const int4*>(x + (size_t)j * d);
-  const int nvec = d / 8;  // 8 bf16 per 16 B
+  // gridDim.y column slices (small batches: more warps in flight than tokens)
+  const int nvec_all = d / 8;  // 8 bf16 per 16 B
+  const int per = (nvec_all + gridDim.y - 1) / gridDim.y;
+  const int vbeg = blockIdx.y * per;
+  const int nvec = min(nvec_all, vbeg + per);
   if constexpr (!kFp8) {
-    for (int v0 = lane; v0 < nvec; v0 += 32 * 4) {
+    for (int v0 = vbeg + lane; v0 < nvec; v0 += 32 * 4) {
       int4 buf[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -696,7 +701,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
       }
     }
   } else {
-    for (int v = lane; v < nvec; v += 32) {
+    for (int v = vbeg + lane; v < nvec; v += 32) {
       const int4 raw = ld_nc_v4(src + v);
       const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
       float f[8];
@@ -743,9 +748,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   float wk[kK];
 #pragma unroll
   for (int k = 0; k < kK; ++k) wk[k] = wts ? wts[(size_t)j * kK + k] : 1.0f;
-  const int nvec = d / 8;
+  const int nvec_all = d / 8;
+  const int per = (nvec_all + gridDim.y - 1) / gridDim.y;  // gridDim.y column slices (small batches)
+  const int vbeg = blockIdx.y * per;
+  const int nvec = min(nvec_all, vbeg + per);
   bool fin = true;
-  for (int v0 = lane; v0 < nvec; v0 += 32 * kU) {
+  for (int v0 = vbeg + lane; v0 < nvec; v0 += 32 * kU) {
     int4 raw[kU][kK];
 #pragma unroll
     for (int u = 0; u < kU; ++u)
@@ -782,10 +790,18 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
   if (!fin) atomicOr(finite_flag, 1);
 }
 
+// Warp-per-token kernels (dispatch, combine): (T/8) x slices CTAs of 8 warps; small batches get
+// up to 8 column slices per token so a few hundred warps are in flight.
+inline dim3 token_grid(int64_t T) {
+  const int blocks = static_cast<int>((T + 7) / 8);
+  const int slices = std::max(1, std::min(8, (4 * 148 + blocks - 1) / blocks));
+  return dim3(blocks, slices);
+}
+
 template <typename OutT>
 inline void launch_combine(const __nv_bfloat16* y, const int32_t* inv, int T, int d, int K, OutT* out, int32_t* flag,
                            cudaStream_t st, const float* wts = nullptr) {
-  const int blocks = (T + 7) / 8;
+  const dim3 blocks = token_grid(T);
   switch (K) {
     case 1: combine_kernel<OutT, 1><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
     case 2: combine_kernel<OutT, 2><<<blocks, 256, 0, st>>>(y, inv, T, d, out, flag, wts); break;
