@@ -2,13 +2,15 @@
 // 128-thread CTAs, thread = (token, expert) chain over L steps; x[tok][l] and w[l][e] in smem.
 #include <cstdio>
 #include <cuda_runtime.h>
-constexpr int N4 = 16, TPC = 8, L = 256;
+constexpr int N4 = 16, TPC = 8, L = 128;
 template <int V>
 __global__ void __launch_bounds__(128) chain(const double* gx, const double* gw, double* out, long long* cyc, int reps) {
   __shared__ double sx[TPC * L];
   __shared__ double sw[L * N4];
+  __shared__ __align__(16) double swT[N4 * (L + 2)];
   for (int i = threadIdx.x; i < TPC * L; i += 128) sx[i] = gx[i];
   for (int i = threadIdx.x; i < L * N4; i += 128) sw[i] = gw[i];
+  for (int i = threadIdx.x; i < L * N4; i += 128) swT[(i % N4) * (L + 2) + i / N4] = gw[i];
   __syncthreads();
   const int tl = threadIdx.x / N4, e = threadIdx.x % N4;
   const double* xr = sx + tl * L;
@@ -27,6 +29,15 @@ __global__ void __launch_bounds__(128) chain(const double* gx, const double* gw,
         for (int i = 0; i < 16; ++i) p[i] = xr[b + i] * wc[(b + i) * N4];
 #pragma unroll
         for (int i = 0; i < 16; ++i) acc += p[i];
+      }
+    } else if (V == 3) {  // expert-major W ([e][l], padded rows), 2 steps per LDS.128 for both operands
+      const double* we = swT + e * (L + 2);
+#pragma unroll 16
+      for (int l = 0; l < L; l += 2) {
+        const double2 xx = *reinterpret_cast<const double2*>(xr + l);
+        const double2 ww = *reinterpret_cast<const double2*>(we + l);
+        acc = fma(xx.x, ww.x, acc);
+        acc = fma(xx.y, ww.y, acc);
       }
     } else {  // registers only: loads once, chain over registers (upper bound)
       double xv[16], wv[16];
@@ -53,6 +64,8 @@ int main() {
   printf("fma chain, smem operands:        %.2f cyc/step\n", (double)h[0] / (reps * L));
   chain<1><<<64, 128>>>(gx, gw, out, cyc, reps); cudaMemcpy(h, cyc, 8 * 64, cudaMemcpyDeviceToHost);
   printf("dmul then dadd chain, smem:      %.2f cyc/step\n", (double)h[0] / (reps * L));
+  chain<3><<<64, 128>>>(gx, gw, out, cyc, reps); cudaMemcpy(h, cyc, 8 * 64, cudaMemcpyDeviceToHost);
+  printf("fma chain, expert-major W, LDS.128: %.2f cyc/step\n", (double)h[0] / (reps * L));
   chain<2><<<64, 128>>>(gx, gw, out, cyc, reps); cudaMemcpy(h, cyc, 8 * 64, cudaMemcpyDeviceToHost);
   printf("fma chain, register operands:    %.2f cyc/step\n", (double)h[0] / (reps * L));
   return 0;
