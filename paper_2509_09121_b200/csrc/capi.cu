@@ -416,11 +416,15 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
 }
 
 // m-tiles per L2-resident group for a row-grouped GEMM whose A rows are k_bytes long (decode_tile).
-int m_group_for(int64_t k_bytes, int bm) {
+int64_t l2_group_budget() {
   static const int64_t budget = [] {
     const char* e = std::getenv("CL_MOE_L2_GROUP_MB");
     return (int64_t)(e ? std::atoi(e) : 32) << 20;
   }();
+  return budget;
+}
+int m_group_for(int64_t k_bytes, int bm) {
+  const int64_t budget = l2_group_budget();
   if (budget <= 0) return 0;
   return static_cast<int>(std::max<int64_t>(1, budget / (k_bytes * bm)));
 }
@@ -431,6 +435,7 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   GemmArgs args = args_in;
   args.tile_counter = h->tile_counter;
   if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
+  if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
   CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((h->num_sms / G) * G);

@@ -56,6 +56,7 @@ struct GemmArgs {
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
   void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
   int32_t m_group;          // row-grouped tile order: m-tiles per group (0 = all), see decode_tile
+  int64_t group_bytes;      // kWgrad tile order: L2 budget of a resident A group (0 = m fastest)
   int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
                             // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
 };
@@ -120,15 +121,26 @@ __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, cons
 }
 
 // K-grouped decode (weight gradients): every expert has m_tiles x n_tiles_n tiles; the K range
-// is the expert's padded row range.
+// is the expert's padded row range, so its operand slabs grow with its row count. m-tiles go in
+// groups whose A slabs fit `group_bytes` of L2 (m fastest inside, sweeping every n-block), as in
+// decode_tile: a hot expert's A slab is then read once instead of once per n-block.
 __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, int bm, TileInfo& ti) {
   const int per = a.m_tiles * a.n_tiles_n;
   if (tile >= a.n_experts * per) return false;
   const int e = tile / per;
   const int local = tile - e * per;
+  const int nkb = a.kb_off[e + 1] - a.kb_off[e];
+  int gm = a.m_tiles;
+  if (a.group_bytes > 0 && nkb > 0) {
+    const int64_t g = a.group_bytes / ((int64_t)bm * nkb * kBKBytes);
+    gm = (int)max((int64_t)1, min((int64_t)a.m_tiles, g));
+  }
+  const int g = local / (gm * a.n_tiles_n);
+  const int within = local - g * gm * a.n_tiles_n;
+  const int gsz = min(gm, a.m_tiles - g * gm);
   ti.e = e;
-  ti.nt = local / a.m_tiles;
-  ti.mt = local - ti.nt * a.m_tiles;
+  ti.nt = within / gsz;
+  ti.mt = g * gm + (within - ti.nt * gsz);
   ti.a_row = ti.mt * bm;
   ti.b_row = ti.nt * kBN;
   ti.row_end = 1 << 30;
