@@ -4,6 +4,10 @@
 // -> CL_ERR_CONFIG, anything else (CUDA error, non-finite output, invalid runtime input)
 // -> CL_ERR_RUN, message kept on the handle. No CPU fallback exists: without a usable sm_100
 // device every entry point fails with CL_ERR_RUN.
+//
+// This file holds the extern "C" entry points; the orchestration they call is in host_handle.cuh
+// (handle state), host_forward.cuh (single-GPU forward), host_ep.cuh (expert parallelism) and
+// host_train.cuh (training), included below into this one translation unit.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -27,1151 +31,11 @@
 
 using namespace cmoe;
 
-namespace {
+#include "host_handle.cuh"
+#include "host_forward.cuh"
+#include "host_ep.cuh"
+#include "host_train.cuh"
 
-struct ConfigErr : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct RunErr : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-std::string fmt(const char* f, ...) {
-  char buf[1024];
-  va_list ap;
-  va_start(ap, f);
-  vsnprintf(buf, sizeof(buf), f, ap);
-  va_end(ap);
-  return buf;
-}
-
-#define CK(x)                                                                                \
-  do {                                                                                       \
-    cudaError_t e_ = (x);                                                                    \
-    if (e_ != cudaSuccess) throw RunErr(fmt("%s failed: %s", #x, cudaGetErrorString(e_)));  \
-  } while (0)
-
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-  static EncodeFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !p) throw RunErr("cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<EncodeFn>(p);
-  }
-  return fn;
-}
-
-// 2D row-major tensor [rows][inner] with a 128-byte-swizzled box of [box_rows][128 bytes].
-CUtensorMap make_map(const void* base, bool fp8, uint64_t inner, uint64_t rows, uint32_t box_rows) {
-  CUtensorMap m;
-  const uint32_t esz = fp8 ? 1 : 2;
-  cuuint64_t dims[2] = {inner, rows};
-  cuuint64_t strides[1] = {inner * esz};
-  cuuint32_t box[2] = {128u / esz, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                           const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw RunErr(fmt("cuTensorMapEncodeTiled failed (%d)", (int)r));
-  return m;
-}
-
-template <typename T>
-T* dalloc(size_t n) {
-  void* p = nullptr;
-  if (n == 0) n = 1;
-  CK(cudaMalloc(&p, n * sizeof(T)));
-  return static_cast<T*>(p);
-}
-
-int grid_for(int64_t n, int threads = 256) {
-  return static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 148 * 32));
-}
-
-}  // namespace
-
-struct cl_moe {
-  cl_moe_config cfg{};
-  int64_t d = 0, N = 0, K = 0, f = 0, cap = 0;
-  int n_local = 0, e0 = 0;
-  int gemm_ctas = 2;
-  bool gemm_auto = true;               // pick cta_group per call from the rows per expert
-  int num_sms = 148;
-  int precision = CL_MOE_BF16;
-  std::string last_error;
-
-  // weights
-  float* wr = nullptr;                 // [d][N] fp32
-  double* wr64 = nullptr;              // [d][N4] fp64 copy streamed by the router
-  __nv_bfloat16* win = nullptr;        // [n_local][2f][d] packed
-  __nv_bfloat16* wout = nullptr;       // [n_local][d][f] packed
-  uint8_t* win8 = nullptr;             // e4m3 copies
-  uint8_t* wout8 = nullptr;
-  float* ws_in = nullptr;              // [n_local][2f]
-  float* ws_out = nullptr;             // [n_local][d]
-  float* sx_in = nullptr;              // [n_local]
-  float* sx_in_all = nullptr;          // [N] GEMM1-input scales of every expert (EP: the source
-                                       //     quantizes a row with its owner's scale)
-  float* calib_all = nullptr;          // [N] EP calibration: source-side max |x| per global expert
-  float* sx_mid = nullptr;             // [n_local]
-  float* calib = nullptr;              // [2][n_local] running maxima
-  float* calib_ch = nullptr;           // [d] per-channel max |hidden| over calibration tokens
-  long long* calib_counts = nullptr;   // [N] routing counts over calibration tokens
-  float* smooth = nullptr;             // [d] scratch for fold_smoothing
-  bool fp8_ready = false;
-
-  // workspaces
-  RouteBufs rb{};
-  int n_tiles_cap = 0;
-  void* xperm = nullptr;               // [cap*K][d] (bf16 or e4m3)
-  void* act = nullptr;                 // [cap*K][f]
-  __nv_bfloat16* y = nullptr;          // [cap*K][d]
-  int32_t* perm = nullptr;
-  int32_t* inv = nullptr;
-  float* row_w = nullptr;
-  // host-buffer entry points: two pipeline slots so the H2D of call i+1 and the D2H of call i-1
-  // overlap the layer compute of call i (separate copy streams, event-ordered).
-  struct HostSlot {
-    void* x = nullptr;       // bf16 [cap][d]
-    float* xf = nullptr;     // fp32 staging [cap][d] (fp32 io only)
-    void* out = nullptr;     // [cap][d] bf16 or fp32
-    cudaEvent_t h2d = nullptr, done = nullptr, d2h = nullptr;
-    bool used = false;
-  } slot[2];
-  int next_slot = 0;
-  void* io_out = nullptr;              // calibration output scratch
-  cudaStream_t own_stream = nullptr;   // compute stream of the host-buffer path
-  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
-  int64_t last_rows = 0;
-  int tpc_cur = 32;                    // router tile (tokens) of the last routing call
-  int64_t last_tokens = 0;             // T of the current call
-
-  // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
-  bool prof = false;
-  std::vector<std::vector<cudaEvent_t>> prof_sets;
-  std::vector<int> prof_kind;          // 0 forward (6 stages), 1 backward (7 stages)
-  size_t prof_used = 0;
-  std::vector<cudaEvent_t>* cur_ev = nullptr;
-
-  // expert parallelism (ep.cuh)
-  NcclApi::Comm comm = nullptr;
-  int64_t recv_cap = 0;                 // receive-buffer rows (worst case: every rank's every slot)
-  __nv_bfloat16* x_recv = nullptr;      // [recv_cap][d]
-  __nv_bfloat16* act_recv = nullptr;    // [recv_cap][f]
-  __nv_bfloat16* y_recv = nullptr;      // [recv_cap][d]
-  int32_t* ep_counts_dev = nullptr;     // [R][N] all-gathered counts
-  int32_t* ep_off_dev = nullptr;        // [NL+1] local expert offsets in the receive buffer
-  int32_t* ep_counts_host = nullptr;    // pinned mirrors
-  int32_t* ep_off_host = nullptr;
-  std::vector<int64_t> ep_C, ep_piece, ep_myoff;  // exchange layout of the last EP forward
-  __nv_bfloat16* dYsrc = nullptr;       // EP training: source-order dY [cap*K][d]
-  __nv_bfloat16* dXsrc = nullptr;       // EP training: source-order dX [cap*K][d]
-  CUtensorMap mA1e[2], mA2e[2];
-  CUtensorMap mA1eq[2], mA2eq[2];       // e4m3 views of x_recv / act_recv
-  bool maps_eq = false;
-  // peer-memory (NVLink) transport (ep.cuh): 0 = NCCL send/recv, 1 = direct peer stores
-  int ep_transport = 0;
-  char** peer_x_dev = nullptr;          // [R] every rank's x_recv, as mapped in this process
-  char** peer_y_dev = nullptr;          // [R] every rank's y (source-order return buffer)
-  float** peer_w_dev = nullptr;         // [R] every rank's w_recv
-  float* w_recv = nullptr;              // [recv_cap] combine weight of each received row
-  void** expert_dst = nullptr;          // [N] dispatch destinations of this rank's pieces
-  float** expert_dst_w = nullptr;       // [N] ... of their combine weights
-  void** row_ptr = nullptr;             // [recv_cap] return address of every received row
-  char** peer_dy_dev = nullptr;         // [R] every rank's dYbuf (training: dY rows to the owners)
-  char** peer_dx_dev = nullptr;         // [R] every rank's dXsrc (training: dX rows back)
-  void** expert_dst_dy = nullptr;       // [N] this rank's dY pieces in the owners' dYbuf
-  void** row_ptr_dx = nullptr;          // [recv_cap] source address of every received row's dX
-  bool ep_group = false;                // member of a single-process EP group (cl_moe_ep_group_*)
-  float* bar_buf = nullptr;             // [1] payload of the exchange barriers
-  std::vector<void*> ipc_opened;        // peers' buffers mapped through CUDA IPC
-
-  // training (expert-FFN backward)
-  bool train_ready = false;
-  int64_t train_T = 0;                  // T of the last cl_moe_forward_train
-  const void* cur_x = nullptr;          // hidden of the last cl_moe_forward_train (caller-owned)
-  int64_t rp_cap = 0;                   // padded-row capacity of the transposes
-  __nv_bfloat16* win_ref = nullptr;     // [NL][d][2f] reference layout (dgrad-2 B operand)
-  __nv_bfloat16* wout_ref = nullptr;    // [NL][f][d]  reference layout (dgrad-1 B operand)
-  __nv_bfloat16* Hbuf = nullptr;        // [cap*K][2f] pre-activations [G | U]
-  __nv_bfloat16* dYbuf = nullptr;       // [cap*K][d]
-  __nv_bfloat16* dHbuf = nullptr;       // [cap*K][2f]
-  __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
-  __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;  // [C][rp_cap]
-  int32_t* poff = nullptr;              // [NL+1]
-  int* tile_counter = nullptr;          // grouped-GEMM dynamic tile scheduler
-  float* rdz = nullptr;                 // router backward: dz [cap][N] fp32
-  float* rpart = nullptr;               // dW_r partials [chunks][d][N]
-  float* dcw_scratch = nullptr;         // d(combine weights) [cap][K] when the caller does not want them
-  int32_t* kb_off = nullptr;            // [NL+1]
-  CUtensorMap mAdg1[2], mBdg1[2], mAdg2[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
-
-  CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
-  CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
-  bool maps_q = false;
-
-  ~cl_moe() {
-    void* ptrs[] = {sx_in_all, calib_all, calib_counts, calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
-                    sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
-                    inv,    row_w,   slot[0].x, slot[0].xf, slot[0].out, slot[1].x, slot[1].xf, slot[1].out,
-                    io_out, rb.logits,    rb.probs,
-                    rb.topk_idx, rb.combine_w, rb.local_rank, rb.tile_cnt, rb.tile_psum, rb.tile_lse2,
-                    rb.counts, rb.offsets, rb.agg_prob, rb.losses, rb.finite_flag};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
-    for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
-                    (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
-                    (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
-                    (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
-                    (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
-                    (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
-                    (void*)row_ptr_dx})
-      if (p) cudaFree(p);
-    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
-    if (ep_counts_host) cudaFreeHost(ep_counts_host);
-    if (ep_off_host) cudaFreeHost(ep_off_host);
-    if (comm) NcclApi::get().CommDestroy(comm);
-    if (own_stream) cudaStreamDestroy(own_stream);
-    if (s_h2d) cudaStreamDestroy(s_h2d);
-    if (s_d2h) cudaStreamDestroy(s_d2h);
-    for (auto& sl : slot)
-      for (cudaEvent_t e : {sl.h2d, sl.done, sl.d2h})
-        if (e) cudaEventDestroy(e);
-    for (auto& v : prof_sets)
-      for (auto e : v) cudaEventDestroy(e);
-  }
-};
-
-namespace {
-
-template <typename Fn>
-cl_status guarded(cl_moe* h, Fn fn) {
-  if (!h) return CL_ERR_CONFIG;
-  try {
-    h->last_error.clear();
-    fn();
-    return CL_OK;
-  } catch (const ConfigErr& e) {
-    h->last_error = e.what();
-    return CL_ERR_CONFIG;
-  } catch (const std::exception& e) {
-    h->last_error = e.what();
-    return CL_ERR_RUN;
-  }
-}
-
-constexpr int kStages = 6;     // forward: router, plan, dispatch, gemm1, gemm2, combine
-constexpr int kBwdStages = 7;  // backward: combine-bwd, dgrad1, dgrad2, dispatch-bwd, transposes, wgrad-out, wgrad-in
-
-void prof_begin(cl_moe* h, cudaStream_t st, int kind = 0) {
-  h->cur_ev = nullptr;
-  if (!h->prof) return;
-  if (h->prof_used == h->prof_sets.size()) {
-    std::vector<cudaEvent_t> v(kBwdStages + 1);
-    for (auto& e : v) CK(cudaEventCreate(&e));
-    h->prof_sets.push_back(v);
-    h->prof_kind.push_back(0);
-  }
-  h->prof_kind[h->prof_used] = kind;
-  h->cur_ev = &h->prof_sets[h->prof_used++];
-  CK(cudaEventRecord((*h->cur_ev)[0], st));
-}
-void prof_mark(cl_moe* h, int stage, cudaStream_t st) {
-  if (h->cur_ev) CK(cudaEventRecord((*h->cur_ev)[stage + 1], st));
-}
-
-void validate(const cl_moe_config* c) {
-  if (!c) throw ConfigErr("config is null");
-  if (c->d_model <= 0 || c->d_model % 256) throw ConfigErr(fmt("d_model=%lld must be a positive multiple of 256", (long long)c->d_model));
-  if (c->d_ff <= 0 || c->d_ff % 128) throw ConfigErr(fmt("d_ff=%lld must be a positive multiple of 128", (long long)c->d_ff));
-  if (c->n_experts < 1 || c->n_experts > 128) throw ConfigErr(fmt("n_experts=%lld outside [1, 128]", (long long)c->n_experts));
-  if (c->top_k < 1 || c->top_k > c->n_experts || c->top_k > 8)
-    throw ConfigErr(fmt("top_k=%lld outside [1, min(N, 8)]", (long long)c->top_k));
-  if (c->max_tokens < 1 || c->max_tokens * c->top_k > (int64_t(1) << 30)) throw ConfigErr("max_tokens out of range");
-  const int ep = c->ep_size <= 0 ? 1 : c->ep_size;
-  if (c->n_experts % ep) throw ConfigErr("n_experts must be divisible by ep_size");
-  if (c->ep_rank < 0 || c->ep_rank >= ep) throw ConfigErr("ep_rank out of range");
-  if (c->gemm_ctas < 0 || c->gemm_ctas > 2) throw ConfigErr("gemm_ctas must be 0, 1 or 2");
-}
-
-void build_maps(cl_moe* h, bool fp8) {
-  const uint64_t rows = static_cast<uint64_t>(h->cap * h->K);
-  for (int v = 0; v < 2; ++v) {
-    const uint32_t brow = v == 0 ? 256 : 128;
-    if (!fp8) {
-      h->mA1[v] = make_map(h->xperm, false, h->d, rows, 128);
-      h->mB1[v] = make_map(h->win, false, h->d, (uint64_t)h->n_local * 2 * h->f, brow);
-      h->mA2[v] = make_map(h->act, false, h->f, rows, 128);
-      h->mB2[v] = make_map(h->wout, false, h->f, (uint64_t)h->n_local * h->d, brow);
-    } else {
-      h->mA1q[v] = make_map(h->xperm, true, h->d, rows, 128);
-      h->mB1q[v] = make_map(h->win8, true, h->d, (uint64_t)h->n_local * 2 * h->f, brow);
-      h->mA2q[v] = make_map(h->act, true, h->f, rows, 128);
-      h->mB2q[v] = make_map(h->wout8, true, h->f, (uint64_t)h->n_local * h->d, brow);
-    }
-  }
-}
-
-void init_handle(cl_moe* h, const cl_moe_config* c) {
-  validate(c);
-  h->cfg = *c;
-  h->d = c->d_model;
-  h->N = c->n_experts;
-  h->K = c->top_k;
-  h->f = c->d_ff;
-  h->cap = c->max_tokens;
-  const int ep = c->ep_size <= 0 ? 1 : c->ep_size;
-  h->n_local = static_cast<int>(h->N / ep);
-  h->e0 = c->ep_rank * h->n_local;
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RunErr("no CUDA device available (the MoE path has no CPU fallback)");
-  CK(cudaSetDevice(c->device));
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, c->device));
-  if (prop.major != 10) throw RunErr(fmt("device %d is sm_%d%d; this library is built for sm_100a only", c->device, prop.major, prop.minor));
-  h->num_sms = prop.multiProcessorCount;
-  h->gemm_auto = c->gemm_ctas == 0;
-  h->gemm_ctas = c->gemm_ctas == 0 ? 2 : c->gemm_ctas;
-  CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
-  for (auto& sl : h->slot) {
-    CK(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
-  }
-
-  const int64_t rows = h->cap * h->K;
-  const int tpc = std::min({router_tokens_per_cta(static_cast<int>(h->N), 32),
-                            RouterBigSmem(static_cast<int>(h->N), 32, 3).tpc,
-                            RouterLatSmem<3, 64>(static_cast<int>(h->N)).tpc});  // smallest tile of any variant
-  h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
-  RouteBufs& rb = h->rb;
-  rb.logits = dalloc<float>(h->cap * h->N);
-  rb.probs = dalloc<float>(h->cap * h->N);
-  rb.topk_idx = dalloc<int32_t>(rows);
-  rb.combine_w = dalloc<float>(rows);
-  rb.local_rank = dalloc<int32_t>(rows);
-  rb.tile_cnt = dalloc<int32_t>((size_t)h->n_tiles_cap * h->N);
-  rb.tile_psum = dalloc<double>((size_t)h->n_tiles_cap * h->N);
-  rb.tile_lse2 = dalloc<double>(h->n_tiles_cap);
-  rb.counts = dalloc<int32_t>(h->N);
-  rb.offsets = dalloc<int32_t>(h->N + 1);
-  rb.agg_prob = dalloc<float>(h->N);
-  rb.losses = dalloc<float>(2);
-  rb.finite_flag = dalloc<int32_t>(1);
-  CK(cudaMemset(rb.finite_flag, 0, sizeof(int32_t)));
-  CK(cudaMemset(rb.offsets, 0, sizeof(int32_t) * (h->N + 1)));
-
-  h->xperm = dalloc<__nv_bfloat16>(rows * h->d);
-  h->act = dalloc<__nv_bfloat16>(rows * h->f);
-  h->y = dalloc<__nv_bfloat16>(rows * h->d);
-  h->perm = dalloc<int32_t>(rows);
-  h->inv = dalloc<int32_t>(rows);
-  h->row_w = dalloc<float>(rows);
-
-  h->wr = dalloc<float>(h->d * h->N);
-  h->wr64 = dalloc<double>(h->d * ((h->N + 3) / 4 * 4));
-  CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
-  h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
-  h->sx_in = dalloc<float>(h->n_local);
-  h->sx_in_all = dalloc<float>(h->N);
-  h->calib_all = dalloc<float>(h->N);
-  CK(cudaMemset(h->calib_all, 0, sizeof(float) * h->N));
-  h->sx_mid = dalloc<float>(h->n_local);
-  h->calib = dalloc<float>(2 * h->n_local);
-  CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
-  h->calib_ch = dalloc<float>(h->d);
-  CK(cudaMemset(h->calib_ch, 0, sizeof(float) * h->d));
-  h->calib_counts = dalloc<long long>(h->N);
-  CK(cudaMemset(h->calib_counts, 0, sizeof(long long) * h->N));
-  h->smooth = dalloc<float>(h->d);
-
-  using namespace cmoe;
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU_BWD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU_BWD, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_WGRAD, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_WGRAD, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-  CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
-}
-
-// m-tiles per L2-resident group for a row-grouped GEMM whose A rows are k_bytes long (decode_tile).
-int64_t l2_group_budget() {
-  static const int64_t budget = [] {
-    const char* e = std::getenv("CL_MOE_L2_GROUP_MB");
-    return (int64_t)(e ? std::atoi(e) : 32) << 20;
-  }();
-  return budget;
-}
-int m_group_for(int64_t k_bytes, int bm) {
-  const int64_t budget = l2_group_budget();
-  if (budget <= 0) return 0;
-  return static_cast<int>(std::max<int64_t>(1, budget / (k_bytes * bm)));
-}
-
-template <int G, int EPI, bool F8, bool OF8, bool WG = false>
-void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st) {
-  if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
-  GemmArgs args = args_in;
-  args.tile_counter = h->tile_counter;
-  if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
-  if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
-  CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((h->num_sms / G) * G);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = GemmCfg<G>::kSmem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = G;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG>, a, b, args));
-}
-
-// route_tokens on device: K1 + K2.
-void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
-  if (T < 1) throw RunErr("route_tokens: B must be >= 1");
-  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
-  const int N = static_cast<int>(h->N);
-  // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
-  // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
-  // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
-  static const int force = [] {
-    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "lat", "small" or "big"
-    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : 0) : 0;
-  }();
-  const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
-  const bool big_ok = RouterBigSmem(N, 32, 3).total <= 220 * 1024;
-  const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
-  // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
-  const int N4r = (N + 3) / 4 * 4;
-  const int lat_chunk = N4r <= 16 ? 256 : N4r <= 32 ? 128 : 64;
-  const int tpc_lat = RouterLatSmem<3, 64>(N).tpc;
-  const bool lat = !big && (force == 3 || (force == 0 && (T + tpc_lat - 1) / tpc_lat <= h->num_sms));
-  const bool small = !big && !lat && router_smem_bytes(N, 32, 8) <= 220 * 1024;
-  const int tpc = big ? tpc_big : lat ? tpc_lat : router_tokens_per_cta(N, small ? 32 : 128);
-  h->tpc_cur = tpc;
-  h->last_tokens = T;
-  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
-  prof_begin(h, st);
-  if (lat && lat_chunk == 256)
-    router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (lat && lat_chunk == 128)
-    router_lat_kernel<3, 128><<<n_tiles, 128, RouterLatSmem<3, 128>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (lat)
-    router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (big)
-    router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (small)
-    router_kernel<32, 8><<<n_tiles, 32, router_smem_bytes(N, 32, 8), st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else
-    router_kernel<128, 3><<<n_tiles, 128, router_smem_bytes(N, 128, 3), st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  CK(cudaGetLastError());
-  prof_mark(h, 0, st);
-  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
-  CK(cudaGetLastError());
-  prof_mark(h, 1, st);
-}
-
-void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T, cudaStream_t st) {
-  if (T < 1) throw RunErr("moe_forward: B must be >= 1");
-  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
-  const int N = static_cast<int>(h->N);
-  const int tpc = router_tokens_per_cta(N, 128);
-  h->tpc_cur = tpc;
-  h->last_tokens = T;
-  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
-  CK(cudaMemcpyAsync(h->rb.topk_idx, idx, sizeof(int32_t) * T * h->K, cudaMemcpyDeviceToDevice, st));
-  CK(cudaMemcpyAsync(h->rb.combine_w, w, sizeof(float) * T * h->K, cudaMemcpyDeviceToDevice, st));
-  prof_begin(h, st);
-  decision_tiles_kernel<<<n_tiles, 128, 0, st>>>(h->rb.topk_idx, (int)T, N, (int)h->K, tpc, h->rb);
-  CK(cudaGetLastError());
-  prof_mark(h, 0, st);
-  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
-  CK(cudaGetLastError());
-  prof_mark(h, 1, st);
-}
-
-// GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
-void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
-               const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
-               cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr) {
-  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
-  GemmArgs g1{};
-  g1.offsets = offsets;
-  if (h->gemm_auto) {
-    // M=256 CTA-pair tiles pay off only when experts have enough rows; small batches (decode)
-    // stream weights and are better served by M=128 tiles (less A over-fetch per B byte).
-    const int64_t rows_per_expert = h->last_tokens * h->K * (h->cfg.ep_size > 1 ? h->cfg.ep_size : 1) / h->n_local;
-    h->gemm_ctas = rows_per_expert >= 1024 ? 2 : 1;
-  }
-  g1.n_experts = h->n_local;
-  g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
-  g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
-  g1.b_rows_per_expert = static_cast<int>(2 * h->f);
-  g1.out = act;
-  g1.ldo = static_cast<int>(h->f);
-  g1.act_scale = h->sx_in;
-  g1.w_scale = h->ws_in;
-  g1.out_scale = h->sx_mid;
-  g1.aux = h_save;
-  g1.ffn = static_cast<int>(h->f);
-  if (h_save) {  // training: also write A^T into the padded K-major buffer of the dW_out GEMM
-    g1.aux_t = h->AT;
-    g1.rp = h->rp_cap;
-    g1.poff = h->poff;
-  }
-  GemmArgs g2{};
-  g2.offsets = offsets;
-  g2.n_experts = h->n_local;
-  g2.n_tiles_n = static_cast<int>(h->d / kBN);
-  g2.num_kb = static_cast<int>(h->f * (fp8 ? 1 : 2) / kBKBytes);
-  g2.b_rows_per_expert = static_cast<int>(h->d);
-  g2.out = y;
-  g2.ldo = static_cast<int>(h->d);
-  g2.row_scale = row_w;
-  g2.row_ptr = row_ptr;
-  g1.half_tail = g2.half_tail = 1;  // 2-CTA: tail m-tiles of <= 128 rows as M=128 pair MMAs
-  g2.act_scale = h->sx_mid;
-  g2.w_scale = h->ws_out;
-  const int v = h->gemm_ctas == 2 ? 1 : 0;
-  if (!fp8) {
-    if (v) {
-      launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<2, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
-    } else {
-      launch_gemm<1, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<1, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
-    }
-  } else {
-    if (v) {
-      launch_gemm<2, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<2, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
-    } else {
-      launch_gemm<1, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
-      prof_mark(h, 3, st);
-      launch_gemm<1, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
-    }
-  }
-}
-
-// dispatch + expert FFN + combine (local experts; ep_size == 1).
-void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train = false);
-
-void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
-  if (h->comm) {  // expert parallel (one rank: loopback through the same exchange code)
-    run_ep(h, x, T, out, out_f32, st);
-    return;
-  }
-  if (h->cfg.ep_size > 1) throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_forward)");
-  const int N = static_cast<int>(h->N);
-  const int tpc = h->tpc_cur;
-  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
-  const int blocks = static_cast<int>((T + 7) / 8);
-  if (fp8)
-    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
-                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
-                                                  h->inv, h->row_w, h->sx_in);
-  else
-    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
-                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
-                                                   h->perm, h->inv, h->row_w, nullptr);
-  CK(cudaGetLastError());
-  prof_mark(h, 2, st);
-
-  run_gemms(h, h->rb.offsets, h->act, h->y, h->row_w, h->mA1, h->mA2, h->mA1q, h->mA2q, st);
-  prof_mark(h, 4, st);
-  if (out_f32)
-    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
-  else
-    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
-                                  h->rb.finite_flag, st);
-  CK(cudaGetLastError());
-  prof_mark(h, 5, st);
-  h->cur_ev = nullptr;
-  h->last_rows = T * h->K;
-}
-
-void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_t st) {
-  if (!o) return;
-  const int64_t N = h->N, K = h->K;
-  if (o->logits) CK(cudaMemcpyAsync(o->logits, h->rb.logits, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
-  if (o->probs) CK(cudaMemcpyAsync(o->probs, h->rb.probs, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
-  if (o->topk_idx) CK(cudaMemcpyAsync(o->topk_idx, h->rb.topk_idx, sizeof(int32_t) * T * K, cudaMemcpyDeviceToDevice, st));
-  if (o->combine_weights)
-    CK(cudaMemcpyAsync(o->combine_weights, h->rb.combine_w, sizeof(float) * T * K, cudaMemcpyDeviceToDevice, st));
-  if (o->counts) {
-    i32_to_i64_kernel<<<(int)((N + 127) / 128), 128, 0, st>>>(h->rb.counts, (int)N, o->counts);
-    CK(cudaGetLastError());
-  }
-  if (o->agg_prob) CK(cudaMemcpyAsync(o->agg_prob, h->rb.agg_prob, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
-  if (o->aux_loss) CK(cudaMemcpyAsync(o->aux_loss, h->rb.losses, sizeof(float), cudaMemcpyDeviceToDevice, st));
-  if (o->z_loss) CK(cudaMemcpyAsync(o->z_loss, h->rb.losses + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
-}
-
-void ensure_fp8_storage(cl_moe* h) {
-  if (h->win8) return;
-  h->win8 = dalloc<uint8_t>((size_t)h->n_local * 2 * h->f * h->d);
-  h->wout8 = dalloc<uint8_t>((size_t)h->n_local * h->d * h->f);
-  h->ws_in = dalloc<float>((size_t)h->n_local * 2 * h->f);
-  h->ws_out = dalloc<float>((size_t)h->n_local * h->d);
-  build_maps(h, true);
-}
-
-void ep_fp8_maps(cl_moe* h) {
-  if (h->maps_eq) return;
-  for (int v = 0; v < 2; ++v) {
-    h->mA1eq[v] = make_map(h->x_recv, true, h->d, h->recv_cap, 128);
-    h->mA2eq[v] = make_map(h->act_recv, true, h->f, h->recv_cap, 128);
-  }
-  h->maps_eq = true;
-}
-
-void ep_alloc(cl_moe* h) {
-  if (h->x_recv) return;
-  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
-  h->recv_cap = h->cap * h->K * R;
-  h->x_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
-  h->act_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->f);
-  h->y_recv = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
-  h->ep_counts_dev = dalloc<int32_t>((size_t)R * h->N);
-  h->ep_off_dev = dalloc<int32_t>(h->n_local + 1);
-  CK(cudaMallocHost(&h->ep_counts_host, sizeof(int32_t) * R * h->N));
-  CK(cudaMallocHost(&h->ep_off_host, sizeof(int32_t) * (h->n_local + 1)));
-  for (int v = 0; v < 2; ++v) {
-    h->mA1e[v] = make_map(h->x_recv, false, h->d, h->recv_cap, 128);
-    h->mA2e[v] = make_map(h->act_recv, false, h->f, h->recv_cap, 128);
-  }
-}
-
-#define NCK(x)                                                                               \
-  do {                                                                                       \
-    int r_ = (x);                                                                            \
-    if (r_ != 0) throw RunErr(fmt("%s failed: %s", #x, NcclApi::get().GetErrorString(r_))); \
-  } while (0)
-
-// One direction of the expert-parallel row exchange (layout of the last EP forward).
-// to_experts: rows of this rank's source permutation `src` (piece g at my_off[g]) go to the
-// owner of expert g, landing at its (local expert, source) slot of `dst`; otherwise the reverse.
-void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStream_t st, size_t row_b = 0) {
-  NcclApi& nc = NcclApi::get();
-  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
-  const int rank = h->cfg.ep_rank;
-  const int N = static_cast<int>(h->N), NL = h->n_local;
-  if (row_b == 0) row_b = static_cast<size_t>(h->d) * 2;
-  const auto& C = h->ep_C;
-  const auto& piece = h->ep_piece;
-  const auto& my_off = h->ep_myoff;
-  const uint8_t* s8 = static_cast<const uint8_t*>(src);
-  uint8_t* d8 = static_cast<uint8_t*>(dst);
-  NCK(nc.GroupStart());
-  if (to_experts) {
-    for (int r = 0; r < R; ++r)
-      for (int e = 0; e < NL; ++e) {
-        const int g = r * NL + e;
-        const int64_t n = C[(size_t)rank * N + g];
-        if (n) NCK(nc.Send(s8 + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
-      }
-    for (int e = 0; e < NL; ++e)
-      for (int sr = 0; sr < R; ++sr) {
-        const int64_t n = C[(size_t)sr * N + rank * NL + e];
-        if (n) NCK(nc.Recv(d8 + piece[(size_t)e * R + sr] * row_b, n * row_b, NcclApi::kUint8, sr, h->comm, st));
-      }
-  } else {
-    for (int e = 0; e < NL; ++e)
-      for (int sr = 0; sr < R; ++sr) {
-        const int64_t n = C[(size_t)sr * N + rank * NL + e];
-        if (n) NCK(nc.Send(s8 + piece[(size_t)e * R + sr] * row_b, n * row_b, NcclApi::kUint8, sr, h->comm, st));
-      }
-    for (int r = 0; r < R; ++r)
-      for (int e = 0; e < NL; ++e) {
-        const int g = r * NL + e;
-        const int64_t n = C[(size_t)rank * N + g];
-        if (n) NCK(nc.Recv(d8 + my_off[g] * row_b, n * row_b, NcclApi::kUint8, r, h->comm, st));
-      }
-  }
-  NCK(nc.GroupEnd());
-}
-
-// Expert-parallel forward (ep.cuh): route + plan + dispatch over all N experts, counts
-// all-gather, (expert, source)-piece exchange, local grouped GEMMs, reverse exchange, weighted
-// combine. Requires cl_moe_ep_init. bf16 only in this round. `train` keeps H / A^T on the expert
-// side for cl_moe_backward.
-void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train);
-
-void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
-  if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
-  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
-  if (fp8 && train) throw ConfigErr("training runs in bf16 (set_precision(BF16) first)");
-  if (fp8) ep_fp8_maps(h);
-  if (h->ep_transport == 1) {
-    run_ep_peer(h, x, T, out, out_f32, st, train);
-    return;
-  }
-  NcclApi& nc = NcclApi::get();
-  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
-  const int rank = h->cfg.ep_rank;
-  const int N = static_cast<int>(h->N), NL = h->n_local;
-  const int tpc = h->tpc_cur;
-  const int blocks = static_cast<int>((T + 7) / 8);
-  if (fp8)  // rows quantized with their owner's GEMM1-input scale (global table)
-    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
-                                                  (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
-                                                  h->perm, h->inv, h->row_w, h->sx_in_all);
-  else
-    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
-                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
-                                                   h->perm, h->inv, h->row_w, nullptr);
-  CK(cudaGetLastError());
-  prof_mark(h, 2, st);
-  // ---- counts exchange ----
-  NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)N, NcclApi::kInt32, h->comm, st));
-  CK(cudaMemcpyAsync(h->ep_counts_host, h->ep_counts_dev, sizeof(int32_t) * R * N, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  h->ep_C.assign((size_t)R * N, 0);
-  h->ep_piece.assign((size_t)NL * R, 0);
-  h->ep_myoff.assign((size_t)N + 1, 0);
-  std::vector<int64_t> loc(NL + 1);
-  for (size_t i = 0; i < h->ep_C.size(); ++i) h->ep_C[i] = h->ep_counts_host[i];
-  const int64_t total = ep_layout(h->ep_C.data(), R, N, rank, loc.data(), h->ep_piece.data());
-  if (total > h->recv_cap) throw RunErr("expert-parallel receive buffer overflow");
-  for (int g = 0; g < N; ++g) h->ep_myoff[g + 1] = h->ep_myoff[g] + h->ep_C[(size_t)rank * N + g];
-  for (int e = 0; e <= NL; ++e) h->ep_off_host[e] = static_cast<int32_t>(loc[e]);
-  CK(cudaMemcpyAsync(h->ep_off_dev, h->ep_off_host, sizeof(int32_t) * (NL + 1), cudaMemcpyHostToDevice, st));
-  // ---- dispatch exchange: piece (dest r, expert g) -> r's (local expert, source) slot ----
-  ep_exchange(h, h->xperm, h->x_recv, true, st, (size_t)h->d * (fp8 ? 1 : 2));
-  // ---- local experts ----
-  if (train) {
-    pad_plan_kernel<<<1, 32, 0, st>>>(h->ep_off_dev, NL, h->poff, h->kb_off);
-    CK(cudaGetLastError());
-  }
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, nullptr, h->mA1e, h->mA2e, h->mA1eq, h->mA2eq, st,
-            train ? h->Hbuf : nullptr);
-  prof_mark(h, 4, st);
-  // ---- reverse exchange into this rank's permutation slots ----
-  ep_exchange(h, h->y_recv, h->y, false, st);
-  if (out_f32)
-    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
-                          h->rb.combine_w);
-  else
-    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
-                                  h->rb.finite_flag, st, h->rb.combine_w);
-  CK(cudaGetLastError());
-  prof_mark(h, 5, st);
-  h->cur_ev = nullptr;
-  h->last_rows = T * h->K;
-  if (train) {
-    h->train_T = T;
-    h->cur_x = x;
-  }
-}
-
-// ---- peer-memory transport (ep.cuh): phases shared by the multi-process path and the
-// single-process emulation group ----
-void ep_peer_alloc(cl_moe* h) {
-  if (h->row_ptr) return;
-  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
-  h->peer_x_dev = dalloc<char*>(R);
-  h->peer_y_dev = dalloc<char*>(R);
-  h->peer_w_dev = dalloc<float*>(R);
-  h->w_recv = dalloc<float>(h->recv_cap);
-  h->expert_dst = dalloc<void*>(h->N);
-  h->expert_dst_w = dalloc<float*>(h->N);
-  h->row_ptr = dalloc<void*>(h->recv_cap);
-  h->peer_dy_dev = dalloc<char*>(R);
-  h->peer_dx_dev = dalloc<char*>(R);
-  h->expert_dst_dy = dalloc<void*>(h->N);
-  h->row_ptr_dx = dalloc<void*>(h->recv_cap);
-  if (h->f % 256 == 0) {  // training-capable: the two backward exchange targets, mapped by peers
-    if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(h->recv_cap * h->d);
-    if (!h->dXsrc) h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * h->d);
-  }
-  h->bar_buf = dalloc<float>(1);
-  CK(cudaMemset(h->bar_buf, 0, sizeof(float)));
-}
-
-void ep_peer_layout(cl_moe* h, cudaStream_t st) {
-  const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
-  const int64_t xrb = h->d * (h->precision == CL_MOE_FP8_E4M3 ? 1 : 2);
-  ep_peer_layout_kernel<<<h->n_local * R + 1, 256, 0, st>>>(h->ep_counts_dev, R, (int)h->N, h->cfg.ep_rank, h->recv_cap,
-                                                             xrb, h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
-                                                             h->expert_dst, h->expert_dst_w, h->ep_off_dev, h->row_ptr,
-                                                             h->rb.finite_flag, h->peer_dy_dev, h->peer_dx_dev,
-                                                             h->expert_dst_dy, h->row_ptr_dx);
-  CK(cudaGetLastError());
-}
-
-void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
-  const int blocks = static_cast<int>((T + 7) / 8);
-  if (h->precision == CL_MOE_FP8_E4M3)
-    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
-                                                  (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
-                                                  h->xperm, h->perm, h->inv, h->row_w, h->sx_in_all, h->expert_dst,
-                                                  h->expert_dst_w);
-  else
-    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
-                                                   (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
-                                                   h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
-                                                   h->expert_dst_w);
-  CK(cudaGetLastError());
-  prof_mark(h, 2, st);
-}
-
-void ep_peer_experts(cl_moe* h, cudaStream_t st, bool train = false) {
-  if (h->precision == CL_MOE_FP8_E4M3) ep_fp8_maps(h);
-  if (train) {  // padded row plan of the receive layout for the weight-gradient GEMMs
-    pad_plan_kernel<<<1, 32, 0, st>>>(h->ep_off_dev, h->n_local, h->poff, h->kb_off);
-    CK(cudaGetLastError());
-  }
-  // inference: rows return weighted (as on one GPU); training keeps Y unweighted for the backward
-  run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, train ? nullptr : h->w_recv, h->mA1e, h->mA2e, h->mA1eq,
-            h->mA2eq, st, train ? h->Hbuf : nullptr, h->row_ptr);
-  prof_mark(h, 4, st);
-}
-
-void ep_peer_combine(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st,
-                     bool train = false) {
-  // inference: rows arrive already scaled by their combine weight (GEMM2 epilogue), as on one GPU
-  const float* w = train ? h->rb.combine_w : nullptr;
-  if (out_f32)
-    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
-                          w);
-  else
-    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
-                                  h->rb.finite_flag, st, w);
-  if (train) {
-    h->train_T = T;
-    h->cur_x = x;
-  }
-  CK(cudaGetLastError());
-  prof_mark(h, 5, st);
-  h->cur_ev = nullptr;
-  h->last_rows = T * h->K;
-}
-
-// Multi-process forward over NVLink peer memory. NCCL carries only the R x N counts and two
-// one-float barriers; the rows move as direct stores of the dispatch kernel and of the GEMM2
-// epilogue. No host synchronisation: the layout is computed on the device.
-//   all-gather(counts) -> layout -> dispatch (stores into owners' x_recv) -> barrier
-//   -> GEMM1 -> GEMM2 (epilogue stores into sources' y) -> barrier -> combine
-// The first all-gather also orders this forward after every rank's previous use of x_recv / y.
-void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
-  NcclApi& nc = NcclApi::get();
-  NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)h->N, NcclApi::kInt32, h->comm, st));
-  ep_peer_layout(h, st);
-  ep_peer_dispatch(h, x, T, st);
-  NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-  ep_peer_experts(h, st, train);
-  NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-  ep_peer_combine(h, x, T, out, out_f32, st, train);
-}
-
-void ensure_training(cl_moe* h) {
-  if (h->train_ready) return;
-  if (h->f % 256) throw ConfigErr("training needs d_ff to be a multiple of 256");
-  if (h->cfg.ep_size > 1 && !h->comm && !h->ep_group)
-    throw ConfigErr("expert-parallel training needs cl_moe_ep_init first");
-  const bool ep = h->comm != nullptr || h->ep_group;
-  // expert-side rows: the receive buffer under expert parallelism
-  const int64_t rows = ep ? h->recv_cap : h->cap * h->K, d = h->d, f = h->f, NL = h->n_local;
-  if (!h->win_ref) {  // buffers and descriptors: once per handle
-    if (ep) {
-      h->dYsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
-      if (!h->dXsrc) h->dXsrc = dalloc<__nv_bfloat16>(h->cap * h->K * d);
-    }
-    h->rp_cap = (rows + 63) / 64 * 64 + 64 * NL;  // 64-aligned: TMA row strides must be 16-byte multiples
-    h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
-    h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
-    h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-    if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
-    h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-    h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
-    h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
-    h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
-    h->dYT = dalloc<__nv_bfloat16>(d * h->rp_cap);
-    h->dHT = dalloc<__nv_bfloat16>(2 * f * h->rp_cap);
-    h->poff = dalloc<int32_t>(NL + 1);
-    h->kb_off = dalloc<int32_t>(NL + 1);
-    for (int v = 0; v < 2; ++v) {
-      const uint32_t brow = v == 0 ? 256 : 128;
-      h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
-      h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
-      h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
-      h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
-      h->mAwo[v] = make_map(h->AT, false, h->rp_cap, f, 128);
-      h->mBwo[v] = make_map(h->dYT, false, h->rp_cap, d, brow);
-      h->mAwi[v] = make_map(h->XT, false, h->rp_cap, d, 128);
-      h->mBwi[v] = make_map(h->dHT, false, h->rp_cap, 2 * f, brow);
-    }
-  }
-  // reference-layout weight copies (re-derived whenever the packed weights change)
-  for (int e = 0; e < NL; ++e) {
-    transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
-        h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, h->win_ref + (size_t)e * d * 2 * f);
-    transpose_weight_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)(f / 32)), 256>>>(
-        h->wout + (size_t)e * d * f, (int)d, (int)f, (int)f, h->wout_ref + (size_t)e * f * d);
-  }
-  CK(cudaGetLastError());
-  CK(cudaDeviceSynchronize());
-  h->train_ready = true;
-}
-
-// Training-mode forward: H = [G | U] kept, Y kept unweighted, combine weights applied in the
-// combine (fp32) so the backward can form d(combine_w) = <dOut, Y>.
-void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStream_t st) {
-  if (h->precision != CL_MOE_BF16) throw ConfigErr("training runs in bf16");
-  if (h->cfg.ep_size > 1 && !h->comm)
-    throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_train_step)");
-  ensure_training(h);
-  if (h->comm) {
-    run_ep(h, x, T, out, false, st, true);
-    return;
-  }
-  const int N = static_cast<int>(h->N);
-  const int tpc = h->tpc_cur;
-  const int blocks = static_cast<int>((T + 7) / 8);
-  dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
-                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
-                                                 h->inv, h->row_w, nullptr);
-  pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, h->n_local, h->poff, h->kb_off);
-  CK(cudaGetLastError());
-  prof_mark(h, 2, st);
-  run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf);
-  prof_mark(h, 4, st);
-  launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
-                                h->rb.finite_flag, st, h->rb.combine_w);
-  CK(cudaGetLastError());
-  prof_mark(h, 5, st);
-  h->cur_ev = nullptr;
-  h->last_rows = T * h->K;
-  h->train_T = T;
-  h->cur_x = x;
-}
-
-// Expert-FFN backward of the last training forward.
-// Backward phases (shared by the single-handle call and the single-process EP group):
-//   A  combine backward (+ dY rows to the experts' owners)
-//   B  dgrad GEMMs on the expert side (+ dX rows back to their sources)
-//   C  dispatch backward (+ router backward)
-//   D  transposes and weight-gradient GEMMs
-// Under the peer transport, A's kernel stores dY rows straight into the owners' dYbuf and B's
-// dgrad-2 epilogue stores dX rows straight into the sources' dXsrc; the caller puts a barrier
-// between A/B and B/C (NCCL all-reduce of one float, or phase order in the group).
-struct BwdArgs {
-  const void* d_out;
-  void* d_hidden;
-  float* d_cw;
-  float* dw_in;
-  float* dw_out;
-  float* dw_router;
-  float g_aux, g_z;
-};
-
-bool ep_mode(const cl_moe* h) { return h->comm != nullptr || h->ep_group; }
-bool ep_peer_mode(const cl_moe* h) { return h->ep_group || (h->comm && h->ep_transport == 1); }
-
-void bwd_check(cl_moe* h) {
-  if (!h->train_ready || h->train_T == 0) throw ConfigErr("backward needs a preceding cl_moe_forward_train");
-}
-
-void bwd_phase_a(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
-  const int64_t T = h->train_T, rows = T * h->K, d = h->d;
-  const bool ep = ep_mode(h), peer = ep_peer_mode(h);
-  __nv_bfloat16* dY_src = ep ? h->dYsrc : h->dYbuf;
-  prof_begin(h, st, 1);
-  // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
-  combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.d_out), h->y, h->perm,
-                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K, dY_src,
-                                                           a.d_cw, peer ? h->expert_dst_dy : nullptr, h->rb.topk_idx,
-                                                           h->rb.offsets);
-  CK(cudaGetLastError());
-  if (ep && !peer) ep_exchange(h, dY_src, h->dYbuf, true, st);  // dY rows to the experts' owners
-  prof_mark(h, 0, st);
-}
-
-void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
-  const int64_t d = h->d, f = h->f;
-  const int NL = h->n_local;
-  const bool ep = ep_mode(h), peer = ep_peer_mode(h);
-  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
-  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
-  const int v = h->gemm_ctas == 2 ? 1 : 0;  // same variant the training forward chose
-  // 2. dA = dY W_out^T fused with the SwiGLU backward -> dH
-  GemmArgs a1{};
-  a1.offsets = es_off;
-  a1.n_experts = NL;
-  a1.n_tiles_n = static_cast<int>(f / kBN);
-  a1.num_kb = static_cast<int>(d * 2 / kBKBytes);
-  a1.b_rows_per_expert = static_cast<int>(f);
-  a1.out = h->dHbuf;
-  a1.aux = h->Hbuf;
-  a1.ffn = static_cast<int>(f);
-  a1.aux_t = h->dHT;  // dH^T straight from the epilogue (dW_in GEMM operand)
-  a1.rp = h->rp_cap;
-  a1.poff = h->poff;
-  // 3. dX = dH W_in^T (peer transport: each row straight back into its source's dXsrc)
-  GemmArgs a2{};
-  a2.offsets = es_off;
-  a2.n_experts = NL;
-  a2.n_tiles_n = static_cast<int>(d / kBN);
-  a2.num_kb = static_cast<int>(2 * f * 2 / kBKBytes);
-  a2.b_rows_per_expert = static_cast<int>(d);
-  a2.out = h->dXbuf;
-  a2.ldo = static_cast<int>(d);
-  a2.row_ptr = peer ? h->row_ptr_dx : nullptr;
-  if (v) {
-    launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
-    prof_mark(h, 1, st);
-    launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
-  } else {
-    launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
-    prof_mark(h, 1, st);
-    launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
-  }
-  if (ep && !peer) ep_exchange(h, h->dXbuf, dX_src, false, st);  // dX rows back to their tokens' ranks
-  prof_mark(h, 2, st);
-}
-
-void bwd_phase_c(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
-  const int64_t T = h->train_T, d = h->d;
-  const bool ep = ep_mode(h);
-  __nv_bfloat16* dX_src = ep ? h->dXsrc : h->dXbuf;
-  // 4. dispatch backward (gather_rows bwd): d_hidden[j] = sum_k dX[inv[j,k]]  (+ router term)
-  if (a.dw_router) {
-    const int N = static_cast<int>(h->N);
-    if (!h->rdz) {
-      h->rdz = dalloc<float>(h->cap * h->N);
-      h->rpart = dalloc<float>(((h->cap + kRwTokens - 1) / kRwTokens) * h->d * h->N);
-    }
-    router_bwd_dz_kernel<<<(int)((T + 127) / 128), 128, 0, st>>>(h->rb.probs, h->rb.logits, h->rb.topk_idx, a.d_cw,
-                                                                h->rb.counts, (int)T, N, (int)h->K, a.g_aux, a.g_z,
-                                                                h->rdz);
-    const int chunks = static_cast<int>((T + kRwTokens - 1) / kRwTokens);
-    router_wgrad_partial_kernel<<<dim3((unsigned)(d / 64), (unsigned)chunks, (unsigned)((N + 15) / 16)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(h->cur_x), h->rdz, (int)T, (int)d, N, h->rpart);
-    router_wgrad_reduce_kernel<<<(int)((d * N + 255) / 256), 256, 0, st>>>(h->rpart, chunks, (int)(d * N), a.dw_router);
-    // the router is replicated: its gradient is the sum over the data-parallel ranks
-    if (h->comm) NCK(NcclApi::get().AllReduce(a.dw_router, a.dw_router, (size_t)(d * N), NcclApi::kFloat32,
-                                              NcclApi::kSum, h->comm, st));
-    const int blocks = static_cast<int>((T + 7) / 8);
-    switch (h->K) {
-      case 1: dispatch_bwd_router_kernel<1><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
-      case 2: dispatch_bwd_router_kernel<2><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
-      case 4: dispatch_bwd_router_kernel<4><<<blocks, 256, 0, st>>>(dX_src, h->inv, (int)T, (int)d, h->rdz, h->wr, N, static_cast<__nv_bfloat16*>(a.d_hidden)); break;
-      default: throw ConfigErr("router backward supports top_k in {1, 2, 4}");
-    }
-  } else {
-    launch_combine<__nv_bfloat16>(dX_src, h->inv, (int)T, (int)d, (int)h->K, static_cast<__nv_bfloat16*>(a.d_hidden),
-                                  h->rb.finite_flag, st);
-  }
-  CK(cudaGetLastError());
-  prof_mark(h, 3, st);
-}
-
-void bwd_phase_d(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
-  const int64_t d = h->d, f = h->f;
-  const int NL = h->n_local;
-  const bool ep = ep_mode(h);
-  const int32_t* es_off = ep ? h->ep_off_dev : h->rb.offsets;
-  const void* es_x = ep ? static_cast<const void*>(h->x_recv) : h->xperm;
-  // 5. weight gradients over each expert's rows (variable K): padded K-major transposes, then
-  //    dW_out[e] = A_e^T dY_e ([f x d]) and dW_in[e] = X_e^T dH_e ([d x 2f]), fp32.
-  //    (A^T and dH^T were written by the GEMM1 / dgrad-1 epilogues; only their padding columns
-  //    need zeroing. X^T and dY^T go through the transpose kernel.)
-  const unsigned pb = static_cast<unsigned>(h->rp_cap / 64);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d,
-                                                                     es_off, h->poff, NL, h->XT, h->rp_cap);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT,
-                                                                     h->rp_cap);
-  zero_pad_cols_kernel<<<dim3((unsigned)((f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
-                                                                                    h->poff);
-  zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
-                                                                                        h->rp_cap, es_off, h->poff);
-  CK(cudaGetLastError());
-  prof_mark(h, 4, st);
-  const int gw = (f % 256 == 0) ? 2 : 1;
-  GemmArgs wo{};
-  wo.n_experts = NL;
-  wo.kb_off = h->kb_off;
-  wo.m_tiles = static_cast<int>(f / (128 * gw));
-  wo.n_tiles_n = static_cast<int>(d / kBN);
-  wo.out = a.dw_out;
-  wo.ldo = static_cast<int>(d);
-  wo.out_estride = f * d;
-  GemmArgs wi{};
-  wi.n_experts = NL;
-  wi.kb_off = h->kb_off;
-  wi.m_tiles = static_cast<int>(d / (128 * gw));
-  wi.n_tiles_n = static_cast<int>(2 * f / kBN);
-  wi.out = a.dw_in;
-  wi.ldo = static_cast<int>(2 * f);
-  wi.out_estride = d * 2 * f;
-  if (gw == 2) {
-    launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwo[1], h->mBwo[1], wo, st);
-    prof_mark(h, 5, st);
-    launch_gemm<2, EPI_WGRAD, false, false, true>(h, h->mAwi[1], h->mBwi[1], wi, st);
-  } else {
-    launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwo[0], h->mBwo[0], wo, st);
-    prof_mark(h, 5, st);
-    launch_gemm<1, EPI_WGRAD, false, false, true>(h, h->mAwi[0], h->mBwi[0], wi, st);
-  }
-  prof_mark(h, 6, st);
-  h->cur_ev = nullptr;
-}
-
-// One float all-reduce on the communicator: orders every rank's preceding peer stores before
-// anything this rank issues next (the stores were fenced with __threadfence_system).
-void ep_barrier(cl_moe* h, cudaStream_t st) {
-  NCK(NcclApi::get().AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-}
-
-void run_backward(cl_moe* h, const void* d_out, void* d_hidden, float* d_cw, float* dw_in, float* dw_out,
-                  cudaStream_t st, float* dw_router = nullptr, float g_aux = 0.0f, float g_z = 0.0f) {
-  bwd_check(h);
-  const BwdArgs a{d_out, d_hidden, d_cw, dw_in, dw_out, dw_router, g_aux, g_z};
-  const bool peer = h->comm && h->ep_transport == 1;
-  bwd_phase_a(h, a, st);
-  if (peer) ep_barrier(h, st);
-  bwd_phase_b(h, a, st);
-  if (peer) ep_barrier(h, st);
-  bwd_phase_c(h, a, st);
-  bwd_phase_d(h, a, st);
-}
-
-}  // namespace
 
 extern "C" {
 

@@ -1,0 +1,244 @@
+// Single-GPU forward orchestration: router, plan, dispatch, grouped-GEMM launches, combine.
+// Host side of libcompass_moe.so, included once, in order, by capi.cu (a single translation
+// unit; the helpers live in an anonymous namespace).
+#pragma once
+
+namespace {
+
+// m-tiles per L2-resident group for a row-grouped GEMM whose A rows are k_bytes long (decode_tile).
+int64_t l2_group_budget() {
+  static const int64_t budget = [] {
+    const char* e = std::getenv("CL_MOE_L2_GROUP_MB");
+    return (int64_t)(e ? std::atoi(e) : 32) << 20;
+  }();
+  return budget;
+}
+int m_group_for(int64_t k_bytes, int bm) {
+  const int64_t budget = l2_group_budget();
+  if (budget <= 0) return 0;
+  return static_cast<int>(std::max<int64_t>(1, budget / (k_bytes * bm)));
+}
+
+template <int G, int EPI, bool F8, bool OF8, bool WG = false>
+void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st) {
+  if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
+  GemmArgs args = args_in;
+  args.tile_counter = h->tile_counter;
+  if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
+  if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
+  CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((h->num_sms / G) * G);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = GemmCfg<G>::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG>, a, b, args));
+}
+
+// route_tokens on device: K1 + K2.
+void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
+  if (T < 1) throw RunErr("route_tokens: B must be >= 1");
+  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
+  const int N = static_cast<int>(h->N);
+  // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
+  // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
+  // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
+  static const int force = [] {
+    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "lat", "small" or "big"
+    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : 0) : 0;
+  }();
+  const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
+  const bool big_ok = RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
+  // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
+  const int N4r = (N + 3) / 4 * 4;
+  const int lat_chunk = N4r <= 16 ? 256 : N4r <= 32 ? 128 : 64;
+  const int tpc_lat = RouterLatSmem<3, 64>(N).tpc;
+  const bool lat = !big && (force == 3 || (force == 0 && (T + tpc_lat - 1) / tpc_lat <= h->num_sms));
+  const bool small = !big && !lat && router_smem_bytes(N, 32, 8) <= 220 * 1024;
+  const int tpc = big ? tpc_big : lat ? tpc_lat : router_tokens_per_cta(N, small ? 32 : 128);
+  h->tpc_cur = tpc;
+  h->last_tokens = T;
+  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
+  prof_begin(h, st);
+  if (lat && lat_chunk == 256)
+    router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (lat && lat_chunk == 128)
+    router_lat_kernel<3, 128><<<n_tiles, 128, RouterLatSmem<3, 128>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (lat)
+    router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (big)
+    router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (small)
+    router_kernel<32, 8><<<n_tiles, 32, router_smem_bytes(N, 32, 8), st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else
+    router_kernel<128, 3><<<n_tiles, 128, router_smem_bytes(N, 128, 3), st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+  prof_mark(h, 0, st);
+  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+  prof_mark(h, 1, st);
+}
+
+void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T, cudaStream_t st) {
+  if (T < 1) throw RunErr("moe_forward: B must be >= 1");
+  if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
+  const int N = static_cast<int>(h->N);
+  const int tpc = router_tokens_per_cta(N, 128);
+  h->tpc_cur = tpc;
+  h->last_tokens = T;
+  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
+  CK(cudaMemcpyAsync(h->rb.topk_idx, idx, sizeof(int32_t) * T * h->K, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemcpyAsync(h->rb.combine_w, w, sizeof(float) * T * h->K, cudaMemcpyDeviceToDevice, st));
+  prof_begin(h, st);
+  decision_tiles_kernel<<<n_tiles, 128, 0, st>>>(h->rb.topk_idx, (int)T, N, (int)h->K, tpc, h->rb);
+  CK(cudaGetLastError());
+  prof_mark(h, 0, st);
+  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+  prof_mark(h, 1, st);
+}
+
+// GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
+void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
+               const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
+               cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr) {
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  GemmArgs g1{};
+  g1.offsets = offsets;
+  if (h->gemm_auto) {
+    // M=256 CTA-pair tiles pay off only when experts have enough rows; small batches (decode)
+    // stream weights and are better served by M=128 tiles (less A over-fetch per B byte).
+    const int64_t rows_per_expert = h->last_tokens * h->K * (h->cfg.ep_size > 1 ? h->cfg.ep_size : 1) / h->n_local;
+    h->gemm_ctas = rows_per_expert >= 1024 ? 2 : 1;
+  }
+  g1.n_experts = h->n_local;
+  g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
+  g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
+  g1.b_rows_per_expert = static_cast<int>(2 * h->f);
+  g1.out = act;
+  g1.ldo = static_cast<int>(h->f);
+  g1.act_scale = h->sx_in;
+  g1.w_scale = h->ws_in;
+  g1.out_scale = h->sx_mid;
+  g1.aux = h_save;
+  g1.ffn = static_cast<int>(h->f);
+  if (h_save) {  // training: also write A^T into the padded K-major buffer of the dW_out GEMM
+    g1.aux_t = h->AT;
+    g1.rp = h->rp_cap;
+    g1.poff = h->poff;
+  }
+  GemmArgs g2{};
+  g2.offsets = offsets;
+  g2.n_experts = h->n_local;
+  g2.n_tiles_n = static_cast<int>(h->d / kBN);
+  g2.num_kb = static_cast<int>(h->f * (fp8 ? 1 : 2) / kBKBytes);
+  g2.b_rows_per_expert = static_cast<int>(h->d);
+  g2.out = y;
+  g2.ldo = static_cast<int>(h->d);
+  g2.row_scale = row_w;
+  g2.row_ptr = row_ptr;
+  g1.half_tail = g2.half_tail = 1;  // 2-CTA: tail m-tiles of <= 128 rows as M=128 pair MMAs
+  g2.act_scale = h->sx_mid;
+  g2.w_scale = h->ws_out;
+  const int v = h->gemm_ctas == 2 ? 1 : 0;
+  if (!fp8) {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<2, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<1, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
+    }
+  } else {
+    if (v) {
+      launch_gemm<2, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<2, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
+    } else {
+      launch_gemm<1, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      prof_mark(h, 3, st);
+      launch_gemm<1, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
+    }
+  }
+}
+
+// dispatch + expert FFN + combine (local experts; ep_size == 1).
+void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train = false);
+
+void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  if (h->comm) {  // expert parallel (one rank: loopback through the same exchange code)
+    run_ep(h, x, T, out, out_f32, st);
+    return;
+  }
+  if (h->cfg.ep_size > 1) throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_forward)");
+  const int N = static_cast<int>(h->N);
+  const int tpc = h->tpc_cur;
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  const int blocks = static_cast<int>((T + 7) / 8);
+  if (fp8)
+    dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+                                                  tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
+                                                  h->inv, h->row_w, h->sx_in);
+  else
+    dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                   (int)h->K, tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm,
+                                                   h->perm, h->inv, h->row_w, nullptr);
+  CK(cudaGetLastError());
+  prof_mark(h, 2, st);
+
+  run_gemms(h, h->rb.offsets, h->act, h->y, h->row_w, h->mA1, h->mA2, h->mA1q, h->mA2q, st);
+  prof_mark(h, 4, st);
+  if (out_f32)
+    launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
+  else
+    launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                  h->rb.finite_flag, st);
+  CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
+  h->last_rows = T * h->K;
+}
+
+void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_t st) {
+  if (!o) return;
+  const int64_t N = h->N, K = h->K;
+  if (o->logits) CK(cudaMemcpyAsync(o->logits, h->rb.logits, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
+  if (o->probs) CK(cudaMemcpyAsync(o->probs, h->rb.probs, sizeof(float) * T * N, cudaMemcpyDeviceToDevice, st));
+  if (o->topk_idx) CK(cudaMemcpyAsync(o->topk_idx, h->rb.topk_idx, sizeof(int32_t) * T * K, cudaMemcpyDeviceToDevice, st));
+  if (o->combine_weights)
+    CK(cudaMemcpyAsync(o->combine_weights, h->rb.combine_w, sizeof(float) * T * K, cudaMemcpyDeviceToDevice, st));
+  if (o->counts) {
+    i32_to_i64_kernel<<<(int)((N + 127) / 128), 128, 0, st>>>(h->rb.counts, (int)N, o->counts);
+    CK(cudaGetLastError());
+  }
+  if (o->agg_prob) CK(cudaMemcpyAsync(o->agg_prob, h->rb.agg_prob, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+  if (o->aux_loss) CK(cudaMemcpyAsync(o->aux_loss, h->rb.losses, sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (o->z_loss) CK(cudaMemcpyAsync(o->z_loss, h->rb.losses + 1, sizeof(float), cudaMemcpyDeviceToDevice, st));
+}
+
+void ensure_fp8_storage(cl_moe* h) {
+  if (h->win8) return;
+  h->win8 = dalloc<uint8_t>((size_t)h->n_local * 2 * h->f * h->d);
+  h->wout8 = dalloc<uint8_t>((size_t)h->n_local * h->d * h->f);
+  h->ws_in = dalloc<float>((size_t)h->n_local * 2 * h->f);
+  h->ws_out = dalloc<float>((size_t)h->n_local * h->d);
+  build_maps(h, true);
+}
+
+}  // namespace
