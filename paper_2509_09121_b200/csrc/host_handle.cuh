@@ -274,6 +274,8 @@ void validate(const cl_moe_config* c) {
   const int ep = c->ep_size <= 0 ? 1 : c->ep_size;
   if (c->n_experts % ep) throw ConfigErr("n_experts must be divisible by ep_size");
   if (c->ep_rank < 0 || c->ep_rank >= ep) throw ConfigErr("ep_rank out of range");
+  if (c->max_tokens * c->top_k * ep > (int64_t(1) << 30))  // receive rows are int32-indexed
+    throw ConfigErr("max_tokens x top_k x ep_size out of range");
   if (c->gemm_ctas < 0 || c->gemm_ctas > 2) throw ConfigErr("gemm_ctas must be 0, 1 or 2");
 }
 
