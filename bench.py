@@ -128,6 +128,17 @@ def dist_env():
 
 # ------------------------------------------------------------------------------------------
 # CPU baseline: the reference implementation (or the oracle port) on a bounded token sample
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(cfg, t_sample: int, kind_pref: str = "reference"):
     """Prepare a bounded sample of the configured layer for the CPU oracle. Weights are random
     uniform values (the reference arithmetic is data-independent: dense fp64-accumulated loops),
@@ -177,7 +188,8 @@ def run_reference(args, cfg):
                 dtype="f32", data="synthetic", impl="reference",
                 config=dict(workload=cfg["workload"], T=cfg["T"], d=cfg["d"], n_experts=cfg["N"], top_k=cfg["K"],
                             d_ff=cfg["f"], parallelism="cpu", sample_tokens=t_s),
-                cpu_baseline=dict(value=val, unit="tokens/s", cores=cores, kind=kind, sample=sample),
+                cpu_baseline=dict(value=val, unit="tokens/s", cores=cores, kind=kind, sample=sample,
+                                  cpu_model=cpu_model(), host_threads=jobs),
                 e2e=dict(value=val, unit="tokens/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
 
@@ -322,6 +334,22 @@ def run_ours(args, cfg):
         e2e_s = float(t.item())
     e2e_val = world * T * e2e_steps / e2e_s
 
+    # ---- NVLink exchange accounting (N > 1): exact rows this rank sent to other ranks ----
+    a2a = None
+    if world > 1:
+        counts = layer.ep_last_counts()  # [R][N], row = source
+        nl_ = N // world
+        mine = counts[rank]
+        remote_rows = int(sum(mine[g] for g in range(N) if g // nl_ != rank))
+        esz_x = 1 if args.precision == "fp8" else 2
+        b_out = remote_rows * d * esz_x                # dispatch direction (x rows)
+        b_back = remote_rows * d * 2                   # return direction (bf16 rows)
+        t = torch.tensor([b_out, b_back], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        a2a = dict(transport=transport, max_rank_bytes_dispatch=float(t[0]), max_rank_bytes_return=float(t[1]),
+                   note="bytes of the last step's rows that crossed NVLink, max over ranks (from the all-gathered "
+                        "counts); the dispatch stage time includes the counts all-gather and the layout kernel")
+
     # ---- roofline of the dominant kernel (GEMM1 + SwiGLU) and of dispatch ----
     peaks = load_peaks()
     nf, nb = calls
@@ -387,9 +415,14 @@ def run_ours(args, cfg):
                      timing=("host wall clock: pinned H2D of x and dOut, forward_train + backward, D2H of out and "
                              "d_hidden, every step" if train else
                              "host wall clock around K pipelined cl_moe_forward_host_async calls + cl_moe_host_wait")),
-            gpu_launches=(6 + 13) * args.steps if train else 6 * args.steps,
+            # ours per step: router, plan, dispatch, GEMM1, GEMM2, combine (+ the EP peer layout
+            # kernel); training adds pad-plan and combine-bwd, dgrad x2, dispatch-bwd, transposes x2,
+            # zero-pad x2, wgrad x2 (NCCL kernels are not counted)
+            gpu_launches=((17 if train else 6) + (1 if (world > 1 and "peer" in transport) else 0)) * args.steps,
             clocks=clocks,
         )
+        if world > 1 and a2a is not None:
+            line["a2a"] = a2a
         if not args.no_cpu_baseline and world == 1:
             t_s = pick_cpu_tokens(cfg)
             o, kind, inp, w_in, w_out = cpu_sample(cfg, t_s)
@@ -399,7 +432,8 @@ def run_ours(args, cfg):
             cpu_step(o, inp, w_in, w_out, K, jobs)
             dt = time.perf_counter() - t0
             line["cpu_baseline"] = dict(
-                value=t_s / dt, unit="tokens/s", cores=min(jobs, N), kind=kind,
+                value=t_s / dt, unit="tokens/s", cores=min(jobs, N), kind=kind, cpu_model=cpu_model(),
+                host_threads=jobs,
                 sample=f"{t_s} tokens of the same layer shape, one forward, fp32 (expert fan-out over "
                        f"{min(jobs, N)} threads)")
         if "frac" not in line["roofline"]:

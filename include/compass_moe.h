@@ -268,6 +268,9 @@ cl_status cl_moe_ep_group_train_step(cl_moe* const* hs, int32_t R, const void* c
                                      const int64_t* T, void* const* out, const void* const* d_out,
                                      void* const* d_hidden, float* const* d_combine_w,
                                      float* const* dw_in, float* const* dw_out, void* stream);
+/* The all-gathered R x N routing counts of the last expert-parallel forward (row = source rank),
+ * e.g. to account the bytes each rank sent over NVLink. */
+cl_status cl_moe_ep_last_counts(cl_moe* h, int64_t* counts);
 /* Pure host helper (no GPU): peer-transport layout of `rank` from counts[R][N]:
  * dispatch_row[g] = first row of this rank's piece for expert g in the owner's receive buffer;
  * return_row[e*R+s] = first row of piece (local expert e, source s) in s's permutation;

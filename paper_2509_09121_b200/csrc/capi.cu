@@ -424,6 +424,19 @@ cl_status cl_moe_balance_calibration(cl_moe* h, const void* base, int64_t T_base
   });
 }
 
+cl_status cl_moe_ep_last_counts(cl_moe* h, int64_t* counts) {
+  return guarded(h, [&] {
+    if (!counts) throw ConfigErr("counts is null");
+    if (!h->ep_counts_dev) throw ConfigErr("no expert-parallel forward has run on this handle");
+    CK(cudaSetDevice(h->cfg.device));
+    const int R = h->cfg.ep_size <= 0 ? 1 : h->cfg.ep_size;
+    std::vector<int32_t> c((size_t)R * h->N);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(c.data(), h->ep_counts_dev, sizeof(int32_t) * c.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < c.size(); ++i) counts[i] = c[i];
+  });
+}
+
 cl_status cl_moe_ep_layout(const int64_t* counts, int32_t R, int32_t N, int32_t rank, int64_t* local_offsets,
                            int64_t* recv_piece, int64_t* recv_total) {
   if (!counts || !local_offsets || !recv_piece || R < 1 || N < R || N % R || rank < 0 || rank >= R)

@@ -322,6 +322,12 @@ class MoELayer:
         """Collective: switch to the NVLink peer-memory transport (cl_moe_ep_peer_init)."""
         self._check(self.L.cl_moe_ep_peer_init(self.h), "ep_peer_init")
 
+    def ep_last_counts(self) -> np.ndarray:
+        """R x N routing counts all-gathered by the last expert-parallel forward (row = source)."""
+        c = np.empty((self.cfg.ep_size, self.cfg.n_experts), np.int64)
+        self._check(self.L.cl_moe_ep_last_counts(self.h, c.ctypes.data), "ep_last_counts")
+        return c
+
     def ep_forward(self, hidden: torch.Tensor) -> torch.Tensor:
         hidden = self._bf16(hidden)
         out = torch.empty_like(hidden)

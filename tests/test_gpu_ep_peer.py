@@ -104,6 +104,8 @@ def test_peer_transport_single_rank_nccl():
         out = lay.ep_forward(x)
         lay.sync()
         assert torch.equal(out, ref.forward(x))
+    counts = Oracle("port").route(inp["x"], inp["w_router"], k)["counts"]
+    assert np.array_equal(lay.ep_last_counts(), counts[None, :])
 
 
 @pytest.mark.parametrize("R,n,k,ts", [(2, 8, 2, (300, 517)), (4, 16, 4, (256, 1, 700, 64))])
