@@ -54,8 +54,16 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
     const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "lat", "small" or "big"
     return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : 0) : 0;
   }();
-  const int tpc_big = RouterBigSmem(N, 32, 3).tpc;
-  const bool big_ok = RouterBigSmem(N, 32, 3).total <= 220 * 1024;
+  // large batches: 4 tokens x 4 experts per thread when that still gives >= 3 CTAs per SM, else
+  // 2 x 4 (2x the CTAs, e.g. C3's 8192 tokens); CL_MOE_BIG_TOK=2|4 pins the choice (benchmarks)
+  static const int big_tok_env = [] {
+    const char* e = std::getenv("CL_MOE_BIG_TOK");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int tiles4 = (int)((T + RouterBigSmem(N, 32, 3, 4).tpc - 1) / RouterBigSmem(N, 32, 3, 4).tpc);
+  const int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
+  const int tpc_big = RouterBigSmem(N, 32, 3, big_tok).tpc;
+  const bool big_ok = RouterBigSmem(N, 32, 3, big_tok).total <= 220 * 1024;
   const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
   // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
   const int N4r = (N + 3) / 4 * 4;
@@ -76,6 +84,9 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   else if (lat)
     router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (big && big_tok == 2)
+    router_big_kernel<32, 3, 2><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 2).total, st>>>(
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   else if (big)
     router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(

@@ -328,7 +328,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
 
   const int64_t rows = h->cap * h->K;
   const int tpc = std::min({router_tokens_per_cta(static_cast<int>(h->N), 32),
-                            RouterBigSmem(static_cast<int>(h->N), 32, 3).tpc,
+                            RouterBigSmem(static_cast<int>(h->N), 32, 3, 2).tpc,
                             RouterLatSmem<3, 64>(static_cast<int>(h->N)).tpc});  // smallest tile of any variant
   h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
   RouteBufs& rb = h->rb;
@@ -360,6 +360,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

@@ -423,9 +423,9 @@ __global__ void __launch_bounds__(128) router_lat_kernel(const __nv_bfloat16* __
 struct RouterBigSmem {
   int tpc, N4;
   size_t rx, sw, slog, sidx, slse, total;
-  __host__ __device__ RouterBigSmem(int n_experts, int threads, int stages) {
+  __host__ __device__ RouterBigSmem(int n_experts, int threads, int stages, int tok = 4) {
     N4 = (n_experts + 3) / 4 * 4;
-    tpc = (threads / (N4 / 4)) * 4;
+    tpc = (threads / (N4 / 4)) * tok;
     rx = 0;
     sw = rx + (size_t)stages * tpc * kRouterChunk * 2;
     slog = sw + (size_t)stages * sizeof(double) * kRouterChunk * N4;
@@ -435,11 +435,11 @@ struct RouterBigSmem {
   }
 };
 
-template <int kThreads, int kStages>
+template <int kThreads, int kStages, int kTok = 4>
 __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bfloat16* __restrict__ x,
                                                                  const double* __restrict__ wr64, int T, int d, int N,
                                                                  int K, RouteBufs rb) {
-  const RouterBigSmem L(N, kThreads, kStages);
+  const RouterBigSmem L(N, kThreads, kStages, kTok);
   const int N4 = L.N4;
   const int groups = N4 / 4;
   const int tg_per_cta = kThreads / groups;
@@ -455,9 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
   const int tg = threadIdx.x / groups;
   const int g = threadIdx.x % groups;
   const bool worker = tg < tg_per_cta;
-  double acc[4][4];
+  double acc[kTok][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < kTok; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
@@ -470,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
       const int r = i >> 3, q = i & 7;
       const bool ok = tok0 + r < T;
       const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
-      const int qs = q ^ ((r >> 2) & 7);
+      const int qs = q ^ ((r / kTok) & 7);
       cp_async16(rawx + ((size_t)buf * tpc + r) * 128 + qs * 16, src, ok);
     }
     const double* wsrc = wr64 + (size_t)c0 * N4;
@@ -493,12 +493,12 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
       const double2* wv = reinterpret_cast<const double2*>(sw + (size_t)buf * kRouterChunk * N4 + g * 4);
 #pragma unroll 1
       for (int q = 0; q < kRouterChunk / 8; ++q) {
-        // 8 l-columns of the 4 tokens, widened to fp64 once for all 4 experts
-        double xd[4][8];
+        // 8 l-columns of the kTok tokens, widened to fp64 once for all 4 experts
+        double xd[kTok][8];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int r = tg * 4 + a;
-          const int4 raw = *reinterpret_cast<const int4*>(xb + (size_t)r * 128 + ((q ^ ((r >> 2) & 7)) * 16));
+        for (int a = 0; a < kTok; ++a) {
+          const int r = tg * kTok + a;
+          const int4 raw = *reinterpret_cast<const int4*>(xb + (size_t)r * 128 + ((q ^ ((r / kTok) & 7)) * 16));
           const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
           for (int i = 0; i < 8; ++i) xd[a][i] = static_cast<double>(__bfloat162float(hv[i]));
@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
           const double2 w01 = wv[l * (N4 / 2)];
           const double2 w23 = wv[l * (N4 / 2) + 1];
 #pragma unroll
-          for (int a = 0; a < 4; ++a) {
+          for (int a = 0; a < kTok; ++a) {
             acc[a][0] = fma(xd[a][i], w01.x, acc[a][0]);
             acc[a][1] = fma(xd[a][i], w01.y, acc[a][1]);
             acc[a][2] = fma(xd[a][i], w23.x, acc[a][2]);
@@ -522,8 +522,8 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
   __syncthreads();
   if (worker) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int tl = tg * 4 + a;
+    for (int a = 0; a < kTok; ++a) {
+      const int tl = tg * kTok + a;
       const int tok = tok0 + tl;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
