@@ -792,9 +792,10 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
 
 // Warp-per-token kernels (dispatch, combine): (T/8) x slices CTAs of 8 warps; small batches get
 // up to 8 column slices per token so a few hundred warps are in flight.
+constexpr int kTargetSms = 148;  // B200 (sm_100a, the only target): sizing hint, not a correctness bound
 inline dim3 token_grid(int64_t T) {
   const int blocks = static_cast<int>((T + 7) / 8);
-  const int slices = std::max(1, std::min(8, (4 * 148 + blocks - 1) / blocks));
+  const int slices = std::max(1, std::min(8, (4 * kTargetSms + blocks - 1) / blocks));
   return dim3(blocks, slices);
 }
 
