@@ -347,6 +347,7 @@ def run_ours(args, cfg):
         t = torch.tensor([b_out, b_back], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         a2a = dict(transport=transport, max_rank_bytes_dispatch=float(t[0]), max_rank_bytes_return=float(t[1]),
+                   dispatch_stage_gbs_rank0=float(t[0]) / max(stage_ms["dispatch"] / max(calls[0], 1), 1e-9) / 1e6,
                    note="bytes of the last step's rows that crossed NVLink, max over ranks (from the all-gathered "
                         "counts); the dispatch stage time includes the counts all-gather and the layout kernel")
 
