@@ -245,11 +245,15 @@ def run_ours(args, cfg):
         layer.quantize_fp8()
     stream = torch.cuda.current_stream()
 
-    def step():
+    def step(xb=None, gb=None, ob=None, dhb=None):
         if train:
-            layer._check(layer.L.cl_moe_forward_train(layer.h, x.data_ptr(), T, out.data_ptr(), None,
+            xb = x if xb is None else xb
+            gb = g_out if gb is None else gb
+            ob = out if ob is None else ob
+            dhb = d_hid if dhb is None else dhb
+            layer._check(layer.L.cl_moe_forward_train(layer.h, xb.data_ptr(), T, ob.data_ptr(), None,
                                                       stream.cuda_stream), "forward_train")
-            layer._check(layer.L.cl_moe_backward(layer.h, g_out.data_ptr(), d_hid.data_ptr(), d_cw.data_ptr(),
+            layer._check(layer.L.cl_moe_backward(layer.h, gb.data_ptr(), dhb.data_ptr(), d_cw.data_ptr(),
                                                  dwi.data_ptr(), dwo.data_ptr(), stream.cuda_stream), "backward")
         else:
             layer._check(layer.L.cl_moe_forward(layer.h, x.data_ptr(), T, out.data_ptr(), None, stream.cuda_stream),
@@ -288,23 +292,43 @@ def run_ours(args, cfg):
     value = world * T * args.steps / (ms / 1e3)
 
     if train:
+        # double-buffered pipeline: H2D of step i+1 and D2H of step i-1 on copy streams overlap
+        # step i's compute; every step still moves its inputs in and its outputs out
         xh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
         gh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
-        oh = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
-        dh_h = torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True)
+        oh = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
+        dh_h = [torch.empty(T, d, dtype=torch.bfloat16, pin_memory=True) for _ in range(2)]
         xh.copy_(x)
         gh.copy_(g_out)
+        xs_, gs_ = [x, torch.empty_like(x)], [g_out, torch.empty_like(x)]
+        os_, dhs_ = [out, torch.empty_like(x)], [d_hid, torch.empty_like(x)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_drained = [torch.cuda.Event() for _ in range(2)]
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         e2e_steps = max(2, args.steps // 2)
-        for _ in range(e2e_steps):
-            x.copy_(xh, non_blocking=True)
-            g_out.copy_(gh, non_blocking=True)
-            step()
-            oh.copy_(out, non_blocking=True)
-            dh_h.copy_(d_hid, non_blocking=True)
+        for i in range(e2e_steps):
+            b = i % 2
+            with torch.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(ev_done[b])  # step i-2 no longer reads this input set
+                xs_[b].copy_(xh, non_blocking=True)
+                gs_[b].copy_(gh, non_blocking=True)
+                ev_in[b].record(s_in)
+            stream.wait_event(ev_in[b])
+            if i >= 2:
+                stream.wait_event(ev_drained[b])  # step i-2's outputs are out of this set
+            step(xs_[b], gs_[b], os_[b], dhs_[b])
+            ev_done[b].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_done[b])
+                oh[b].copy_(os_[b], non_blocking=True)
+                dh_h[b].copy_(dhs_[b], non_blocking=True)
+                ev_drained[b].record(s_out)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         e2e_val = world * T * e2e_steps / e2e_s
@@ -414,7 +438,7 @@ def run_ours(args, cfg):
                 layer_tflops=(g1_flop + g2_flop) / (ms_step * 1e-3) / 1e12),
             e2e=dict(value=e2e_val, unit="tokens/s", h2d_bytes_per_step=h2d_b, d2h_bytes_per_step=d2h_b,
                      timing=("host wall clock: pinned H2D of x and dOut, forward_train + backward, D2H of out and "
-                             "d_hidden, every step" if train else
+                             "d_hidden, every step (copies double-buffered on two copy streams)" if train else
                              "host wall clock around K pipelined cl_moe_forward_host_async calls + cl_moe_host_wait")),
             # ours per step: router, plan, dispatch, GEMM1, GEMM2, combine (+ the EP peer layout
             # kernel); training adds pad-plan and combine-bwd, dgrad x2, dispatch-bwd, transposes x2,
