@@ -372,3 +372,113 @@ def test_ep_peer_transport_gloo_matches_single_process_oracle(tmp_path, world, n
     ref = o.moe_forward(full["x"], full["w_in"], full["w_out"], r["topk_idx"], r["combine_weights"])
     got = np.concatenate([np.load(tmp_path / f"out{i}.npy") for i in range(world)])
     assert np.array_equal(got, ref)
+
+
+def _one_sided(rank, world, stores, rows, d):
+    """stores[dst] = (row indices, data): every writer ships rows it addressed itself; the target
+    only scatters (and checks that no row is written twice or left empty)."""
+    sent = [None] * world
+    dist.all_gather_object(sent, stores)
+    buf = np.full((rows, d), np.nan, np.float32)
+    for s in range(world):
+        ridx, data = sent[s][rank]
+        assert np.isnan(buf[ridx]).all(), "two writers hit the same row"
+        buf[ridx] = data
+    assert not np.isnan(buf).any(), "buffer has holes"
+    return buf
+
+
+def _pack(stores):
+    return [(np.array(a, np.int64), np.array(b, np.float32).reshape(-1, stores[0][2])) for a, b, _ in stores]
+
+
+def _ep_peer_bwd_worker(rank, world, port, t, d, n, k, f, result_dir):
+    """Training over the peer transport, restated with one-sided stores: dispatch (x rows) and
+    the combine-backward kernel (dY rows) write at disp[g] + rank-in-expert of the owner; the
+    GEMM2 epilogue (Y rows) and the dgrad-2 epilogue (dX rows) write at ret[e, s] + j of the
+    source -- every address computed by the writer from cl_moe_ep_peer_layout."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.oracle import Oracle, make_inputs
+    from paper_2509_09121_b200.moe import ep_peer_layout
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    gfull = make_inputs(t * world, d, 1, f, seed=31, experts=False)["x"]
+    nl = n // world
+    xs = full["x"][rank * t:(rank + 1) * t]
+    gs = gfull[rank * t:(rank + 1) * t]
+    r = o.route(xs, full["w_router"], k)
+    idx, w = r["topk_idx"], r["combine_weights"]
+    offsets, perm, inv = o.plan(idx, n)
+    allc = [torch.zeros(n, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(allc, torch.from_numpy(np.diff(offsets).astype(np.int64)))
+    cmat = torch.stack(allc).numpy()
+    disp, ret, loc = ep_peer_layout(cmat, rank)
+
+    def to_owners(rows_src):  # source-permutation rows -> owners' receive buffers
+        st = [([], [], d) for _ in range(world)]
+        for g in range(n):
+            for j in range(offsets[g], offsets[g + 1]):
+                st[g // nl][0].append(disp[g] + j - offsets[g])
+                st[g // nl][1].append(rows_src[j])
+        return _one_sided(rank, world, _pack(st), loc[-1], d)
+
+    def to_sources(rows_recv):  # receive-layout rows -> sources' permutations
+        st = [([], [], d) for _ in range(world)]
+        row = 0
+        for e in range(nl):
+            for s in range(world):
+                cnt = cmat[s, rank * nl + e]
+                st[s][0].extend(range(ret[e, s], ret[e, s] + cnt))
+                st[s][1].extend(rows_recv[row:row + cnt])
+                row += cnt
+        return _one_sided(rank, world, _pack(st), t * k, d)
+
+    x_recv = to_owners(xs[perm // k])
+    y_recv = np.zeros_like(x_recv)
+    for e in range(nl):
+        a, b = loc[e], loc[e + 1]
+        if b > a:
+            _, y_recv[a:b] = o.expert_ffn(x_recv[a:b], full["w_in"][rank * nl + e], full["w_out"][rank * nl + e])
+    y = to_sources(y_recv)  # unweighted Y at the source (training keeps it for d(combine w))
+    wslot = w.ravel()[perm]
+    dy_src = (gs[perm // k] * wslot[:, None]).astype(np.float32)
+    dcw = np.zeros(t * k, np.float32)
+    dcw[perm] = (gs[perm // k].astype(np.float64) * y.astype(np.float64)).sum(1).astype(np.float32)
+    dy_recv = to_owners(dy_src)
+    dx_recv = np.zeros_like(x_recv)
+    dwi = np.zeros((nl, d, 2 * f), np.float32)
+    dwo = np.zeros((nl, f, d), np.float32)
+    for e in range(nl):
+        a, b = loc[e], loc[e + 1]
+        if b > a:
+            dx_recv[a:b], dwi[e], dwo[e] = o.expert_ffn_backward(x_recv[a:b], full["w_in"][rank * nl + e],
+                                                                 full["w_out"][rank * nl + e], dy_recv[a:b])
+    dx = to_sources(dx_recv)
+    dh = np.zeros((t, d), np.float32)
+    for j in range(t):
+        for kk in range(k):
+            dh[j] = dh[j] + dx[inv[j * k + kk]]
+    np.savez(os.path.join(result_dir, f"pbwd{rank}.npz"), dh=dh, dcw=dcw.reshape(t, k), dwi=dwi, dwo=dwo)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n,k", [(2, 8, 2), (4, 16, 2)])
+def test_ep_peer_transport_backward_gloo_matches_single_process_oracle(tmp_path, world, n, k):
+    t, d, f = 32, 64, 32
+    mp.spawn(_ep_peer_bwd_worker, args=(world, _free_port(), t, d, n, k, f, str(tmp_path)), nprocs=world, join=True)
+    from oracle.oracle import Oracle, make_inputs
+    o = Oracle("port")
+    full = make_inputs(t * world, d, n, f)
+    g = make_inputs(t * world, d, 1, f, seed=31, experts=False)["x"]
+    r = o.route(full["x"], full["w_router"], k)
+    rdh, rdcw, rdwi, rdwo = o.moe_backward(full["x"], full["w_in"], full["w_out"], r["topk_idx"], r["combine_weights"], g)
+    parts = [np.load(tmp_path / f"pbwd{i}.npz") for i in range(world)]
+    assert np.array_equal(np.concatenate([p_["dh"] for p_ in parts]), rdh)
+    assert np.array_equal(np.concatenate([p_["dcw"] for p_ in parts]), rdcw)
+    nl = n // world
+    for i, p_ in enumerate(parts):
+        for e in range(nl):
+            if int((r["topk_idx"] == i * nl + e).sum()):
+                assert np.array_equal(p_["dwi"][e], rdwi[i * nl + e]), (i, e)
+                assert np.array_equal(p_["dwo"][e], rdwo[i * nl + e]), (i, e)
