@@ -139,6 +139,10 @@ cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int
  * `decision` may be NULL. */
 cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
                          const cl_moe_decision* decision, void* stream);
+/* cl_moe_forward without the decision outputs, captured into a CUDA graph on first use for each
+ * (hidden, out, T, precision) and replayed afterwards (one launch per call; decode-size steps).
+ * Single-GPU layer only. The graph bakes in the buffer addresses: reuse the same buffers. */
+cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* out, void* stream);
 
 /* Same layer through HOST buffers (the reference-facing call): copies hidden in, runs the
  * layer and copies the output back; synchronous. io_dtype selects bf16 or fp32 host tensors. */

@@ -107,6 +107,7 @@ _PROTOS = {
     "cl_moe_ep_peer_init": (C.c_int, [C.c_void_p]),
     "cl_moe_ep_group_forward": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cl_moe_ep_group_train_step": (C.c_int, [C.c_void_p, C.c_int32] + [C.c_void_p] * 9),
+    "cl_moe_forward_graph": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "cl_moe_ep_last_counts": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cl_moe_ep_peer_layout": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                         C.c_void_p]),

@@ -582,6 +582,47 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, co
   });
 }
 
+// The single-GPU forward captured once per (hidden, out, T, precision) into a CUDA graph and
+// replayed: the six kernels and two counter memsets go out as one launch.
+cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* out, void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !out) throw ConfigErr("null argument");
+    if (h->comm || h->cfg.ep_size > 1) throw ConfigErr("graph capture covers the single-GPU layer only");
+    CK(cudaSetDevice(h->cfg.device));
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : h->graphs)
+      if (g.x == hidden && g.out == out && g.T == T && g.precision == h->precision) exec = g.exec;
+    if (!exec) {
+      if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      const bool prof = h->prof;
+      h->prof = false;  // no timing events inside the graph
+      CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        run_router(h, hidden, T, h->cap_stream);
+        run_experts(h, hidden, T, out, false, h->cap_stream);
+      } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(h->cap_stream, &g);
+        if (g) cudaGraphDestroy(g);
+        h->prof = prof;
+        throw;
+      }
+      h->prof = prof;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamEndCapture(h->cap_stream, &g));
+      const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+      cudaGraphDestroy(g);
+      CK(ie);
+      if (h->graphs.size() >= 16) {  // bounded cache: drop the oldest
+        cudaGraphExecDestroy(h->graphs.front().exec);
+        h->graphs.erase(h->graphs.begin());
+      }
+      h->graphs.push_back({hidden, out, T, h->precision, exec});
+    }
+    CK(cudaGraphLaunch(exec, (cudaStream_t)stream));
+  });
+}
+
 static void host_enqueue(cl_moe* h, const void* hidden_host, int64_t T, void* out_host, int32_t io_dtype) {
   if (!hidden_host || !out_host) throw ConfigErr("null argument");
   if (io_dtype != CL_MOE_IO_BF16 && io_dtype != CL_MOE_IO_F32) throw ConfigErr("io_dtype must be BF16 or F32");

@@ -124,6 +124,16 @@ struct cl_moe {
   int next_slot = 0;
   void* io_out = nullptr;              // calibration output scratch
   cudaStream_t own_stream = nullptr;   // compute stream of the host-buffer path
+  // captured forwards (cl_moe_forward_graph), keyed by buffers, T and precision
+  struct GraphEntry {
+    const void* x;
+    void* out;
+    int64_t T;
+    int precision;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   int64_t last_rows = 0;
   int tpc_cur = 32;                    // router tile (tokens) of the last routing call
@@ -214,6 +224,8 @@ struct cl_moe {
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
     if (ep_off_host) cudaFreeHost(ep_off_host);
     if (comm) NcclApi::get().CommDestroy(comm);
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
     if (own_stream) cudaStreamDestroy(own_stream);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
@@ -318,6 +330,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->gemm_auto = c->gemm_ctas == 0;
   h->gemm_ctas = c->gemm_ctas == 0 ? 2 : c->gemm_ctas;
   CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+  h->tile_counter = dalloc<int>(1);  // (allocated up front: no cudaMalloc inside a graph capture)
   CK(cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking));
   for (auto& sl : h->slot) {

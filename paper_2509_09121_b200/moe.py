@@ -150,6 +150,14 @@ class MoELayer:
                     "forward")
         return (out, dec) if want_decision else out
 
+    def forward_graph(self, hidden: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """forward() replayed from a CUDA graph captured per (hidden, out, T, precision)."""
+        hidden = self._bf16(hidden)
+        out = torch.empty_like(hidden) if out is None else out
+        self._check(self.L.cl_moe_forward_graph(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), _stream(self.device)),
+                    "forward_graph")
+        return out
+
     def forward_host(self, x: np.ndarray, io_dtype: str = "bf16") -> np.ndarray:
         """Reference-facing call on HOST buffers (H2D + layer + D2H, synchronous).
 

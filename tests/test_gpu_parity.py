@@ -358,3 +358,27 @@ def test_layer_forward_edge_shapes(gemm_ctas, t, d, n, k, f):
     rf, rm = _rel(out.float().cpu().numpy(), ref)
     assert rf <= 1e-2 and rm <= 3e-2, (rf, rm)
     lay.close()
+
+
+def test_forward_graph_replays_bit_identically():
+    """cl_moe_forward_graph: captured once per (buffers, T, precision), replayed after."""
+    t, d, n, k, f = 200, 512, 16, 2, 256
+    inp = make_inputs(t, d, n, f)
+    lay = _layer(inp, t, k)
+    x = _x_dev(inp["x"])
+    ref = lay.forward(x)
+    out = torch.empty_like(x)
+    for _ in range(3):
+        out.zero_()
+        lay.forward_graph(x, out)
+        lay.sync()
+        assert torch.equal(out, ref)
+    xs = x[:77].contiguous()  # a different T -> a second graph
+    o2 = lay.forward_graph(xs)
+    assert torch.equal(o2, lay.forward(xs))
+    lay.calibrate(x)
+    lay.quantize_fp8()  # precision is part of the key
+    ref8 = lay.forward(x)
+    lay.forward_graph(x, out)
+    lay.sync()
+    assert torch.equal(out, ref8)
