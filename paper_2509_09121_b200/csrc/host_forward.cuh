@@ -99,7 +99,7 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
-  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  launch_plan(n_tiles, (int)T, N, (int)h->K, h->rb, st);
   CK(cudaGetLastError());
   prof_mark(h, 1, st);
 }
@@ -118,7 +118,7 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
   decision_tiles_kernel<<<n_tiles, 128, 0, st>>>(h->rb.topk_idx, (int)T, N, (int)h->K, tpc, h->rb);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
-  plan_kernel<<<1, kPlanThreads, 0, st>>>(n_tiles, (int)T, N, (int)h->K, h->rb);
+  launch_plan(n_tiles, (int)T, N, (int)h->K, h->rb, st);
   CK(cudaGetLastError());
   prof_mark(h, 1, st);
 }

@@ -545,12 +545,13 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
 // K2: dispatch plan. Exclusive scan of the per-tile expert counts (tile-major within each
 // expert) -> each tile's base row inside its expert segment; expert offsets; agg_prob, aux-loss
 // and Z-loss reductions in a fixed order. One CTA; deterministic (no atomics).
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(int n_tiles, int T, int N, int K, RouteBufs rb) {
-  __shared__ int s_chunk[kPlanThreads];
-  __shared__ double s_red[kPlanThreads];
+template <int kThreads>
+__global__ void __launch_bounds__(kThreads) plan_kernel(int n_tiles, int T, int N, int K, RouteBufs rb) {
+  __shared__ int s_chunk[kThreads];
+  __shared__ double s_red[kThreads];
   __shared__ double s_p[128];
   __shared__ int s_counts[128];
-  const int chunks = kPlanThreads / N;  // chunks of tiles per expert
+  const int chunks = kThreads / N;  // chunks of tiles per expert
   const int per = (n_tiles + chunks - 1) / chunks;
   const int e = threadIdx.x % N;
   const int c = threadIdx.x / N;
@@ -593,10 +594,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(int n_tiles, int T, 
   }
   // Z-loss: fixed-order two-level reduction of the per-tile lse^2 sums.
   double z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kPlanThreads) z += rb.tile_lse2[t];
+  for (int t = threadIdx.x; t < n_tiles; t += kThreads) z += rb.tile_lse2[t];
   s_red[threadIdx.x] = z;
   __syncthreads();
-  for (int w = kPlanThreads / 2; w > 0; w >>= 1) {
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
     __syncthreads();
   }
@@ -788,6 +789,15 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
     }
   }
   if (!fin) atomicOr(finite_flag, 1);
+}
+
+// K2 launch: a 128-thread CTA when there are few tiles (decode: fewer warps, cheaper barriers),
+// 1024 threads otherwise. The fixed-order reductions depend only on (n_tiles, N).
+inline void launch_plan(int n_tiles, int T, int N, int K, const RouteBufs& rb, cudaStream_t st) {
+  if (n_tiles * N <= 1024)
+    plan_kernel<128><<<1, 128, 0, st>>>(n_tiles, T, N, K, rb);
+  else
+    plan_kernel<kPlanThreads><<<1, kPlanThreads, 0, st>>>(n_tiles, T, N, K, rb);
 }
 
 // Warp-per-token kernels (dispatch, combine): (T/8) x slices CTAs of 8 warps; small batches get
