@@ -76,54 +76,36 @@ __global__ void pad_plan_kernel(const int32_t* __restrict__ offsets, int n, int3
   kb_off[n] = p / 64;
 }
 
-// dst[c][p] = src[offsets[e] + p - poff[e]][c] for p inside expert e's padded range, 0 in the
-// padding. src is [rows][C] bf16 row-major, dst is [C][Rp_cap]. 64 x 64 tiles through smem.
-__global__ void __launch_bounds__(256) transpose_pad_kernel(const __nv_bfloat16* __restrict__ src, int C,
-                                                            const int32_t* __restrict__ offsets,
-                                                            const int32_t* __restrict__ poff, int n,
-                                                            __nv_bfloat16* __restrict__ dst, int64_t rp_cap) {
-  // 16-byte global accesses both ways; the smem row pitch of 72 bf16 (144 B) keeps the 8-row
-  // column gathers of the store phase on distinct banks.
-  __shared__ __align__(16) __nv_bfloat16 tile[64][72];
-  const int c0 = blockIdx.x * 64;
-  const int p0 = blockIdx.y * 64;
-  if (p0 >= poff[n]) return;
+// dst[p][:] = src[offsets[e] + p - poff[e]][:] inside expert e's padded row range, zeros in its
+// padding rows: the row-major padded layout the weight-gradient GEMMs read MN-major. One warp per
+// padded row, 16-byte accesses.
+__global__ void __launch_bounds__(256) pad_rows_kernel(const __nv_bfloat16* __restrict__ src, int C,
+                                                       const int32_t* __restrict__ offsets,
+                                                       const int32_t* __restrict__ poff, int n,
+                                                       __nv_bfloat16* __restrict__ dst) {
+  const int p = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= poff[n]) return;
   int e = 0;
-  while (p0 >= poff[e + 1]) ++e;
-  const int cnt = offsets[e + 1] - offsets[e];
-  const int base_row = offsets[e] + (p0 - poff[e]);
-  const int valid_p = min(64, cnt - (p0 - poff[e]));  // may be <= 0 in a pure padding block
-  // load: 64 rows (p) x 64 cols (c), 8 columns (16 B) per thread and step
-  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
-    const int pr = i >> 3, cc = (i & 7) * 8;
-    int4 v = make_int4(0, 0, 0, 0);
-    if (pr < valid_p) v = ld_nc_v4(src + (size_t)(base_row + pr) * C + c0 + cc);
-    *reinterpret_cast<int4*>(&tile[pr][cc]) = v;
-  }
-  __syncthreads();
-  // store: column c of the tile = 64 consecutive p, 8 of them (16 B) per thread and step
-  for (int i = threadIdx.x; i < 64 * 8; i += 256) {
-    const int cr = i >> 3, pp = (i & 7) * 8;
-    __align__(16) __nv_bfloat16 v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = tile[pp + j][cr];
-    *reinterpret_cast<int4*>(dst + (size_t)(c0 + cr) * rp_cap + p0 + pp) = *reinterpret_cast<const int4*>(v);
-  }
+  while (p >= poff[e + 1]) ++e;
+  const int r = p - poff[e];
+  const bool live = r < offsets[e + 1] - offsets[e];
+  const int4* s4 = reinterpret_cast<const int4*>(src + (size_t)(offsets[e] + (live ? r : 0)) * C);
+  int4* d4 = reinterpret_cast<int4*>(dst + (size_t)p * C);
+  for (int v = lane; v < C / 8; v += 32) d4[v] = live ? ld_nc_v4(s4 + v) : make_int4(0, 0, 0, 0);
 }
 
-// Zero the padding columns [poff[e] + cnt_e, poff[e+1]) of a transposed buffer [C][rp] whose data
-// columns are written by a GEMM epilogue. Grid: (C / 256, n_experts), 256 threads.
-__global__ void __launch_bounds__(256) zero_pad_cols_kernel(__nv_bfloat16* __restrict__ buf, int C, int64_t rp,
+// Zero the padding rows [poff[e] + cnt_e, poff[e+1]) of a padded row-major buffer [rp][C] whose
+// live rows are written by a GEMM epilogue. Grid (64 / 8, n_experts), 256 threads.
+__global__ void __launch_bounds__(256) zero_pad_rows_kernel(__nv_bfloat16* __restrict__ buf, int C,
                                                             const int32_t* __restrict__ offsets,
                                                             const int32_t* __restrict__ poff) {
-  // one warp per row c: the < 64 padding entries of expert e are contiguous in the row
   const int e = blockIdx.y;
-  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (c >= C) return;
-  const int64_t start = poff[e] + (offsets[e + 1] - offsets[e]);
-  const int64_t end = poff[e + 1];
-  __nv_bfloat16* row = buf + (size_t)c * rp;
-  for (int64_t k = start + (threadIdx.x & 31); k < end; k += 32) row[k] = __float2bfloat16_rn(0.0f);
+  const int start = poff[e] + (offsets[e + 1] - offsets[e]);
+  const int p = start + blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p >= poff[e + 1]) return;
+  int4* d4 = reinterpret_cast<int4*>(buf + (size_t)p * C);
+  for (int v = threadIdx.x & 31; v < C / 8; v += 32) d4[v] = make_int4(0, 0, 0, 0);
 }
 
 // dst[i][j] = src[rowmap(j)][i]: src [rows_src][cols_src] bf16 -> dst [cols_src][rows_src].

@@ -9,6 +9,8 @@
 //                    dH[r, c] = dA*U*silu'(G), dH[r, f+c] = dA*silu(G)           (bf16)
 // K-grouped mode (kWgrad; M, N = weight dims, K = the rows of expert e, variable):
 //   EPI_WGRAD        dW[e] = Lhs_e^T Rhs_e accumulated over the expert's rows    (fp32)
+//                    Both operands are read MN-major straight from row-major [rows][C] buffers
+//                    whose expert segments are padded to 64 zero rows (no transposes).
 //
 // Replaces the per-expert ops::matmul + slice_cols + silu + mul (+ mul_rowwise) chain of the
 // reference composition and its Tape backward closures (proj/src/tensor.cpp:350-375 incl. the
@@ -51,8 +53,9 @@ struct GemmArgs {
   int32_t m_tiles;          // kWgrad: m-tiles per expert
   int64_t out_estride;      // kWgrad: elements between consecutive experts' outputs
   int* tile_counter;        // dynamic tile scheduler: global counter, zeroed before the launch
-  void* aux_t;              // training: transposed copy of the output, bf16 [C][rp] (nullable)
-  int64_t rp;               // row stride of aux_t (padded-row capacity)
+  void* aux_t;              // training: copy of the output in the padded row layout, bf16 [rp][C]
+                            // (expert e's rows from poff[e]; operand of the weight gradients)
+  int64_t rp;               // padded-row capacity of aux_t
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
   void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
   int32_t m_group;          // row-grouped tile order: m-tiles per group (0 = all), see decode_tile
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int S = Cfg::kStages;
   constexpr int kUmmaKBytes = 32;                    // 16 bf16 or 32 e4m3 per MMA
   constexpr int kMmaPerKb = kBKBytes / kUmmaKBytes;  // 4
-  constexpr uint32_t kIdesc = idesc_f32acc<kFp8>(Cfg::kBM, kBN);
+  constexpr uint32_t kIdesc = idesc_f32acc<kFp8>(Cfg::kBM, kBN) | (kWgrad ? kIdescMnMajorAB : 0u);
   constexpr uint32_t kIdescHalf = idesc_f32acc<kFp8>(128, kBN);  // 2-CTA tail tiles
   constexpr int kElemBytes = kFp8 ? 1 : 2;
   constexpr int kBKElems = kBKBytes / kElemBytes;
@@ -322,7 +325,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
-          if constexpr (kCtaGroup == 1) {
+          if constexpr (kWgrad) {
+            // MN-major operands: boxes {64 columns, 64 rows} of the padded row-major buffers;
+            // a_row / b_row are column offsets here, the k-block is a block of 64 rows
+            if (kCtaGroup == 1 || cta_rank == 0) mbar_arrive_expect_tx(&full[s], kCtaGroup * Cfg::kStageBytes);
+#pragma unroll
+            for (int c = 0; c < Cfg::kRowsPerCta / 64; ++c) {
+              if constexpr (kCtaGroup == 1)
+                tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA + c * 8192, a_row + c * 64, kb * 64, kAHint);
+              else
+                tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA + c * 8192, a_row + c * 64, kb * 64, kAHint);
+            }
+#pragma unroll
+            for (int c = 0; c < Cfg::kBRowsPerCta / 64; ++c) {
+              if constexpr (kCtaGroup == 1)
+                tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64, kEvictNormal);
+              else
+                tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64,
+                                 kEvictNormal);
+            }
+          } else if constexpr (kCtaGroup == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
             tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
             tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
@@ -355,11 +377,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < ti.nkb; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t adesc = sdesc_k_sw128(smem_u32(sA + s * Cfg::kStageA));
-          const uint64_t bdesc = sdesc_k_sw128(smem_u32(sB + s * Cfg::kStageB));
+          // K-major: a K=16 step is 32 B along the swizzled row; MN-major (weight gradients): 16 rows
+          const uint64_t adesc = kWgrad ? sdesc_mn_sw128(smem_u32(sA + s * Cfg::kStageA), 8192)
+                                        : sdesc_k_sw128(smem_u32(sA + s * Cfg::kStageA));
+          const uint64_t bdesc = kWgrad ? sdesc_mn_sw128(smem_u32(sB + s * Cfg::kStageB), 8192)
+                                        : sdesc_k_sw128(smem_u32(sB + s * Cfg::kStageB));
+          constexpr int kStepBytes = kWgrad ? 16 * 128 : kUmmaKBytes;
 #pragma unroll
           for (int k = 0; k < kMmaPerKb; ++k) {
-            const uint64_t koff = static_cast<uint64_t>((k * kUmmaKBytes) >> 4);
+            const uint64_t koff = static_cast<uint64_t>((k * kStepBytes) >> 4);
             mma_ss<kCtaGroup, kFp8>(d_tmem, adesc + koff, bdesc + koff, idesc, (kb | k) != 0);
           }
           mma_commit<kCtaGroup>(&empty[s]);
@@ -423,8 +449,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               store_bf16x32(hrow + col, gv);
               store_bf16x32(hrow + args.ffn + col, uv);
             }
-            if (args.aux_t)  // training: A^T (padded K-major) for the dW_out gradient GEMM
-              store_t_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)col * args.rp + prow, args.rp, v);
+            if (args.aux_t)  // training: A in the padded row layout (dW_out gradient operand)
+              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)prow * args.ffn + col, v);
           }
         };
         if (kCtaGroup == 2 && ti.half) {
@@ -579,10 +605,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * (2 * args.ffn);
             store_bf16x32(drow + col, dg);
             store_bf16x32(drow + args.ffn + col, du);
-            if (args.aux_t) {  // dH^T (padded K-major) for the dW_in gradient GEMM
-              __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(args.aux_t) + prow;
-              store_t_bf16x32(t + (size_t)col * args.rp, args.rp, dg);
-              store_t_bf16x32(t + (size_t)(args.ffn + col) * args.rp, args.rp, du);
+            if (args.aux_t) {  // dH in the padded row layout (dW_in gradient operand)
+              __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)prow * (2 * args.ffn);
+              store_bf16x32(t + col, dg);
+              store_bf16x32(t + args.ffn + col, du);
             }
           }
         }

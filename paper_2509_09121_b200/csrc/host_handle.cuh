@@ -190,7 +190,9 @@ struct cl_moe {
   __nv_bfloat16* dYbuf = nullptr;       // [cap*K][d]
   __nv_bfloat16* dHbuf = nullptr;       // [cap*K][2f]
   __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
-  __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;  // [C][rp_cap]
+  // weight-gradient operands in the padded row layout [rp_cap][C] (expert e's rows from poff[e],
+  // zero padding rows): X, A (= SwiGLU output), dY, dH
+  __nv_bfloat16 *XT = nullptr, *AT = nullptr, *dYT = nullptr, *dHT = nullptr;
   int32_t* poff = nullptr;              // [NL+1]
   int* tile_counter = nullptr;          // grouped-GEMM dynamic tile scheduler
   float* rdz = nullptr;                 // router backward: dz [cap][N] fp32

@@ -37,10 +37,11 @@ void ensure_training(cl_moe* h) {
       h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
       h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
       h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
-      h->mAwo[v] = make_map(h->AT, false, h->rp_cap, f, 128);
-      h->mBwo[v] = make_map(h->dYT, false, h->rp_cap, d, brow);
-      h->mAwi[v] = make_map(h->XT, false, h->rp_cap, d, 128);
-      h->mBwi[v] = make_map(h->dHT, false, h->rp_cap, 2 * f, brow);
+      // weight-gradient operands, MN-major: boxes of 64 columns x 64 padded rows
+      h->mAwo[v] = make_map(h->AT, false, f, h->rp_cap, 64);
+      h->mBwo[v] = make_map(h->dYT, false, d, h->rp_cap, 64);
+      h->mAwi[v] = make_map(h->XT, false, d, h->rp_cap, 64);
+      h->mBwi[v] = make_map(h->dHT, false, 2 * f, h->rp_cap, 64);
     }
   }
   // reference-layout weight copies (re-derived whenever the packed weights change)
@@ -217,15 +218,13 @@ void bwd_phase_d(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   //    dW_out[e] = A_e^T dY_e ([f x d]) and dW_in[e] = X_e^T dH_e ([d x 2f]), fp32.
   //    (A^T and dH^T were written by the GEMM1 / dgrad-1 epilogues; only their padding columns
   //    need zeroing. X^T and dY^T go through the transpose kernel.)
-  const unsigned pb = static_cast<unsigned>(h->rp_cap / 64);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d,
-                                                                     es_off, h->poff, NL, h->XT, h->rp_cap);
-  transpose_pad_kernel<<<dim3((unsigned)(d / 64), pb), 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT,
-                                                                     h->rp_cap);
-  zero_pad_cols_kernel<<<dim3((unsigned)((f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, h->rp_cap, es_off,
-                                                                                    h->poff);
-  zero_pad_cols_kernel<<<dim3((unsigned)((2 * f + 7) / 8), (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f),
-                                                                                        h->rp_cap, es_off, h->poff);
+  // padded row-major operands of the weight gradients: X and dY copied into the padded row
+  // layout; A and dH were written there by the GEMM1 / dgrad-1 epilogues (zero their padding)
+  const unsigned pr = static_cast<unsigned>(h->rp_cap / 8);
+  pad_rows_kernel<<<pr, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d, es_off, h->poff, NL, h->XT);
+  pad_rows_kernel<<<pr, 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT);
+  zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, es_off, h->poff);
+  zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f), es_off, h->poff);
   CK(cudaGetLastError());
   prof_mark(h, 4, st);
   const int gw = (f % 256 == 0) ? 2 : 1;

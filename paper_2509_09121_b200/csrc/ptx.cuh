@@ -197,6 +197,21 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
 
 // Instruction descriptor for kind::f16 (A/B = BF16) or kind::f8f6f4 (A/B = E4M3), FP32 accumulate,
 // both operands K-major.
+// Shared-memory matrix descriptor, MN-major operand in the 128-byte-swizzle layout produced by a
+// TMA box {64 elements along MN (inner), K rows}: the operand is a sequence of 64-element MN
+// chunks, each K rows x 128 B; LBO = bytes between MN chunks, SBO = 1024 (8 K rows). One K=16
+// MMA step advances the start address by 16 rows x 128 B. (Validated by tools/mn_major_probe.cu.)
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t saddr, uint32_t chunk_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((chunk_bytes >> 4) & 0x3FFFu) << 16;  // LBO
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;                    // SBO
+  d |= static_cast<uint64_t>(1u) << 46;                            // version
+  d |= static_cast<uint64_t>(2u) << 61;                            // SWIZZLE_128B
+  return d;
+}
+constexpr uint32_t kIdescMnMajorAB = (1u << 15) | (1u << 16);  // A and B MN-major
+
 template <bool kFp8>
 __host__ __device__ constexpr uint32_t idesc_f32acc(uint32_t M, uint32_t N) {
   return (1u << 4)                          // D format F32
