@@ -11,7 +11,9 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcompass_moe.so")
+# CL_MOE_LIB_VARIANT=<name> loads libcompass_moe.<name>.so from the same directory (A/B builds)
+LIB_PATH = os.path.join(HERE, "libcompass_moe.so" if not os.environ.get("CL_MOE_LIB_VARIANT")
+                        else f"libcompass_moe.{os.environ['CL_MOE_LIB_VARIANT']}.so")
 CSRC = os.path.join(HERE, "csrc")
 
 CL_OK, CL_ERR_RUN, CL_ERR_CONFIG = 0, 1, 2

@@ -68,7 +68,7 @@ constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; 
 constexpr int kEpiWarps = 8;      // two warps per TMEM lane quarter, each owning half of the columns
 constexpr int kBN = 256;                 // MMA N (output columns of one tile, pre-SwiGLU)
 constexpr int kBKBytes = 128;            // one swizzle atom along K
-constexpr int kMaxExperts = 256;
+constexpr int kMaxExperts = 128;  // experts per rank (cl_moe validates N <= 128)
 constexpr int kTileSlots = 4;            // depth of the tile-index broadcast ring
 
 template <int kCtaGroup>
@@ -83,7 +83,9 @@ struct GemmCfg {
   // half tiles (2-CTA): gate/up exchange between TMEM lane halves, [64 rows][129 fp32] (padded)
   static constexpr int kXStride = 129;
   static constexpr int kXBytes = kCtaGroup == 2 ? 64 * kXStride * 4 : 0;
-  static constexpr int kSmemCtl = 1024 /*align*/ + 256 /*barriers*/ + (kMaxExperts + 1) * 4;
+  // per-expert tables cached in smem (tile prefix + row / k-block offsets): a tile decode must not
+  // wait on global memory, or the MMA issuer idles the tensor pipe between tiles
+  static constexpr int kSmemCtl = 1024 /*align*/ + 256 /*barriers*/ + 2 * (kMaxExperts + 1) * 4;
   static constexpr int kSmem = kStages * kStageBytes + kSmemCtl + kXBytes;
   static_assert(kSmem <= 232448, "shared memory budget");
 };
@@ -101,7 +103,8 @@ struct TileInfo {
 // in groups of m_group; inside a group m is fastest and the group sweeps every n-block before the
 // next group starts. The group's A rows stay resident in L2 while the weight n-blocks stream past
 // (an expert whose rows exceed L2 would otherwise re-stream its rows for every n-block).
-__device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, const GemmArgs& a, int bm, TileInfo& ti) {
+__device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, const int* s_off, const GemmArgs& a, int bm,
+                                            TileInfo& ti) {
   if (tile >= mt_prefix[a.n_experts] * a.n_tiles_n) return false;
   int e = 0;
   while (tile >= mt_prefix[e + 1] * a.n_tiles_n) ++e;
@@ -114,9 +117,9 @@ __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, cons
   ti.e = e;
   ti.nt = within / gsz;
   ti.mt = g * gm + (within - ti.nt * gsz);
-  ti.a_row = a.offsets[e] + ti.mt * bm;
+  ti.a_row = s_off[e] + ti.mt * bm;
   ti.b_row = e * a.b_rows_per_expert + ti.nt * kBN;
-  ti.row_end = a.offsets[e + 1];
+  ti.row_end = s_off[e + 1];
   ti.kb0 = 0;
   ti.nkb = a.num_kb;
   ti.half = a.half_tail && ti.row_end - ti.a_row <= bm / 2;
@@ -127,12 +130,12 @@ __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, cons
 // is the expert's padded row range, so its operand slabs grow with its row count. m-tiles go in
 // groups whose A slabs fit `group_bytes` of L2 (m fastest inside, sweeping every n-block), as in
 // decode_tile: a hot expert's A slab is then read once instead of once per n-block.
-__device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, int bm, TileInfo& ti) {
+__device__ __forceinline__ bool decode_tile_wgrad(int tile, const int* s_kb, const GemmArgs& a, int bm, TileInfo& ti) {
   const int per = a.m_tiles * a.n_tiles_n;
   if (tile >= a.n_experts * per) return false;
   const int e = tile / per;
   const int local = tile - e * per;
-  const int nkb = a.kb_off[e + 1] - a.kb_off[e];
+  const int nkb = s_kb[e + 1] - s_kb[e];
   int gm = a.m_tiles;
   if (a.group_bytes > 0 && nkb > 0) {
     const int64_t g = a.group_bytes / ((int64_t)bm * nkb * kBKBytes);
@@ -147,8 +150,8 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const GemmArgs& a, i
   ti.a_row = ti.mt * bm;
   ti.b_row = ti.nt * kBN;
   ti.row_end = 1 << 30;
-  ti.kb0 = a.kb_off[e];
-  ti.nkb = a.kb_off[e + 1] - a.kb_off[e];
+  ti.kb0 = s_kb[e];
+  ti.nkb = nkb;
   ti.half = false;
   return true;
 }
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   int* tile_ring = reinterpret_cast<int*>(tfree + kTileSlots);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileSlots);
   int* mt_prefix = reinterpret_cast<int*>(smem + S * Cfg::kStageBytes + 256);
+  int* s_off = mt_prefix + (kMaxExperts + 1);  // expert row offsets (row-grouped) or k-block offsets (kWgrad)
   float* xbuf = reinterpret_cast<float*>(smem + S * Cfg::kStageBytes + Cfg::kSmemCtl - 1024);
 
   const uint32_t warp = warp_id();
@@ -237,6 +241,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int cluster = kCtaGroup == 1 ? blockIdx.x : cluster_id_x();
   const int nclusters = kCtaGroup == 1 ? gridDim.x : nclusters_x();
 
+  for (int i = threadIdx.x; i <= args.n_experts; i += blockDim.x) s_off[i] = kWgrad ? args.kb_off[i] : args.offsets[i];
   if (!kWgrad && threadIdx.x == 0) {
     int acc = 0;
     mt_prefix[0] = 0;
@@ -274,8 +279,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto decode = [&](int tile, TileInfo& ti) -> bool {
-    if constexpr (kWgrad) return decode_tile_wgrad(tile, args, Cfg::kBM, ti);
-    else return decode_tile(tile, mt_prefix, args, Cfg::kBM, ti);
+    if constexpr (kWgrad) return decode_tile_wgrad(tile, s_off, args, Cfg::kBM, ti);
+    else return decode_tile(tile, mt_prefix, s_off, args, Cfg::kBM, ti);
   };
   const int total_tiles = kWgrad ? args.n_experts * args.m_tiles * args.n_tiles_n : mt_prefix[args.n_experts] * args.n_tiles_n;
   // Dynamic in-order tile scheduler: the leader's producer takes tiles from a global counter and
