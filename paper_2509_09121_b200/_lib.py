@@ -136,6 +136,8 @@ def lib():
             build()
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _PROTOS.items():
+            if os.environ.get("CL_MOE_LIB_VARIANT") and not hasattr(L, name):
+                continue  # an older A/B build may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
