@@ -51,8 +51,8 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
   // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
   static const int force = [] {
-    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "lat", "small" or "big"
-    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : 0) : 0;
+    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "ws", "lat", "small" or "big"
+    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : e[0] == 'w' ? 4 : 0) : 0;
   }();
   // large batches: 4 tokens x 4 experts per thread when that still gives >= 3 CTAs per SM, else
   // 2 x 4 (2x the CTAs, e.g. C3's 8192 tokens); CL_MOE_BIG_TOK=2|4 pins the choice (benchmarks)
@@ -69,14 +69,33 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
   const int N4r = (N + 3) / 4 * 4;
   const int lat_chunk = N4r <= 16 ? 256 : N4r <= 32 ? 128 : 64;
   const int tpc_lat = RouterLatSmem<3, 64>(N).tpc;
-  const bool lat = !big && (force == 3 || (force == 0 && (T + tpc_lat - 1) / tpc_lat <= h->num_sms));
-  const bool small = !big && !lat && router_smem_bytes(N, 32, 8) <= 220 * 1024;
-  const int tpc = big ? tpc_big : lat ? tpc_lat : router_tokens_per_cta(N, small ? 32 : 128);
+  const bool lat_size = (T + tpc_lat - 1) / tpc_lat <= h->num_sms;
+  // decode-size batches: the warp-specialised chain kernel (ws), on the smallest CTA (32 / 64 / 128
+  // chain threads) that still gives every CTA its own SM; CL_MOE_ROUTER=lat keeps the older variant
+  const bool ws = !big && (force == 4 || (force == 0 && lat_size));
+  const bool lat = !big && !ws && (force == 3 || (force == 0 && lat_size));
+  int ws_cons = 128;
+  for (int c : {32, 64}) {
+    const int tp = RouterWsSmem(N, c).tpc;
+    if (ws_cons == 128 && tp >= 1 && (T + tp - 1) / tp <= h->num_sms) ws_cons = c;
+  }
+  const bool small = !big && !lat && !ws && router_smem_bytes(N, 32, 8) <= 220 * 1024;
+  const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons).tpc : lat ? tpc_lat
+                                 : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   prof_begin(h, st);
-  if (lat && lat_chunk == 256)
+  if (ws && ws_cons == 32)
+    router_ws_kernel<32><<<n_tiles, 32 + 64, RouterWsSmem(N, 32).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (ws && ws_cons == 64)
+    router_ws_kernel<64><<<n_tiles, 64 + 64, RouterWsSmem(N, 64).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (ws)
+    router_ws_kernel<128><<<n_tiles, 128 + 64, RouterWsSmem(N, 128).total, st>>>(
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  else if (lat && lat_chunk == 256)
     router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   else if (lat && lat_chunk == 128)

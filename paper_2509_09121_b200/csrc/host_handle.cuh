@@ -85,7 +85,7 @@ struct cl_moe {
 
   // weights
   float* wr = nullptr;                 // [d][N] fp32
-  double* wr64 = nullptr;              // [d][N4] fp64 copy streamed by the router
+  double* wr64 = nullptr;              // [d][N4] fp64 copy streamed by the router, then [N4][d]
   __nv_bfloat16* win = nullptr;        // [n_local][2f][d] packed
   __nv_bfloat16* wout = nullptr;       // [n_local][d][f] packed
   uint8_t* win8 = nullptr;             // e4m3 copies
@@ -344,7 +344,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   const int64_t rows = h->cap * h->K;
   const int tpc = std::min({router_tokens_per_cta(static_cast<int>(h->N), 32),
                             RouterBigSmem(static_cast<int>(h->N), 32, 3, 2).tpc,
-                            RouterLatSmem<3, 64>(static_cast<int>(h->N)).tpc});  // smallest tile of any variant
+                            RouterLatSmem<3, 64>(static_cast<int>(h->N)).tpc,
+                            std::max(1, RouterWsSmem(static_cast<int>(h->N), 32).tpc)});  // smallest tile of any variant
   h->n_tiles_cap = static_cast<int>((h->cap + tpc - 1) / tpc);
   RouteBufs& rb = h->rb;
   rb.logits = dalloc<float>(h->cap * h->N);
@@ -371,7 +372,7 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->row_w = dalloc<float>(rows);
 
   h->wr = dalloc<float>(h->d * h->N);
-  h->wr64 = dalloc<double>(h->d * ((h->N + 3) / 4 * 4));
+  h->wr64 = dalloc<double>(3 * h->d * ((h->N + 3) / 4 * 4));  // [d][N4] + the router_ws layout (<= 2x)
   CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -379,6 +380,9 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);

@@ -64,12 +64,25 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// W_r [d][N] fp32 -> fp64 [d][N4] (zero-padded experts), once per handle.
+// Chunk length (steps) of router_ws_kernel's ring, by padded expert count.
+__host__ __device__ inline int router_ws_chunk(int N4) { return N4 <= 16 ? 256 : N4 <= 32 ? 128 : N4 <= 64 ? 64 : 32; }
+
+// W_r [d][N] fp32 -> fp64 [d][N4] (zero-padded experts), followed by the layout router_ws_kernel
+// streams: per chunk of router_ws_chunk(N4) steps, [N4][chunk + 2] expert-major rows (2 pad
+// doubles per row so a warp's experts hit distinct banks) — one contiguous bulk copy per ring
+// slot. Once per weight update.
 __global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, double* __restrict__ out) {
   const int N4 = (N + 3) / 4 * 4;
+  const int chunk = router_ws_chunk(N4), pitch = chunk + 2;
+  double* wt = out + (size_t)d * N4;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * N4; i += gridDim.x * blockDim.x) {
     const int l = i / N4, e = i % N4;
-    out[i] = e < N ? static_cast<double>(wr[(size_t)l * N + e]) : 0.0;
+    const double v = e < N ? static_cast<double>(wr[(size_t)l * N + e]) : 0.0;
+    out[i] = v;
+    const int c = l / chunk, j = l % chunk;
+    double* row = wt + ((size_t)c * N4 + e) * pitch;
+    row[j] = v;
+    if (j == 0) row[chunk] = row[chunk + 1] = 0.0;
   }
 }
 
@@ -411,6 +424,323 @@ __global__ void __launch_bounds__(128) router_lat_kernel(const __nv_bfloat16* __
   }
   __syncthreads();
   router_finish(tile, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb, kThreads);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1, warp-specialised latency variant (decode-size batches; replaces the barrier-paced ring of
+// router_lat_kernel). Same chains (one thread per (token, expert), ascending l), fed by a deep
+// ring so the chains never wait on global memory:
+//   producer warp:  1-D TMA bulk copies, per ring slot, of the W_r chunk (one contiguous copy of
+//                   the padded expert-major layout widen_router_kernel writes) and of each token's
+//                   x chunk; completion on full[s]; sleeps while the ring is full;
+//   converter warp: widens the slot's x chunk to fp64 once for all experts (F2F runs at
+//                   15/clk/SM: kept off the chains' SM sub-partition) -> xready[s];
+//   chain warps:    per 256-step chunk, run the chain from a register ring filled 16 steps ahead
+//                   (two steps per 16-byte load of each operand), then publish the slot as free.
+//                   The next slot's flag is read when a chunk starts, so the check overlaps the
+//                   chain instead of stalling it.
+// The chain step is one asm block (the FMA, then on odd steps the two ring loads), which pins the
+// interleaving in PTX: measured 9.2 cycles per step against 8.5 for operands already in registers
+// and 11.9 for the [l][e] layout with a runtime stride (tools/chain_ring_probe.cu).
+// kCons (chain threads) is 32, 64 or 128: the host picks the smallest that keeps one CTA per SM, so
+// a decode batch spreads over the most SMs. The per-token softmax / top-K runs one warp per token.
+struct RouterWsSmem {
+  static constexpr int kMaxStages = 12;
+  static constexpr int kAhead = 16;  // ring distance (steps); loads run up to kAhead past a row
+  int tpc, N4, chunk, wpitch, stages;
+  size_t sw, rx, xd, bars, slog, sidx, slse, total;
+  __host__ __device__ RouterWsSmem(int n_experts, int cons) {
+    N4 = (n_experts + 3) / 4 * 4;
+    tpc = cons / N4;
+    chunk = router_ws_chunk(N4);
+    wpitch = chunk + 2;  // doubles per expert row
+    // as many ring slots as ~200 KB allow (the producer runs several L2 round trips ahead)
+    const size_t slot = (size_t)N4 * wpitch * 8 + ((size_t)tpc * chunk * 2 + 15) / 16 * 16 + (size_t)tpc * chunk * 8;
+    const size_t fixed = 4096;
+    stages = (int)(((size_t)200 * 1024 - fixed) / slot);
+    stages = stages < 2 ? 2 : stages > kMaxStages ? kMaxStages : stages;
+    sw = 0;                                                          // [stages][N4][wpitch] fp64
+    rx = sw + (size_t)stages * N4 * wpitch * 8;                      // [stages][tpc][chunk] bf16
+    xd = rx + ((size_t)stages * tpc * chunk * 2 + 15) / 16 * 16;     // [stages][tpc][chunk] fp64
+    bars = xd + (size_t)stages * tpc * chunk * 8;                    // full[kMaxStages] + flags
+    slog = bars + kMaxStages * 8 + (kMaxStages + 4) * 4;
+    sidx = slog + sizeof(float) * tpc * N4;
+    slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
+    total = slse + sizeof(double) * tpc + kAhead * 8;  // guard for the ring's overrun past the last row
+  }
+};
+
+// One chain step: acc = fma(xx, ww, acc); on odd steps also the next x / W pairs of the ring.
+__device__ __forceinline__ void ws_step(double& acc, double xx, double ww) {
+  asm volatile("fma.rn.f64 %0, %1, %2, %0;" : "+d"(acc) : "d"(xx), "d"(ww));
+}
+__device__ __forceinline__ void ws_step_ld(double& acc, double xx, double ww, double& x0, double& x1, double& w0,
+                                           double& w1, uint32_t xa, uint32_t wa) {
+  asm volatile(
+      "fma.rn.f64 %0, %5, %6, %0;\n\t"
+      "ld.shared.v2.f64 {%1, %2}, [%7];\n\t"
+      "ld.shared.v2.f64 {%3, %4}, [%8];"
+      : "+d"(acc), "=d"(x0), "=d"(x1), "=d"(w0), "=d"(w1)
+      : "d"(xx), "d"(ww), "r"(xa), "r"(wa)
+      : "memory");
+}
+
+// Per-token softmax / top-K / combine weights with one warp per token (lanes own experts), then the
+// per-tile statistics. Same arithmetic as router_finish: the max is order-free, the fp64 softmax
+// denominator and the top-K weight sum are accumulated in ascending order (every lane runs the same
+// sequence over shuffled terms), and top-K is an argmax with the lowest index winning ties. A row
+// with a NaN probability takes the sequential path on lane 0 (its NaN semantics are positional).
+__device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc, int T, int N, int N4, int K,
+                                                    float* slog, int* sidx, double* slse, const RouteBufs& rb) {
+  const int ntok = min(tpc, T - tok0);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  constexpr unsigned kAll = 0xffffffffu;
+  for (int tl = warp; tl < tpc; tl += nwarps) {
+    double lse2 = 0.0;
+    if (tl < ntok) {
+      const int j = tok0 + tl;
+      float* zrow = slog + tl * N4;
+      double mx = zrow[0];
+      for (int e = lane; e < N; e += 32) mx = fmax(mx, static_cast<double>(zrow[e]));
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kAll, mx, o));
+      double ex[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = q * 32 + lane;
+        if (q * 32 < N && e < N) ex[q] = exp(static_cast<double>(zrow[e]) - mx);
+      }
+      // ascending-e sum: every lane adds the same shuffled terms in the same order
+      double denom = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q * 32 >= N) break;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const double v = __shfl_sync(kAll, ex[q], i);
+          if (q * 32 + i < N) denom += v;
+        }
+      }
+      float pv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      bool nan = false;
+      __syncwarp();  // every lane has read zrow (logits) before it is overwritten with probs
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = q * 32 + lane;
+        if (q * 32 >= N) break;
+        pv[q] = static_cast<float>(ex[q] / denom);
+        if (e < N) {
+          rb.probs[(size_t)j * N + e] = pv[q];
+          zrow[e] = pv[q];  // the row now holds probs
+          nan |= isnan(pv[q]);
+        }
+      }
+      const double lse = mx + log(denom);
+      lse2 = lse * lse;
+      if (!__any_sync(kAll, nan)) {
+        // K rounds of a warp argmax: probs are >= +0 and not NaN, so their bit patterns order like
+        // the values; the lowest index wins ties (the reference's strict '>' scan)
+        unsigned taken = 0;  // bit q: this lane's expert q*32+lane is taken
+        float myv = 0.0f;    // lane k keeps round k's winner
+        int myi = 0;
+        double sum = 0.0;    // sum of the winners in round order, as the reference
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k >= K) break;
+          unsigned key = 0;
+          int best = -1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = q * 32 + lane;
+            const unsigned kq = __float_as_uint(pv[q]);
+            if (e < N && !((taken >> q) & 1u) && (best < 0 || kq > key)) { best = e; key = kq; }
+          }
+          const unsigned m = __reduce_max_sync(kAll, best >= 0 ? key : 0u);
+          const int win = static_cast<int>(
+              __reduce_min_sync(kAll, (best >= 0 && key == m) ? static_cast<unsigned>(best) : 0x7fffffffu));
+          if ((win & 31) == lane) taken |= 1u << (win >> 5);
+          const float bv = __uint_as_float(m);
+          if (lane == k) {
+            myv = bv;
+            myi = win;
+          }
+          sum += static_cast<double>(bv);
+        }
+        if (lane < K) {
+          rb.topk_idx[(size_t)j * K + lane] = myi;
+          rb.combine_w[(size_t)j * K + lane] = static_cast<float>(static_cast<double>(myv) / sum);
+          sidx[tl * 8 + lane] = myi;
+        }
+      } else if (lane == 0) {  // sequential reference order (rows with a NaN probability)
+        float vals[8];
+        int ids[8];
+        uint64_t taken_lo = 0, taken_hi = 0;
+        for (int k = 0; k < K; ++k) {
+          int best = -1;
+          float bv = 0.0f;
+          for (int e = 0; e < N; ++e) {
+            const bool tk = e < 64 ? ((taken_lo >> e) & 1ull) : ((taken_hi >> (e - 64)) & 1ull);
+            if (tk) continue;
+            const float v = zrow[e];
+            if (best < 0 || v > bv) { best = e; bv = v; }
+          }
+          if (best < 64) taken_lo |= 1ull << best; else taken_hi |= 1ull << (best - 64);
+          vals[k] = bv;
+          ids[k] = best;
+        }
+        double sum = 0.0;
+        for (int k = 0; k < K; ++k) sum += static_cast<double>(vals[k]);
+        for (int k = 0; k < K; ++k) {
+          rb.topk_idx[(size_t)j * K + k] = ids[k];
+          rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / sum);
+          sidx[tl * 8 + k] = ids[k];
+        }
+      }
+    }
+    if (lane == 0) slse[tl] = lse2;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    int cnt = 0;
+    double ps = 0.0;
+    for (int t = 0; t < ntok; ++t) {
+      ps += static_cast<double>(slog[t * N4 + e]);
+      for (int k = 0; k < K; ++k)
+        if (sidx[t * 8 + k] == e) rb.local_rank[(size_t)(tok0 + t) * K + k] = cnt++;
+    }
+    rb.tile_cnt[(size_t)tile * N + e] = cnt;
+    rb.tile_psum[(size_t)tile * N + e] = ps;
+  }
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < ntok; ++t) a += slse[t];
+    rb.tile_lse2[tile] = a;
+  }
+}
+
+template <int kCons>
+__global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                 const double* __restrict__ wr64, int T, int d,
+                                                                 int N, int K, RouteBufs rb) {
+  constexpr int kD = RouterWsSmem::kAhead, kB = 32;
+  const RouterWsSmem L(N, kCons);
+  const int N4 = L.N4, tpc = L.tpc, chunk = L.chunk, wpitch = L.wpitch, kStages = L.stages;
+  const double* wt = wr64 + (size_t)d * N4;  // per chunk [N4][wpitch] (widen_router_kernel)
+  const int tok0 = blockIdx.x * tpc;
+  const int ntok = min(tpc, T - tok0);
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  double* sw = reinterpret_cast<double*>(smem_raw + L.sw);
+  __nv_bfloat16* rawx = reinterpret_cast<__nv_bfloat16*>(smem_raw + L.rx);
+  double* xd = reinterpret_cast<double*>(smem_raw + L.xd);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
+  // the chain side synchronises through chunk-granular flags (CTA-scope release stores / acquire
+  // loads) rather than mbarriers:
+  //   xflag[s] = c + 1 once the converter has widened chunk c into slot s (release);
+  //   eflag[w] = number of chunks chain warp w has finished (release).
+  int* xflag = reinterpret_cast<int*>(full + RouterWsSmem::kMaxStages);
+  int* eflag = xflag + RouterWsSmem::kMaxStages;
+  float* slog = reinterpret_cast<float*>(smem_raw + L.slog);
+  int* sidx = reinterpret_cast<int*>(smem_raw + L.sidx);
+  double* slse = reinterpret_cast<double*>(smem_raw + L.slse);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      xflag[s] = 0;
+    }
+    for (int w = 0; w < kCons / 32; ++w) eflag[w] = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunks = d / chunk;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (warp == kCons / 32 + 1) {  // producer
+    if (lane == 0) {
+      const uint32_t wbytes = N4 * wpitch * 8, xbytes = chunk * 2;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % kStages;
+        if (c >= kStages)  // sleep-poll until every chain warp has finished chunk c - kStages
+          for (int w = 0; w < kCons / 32; ++w)
+            while (ld_acquire_cta(&eflag[w]) <= c - kStages) __nanosleep(128);
+        mbar_arrive_expect_tx(&full[s], wbytes + ntok * xbytes);
+        bulk_g2s(sw + (size_t)s * N4 * wpitch, wt + (size_t)c * N4 * wpitch, wbytes, &full[s]);
+        for (int r = 0; r < ntok; ++r)
+          bulk_g2s(rawx + ((size_t)s * tpc + r) * chunk, x + (size_t)(tok0 + r) * d + (size_t)c * chunk, xbytes,
+                   &full[s]);
+      }
+    }
+  } else if (warp == kCons / 32) {  // converter
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % kStages;
+      mbar_wait(&full[s], (c / kStages) & 1);
+      const __nv_bfloat16* rx = rawx + (size_t)s * tpc * chunk;
+      double* xo = xd + (size_t)s * tpc * chunk;
+      for (int i = lane * 8; i < ntok * chunk; i += 32 * 8) {
+        const int4 raw = *reinterpret_cast<const int4*>(rx + i);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 8; j += 2)
+          *reinterpret_cast<double2*>(xo + i + j) = make_double2(static_cast<double>(__bfloat162float(hv[j])),
+                                                                 static_cast<double>(__bfloat162float(hv[j + 1])));
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cta(&xflag[s], c + 1);  // publishes the widened x and, by cumulativity,
+    }                                                    // the W chunk this warp acquired via full[s]
+  } else {  // chain warps
+    const int tl = threadIdx.x / N4, e = threadIdx.x % N4;
+    const bool worker = tl < ntok;
+    double acc = 0.0;
+    bool ready = false;  // the current chunk's flag already observed (acquired) one chunk earlier
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % kStages;
+      if (!ready)
+        while (ld_acquire_cta(&xflag[s]) <= c) {
+        }
+      // look at the next slot now: the flag read's latency overlaps this chunk's chain
+      ready = c + 1 < nchunks && ld_acquire_cta(&xflag[(c + 1) % kStages]) > c + 1;
+      if (worker) {
+        const double* xr = xd + ((size_t)s * tpc + tl) * chunk;
+        const double* we = sw + ((size_t)s * N4 + e) * wpitch;
+        double xa[kD], wa[kD];
+#pragma unroll
+        for (int i = 0; i < kD; i += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(xr + i);
+          const double2 u = *reinterpret_cast<const double2*>(we + i);
+          xa[i] = t.x;
+          xa[i + 1] = t.y;
+          wa[i] = u.x;
+          wa[i + 1] = u.y;
+        }
+        const uint32_t xs = smem_u32(xr), ws = smem_u32(we);
+        // loads past the row end (last kD steps of the chunk) fill ring slots that are never consumed
+#pragma unroll 1
+        for (int b = 0; b < chunk; b += kB) {
+          const uint32_t xq = xs + (b + kD) * 8, wq = ws + (b + kD) * 8;
+#pragma unroll
+          for (int i = 0; i < kB; ++i) {
+            const double xx = xa[i % kD], ww = wa[i % kD];
+            if (i & 1)
+              ws_step_ld(acc, xx, ww, xa[(i - 1) % kD], xa[i % kD], wa[(i - 1) % kD], wa[i % kD], xq + (i - 1) * 8,
+                         wq + (i - 1) * 8);
+            else
+              ws_step(acc, xx, ww);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) st_release_cta(&eflag[warp], c + 1);
+    }
+    if (worker) {
+      const int tok = tok0 + tl;
+      const float z = static_cast<float>(acc);
+      slog[tl * N4 + e] = z;
+      if (e < N) {
+        rb.logits[(size_t)tok * N + e] = z;
+        if (!isfinite(z)) atomicOr(rb.finite_flag, 1);
+      }
+    }
+  }
+  __syncthreads();
+  router_finish_warps(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
 }
 
 // ---------------------------------------------------------------------------------------

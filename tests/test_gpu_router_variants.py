@@ -1,4 +1,4 @@
-"""Every K1 router variant (lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4), forced through
+"""Every K1 router variant (ws and lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4), forced through
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
 including ragged last tiles and shapes where the automatic choice would pick another variant."""
 import os
@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("variant", ["small", "big2", "big4", "lat"])
+@pytest.mark.parametrize("variant", ["small", "big2", "big4", "lat", "ws"])
 @pytest.mark.parametrize("t,d,n,k", [(333, 256, 16, 2), (1000, 512, 8, 2), (257, 256, 32, 4), (70, 1024, 4, 1), (5, 256, 128, 8)])
 def test_router_variant_bit_exact(variant, t, d, n, k):
     env = dict(os.environ, CL_MOE_ROUTER=variant.rstrip("24"), PYTHONPATH=ROOT)
