@@ -220,7 +220,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr uint64_t kAHint = kWgrad ? kEvictNormal : kEvictLast;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned by an offset from the shared array itself, so the compiler keeps the pointer
+  // in the shared window (LDS/STS, 32-bit addresses) instead of generic loads
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kStageA;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
