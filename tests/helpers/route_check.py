@@ -9,8 +9,16 @@ from oracle.oracle import Oracle, make_inputs
 from paper_2509_09121_b200.moe import MoEConfig, MoELayer
 
 
-def main(t, d, n, k):
+def main(t, d, n, k, mode="random"):
     inp = make_inputs(t, d, n, 128, experts=False)
+    if mode == "ties":
+        # exact ties: odd router columns duplicate the even ones (equal logits -> equal probs, the
+        # lowest index must win), every 7th token is all-zero (uniform probs -> experts 0..K-1),
+        # and the last expert's column is zero
+        wr = inp["w_router"]
+        wr[:, 1::2] = wr[:, 0:(n // 2) * 2:2]
+        wr[:, n - 1] = 0.0
+        inp["x"][::7] = 0.0
     lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=128, max_tokens=t), inp["w_router"],
                    np.zeros((n, d, 256), np.float32), np.zeros((n, 128, d), np.float32))
     dec = lay.route_tokens(torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16))
@@ -24,4 +32,4 @@ def main(t, d, n, k):
 
 
 if __name__ == "__main__":
-    sys.exit(main(*map(int, sys.argv[1:5])))
+    sys.exit(main(*map(int, sys.argv[1:5]), *sys.argv[5:6]))

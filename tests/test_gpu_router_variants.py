@@ -1,6 +1,7 @@
 """Every K1 router variant (ws and lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4), forced through
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
-including ragged last tiles and shapes where the automatic choice would pick another variant."""
+including ragged last tiles, shapes where the automatic choice would pick another variant, and exact
+ties (duplicated router columns, all-zero tokens: the lowest expert index must win)."""
 import os
 import subprocess
 import sys
@@ -13,11 +14,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("variant", ["small", "big2", "big4", "lat", "ws"])
-@pytest.mark.parametrize("t,d,n,k", [(333, 256, 16, 2), (1000, 512, 8, 2), (257, 256, 32, 4), (70, 1024, 4, 1), (5, 256, 128, 8)])
-def test_router_variant_bit_exact(variant, t, d, n, k):
+@pytest.mark.parametrize("t,d,n,k,mode", [(333, 256, 16, 2, "random"), (1000, 512, 8, 2, "random"),
+                                          (257, 256, 32, 4, "random"), (70, 1024, 4, 1, "random"),
+                                          (5, 256, 128, 8, "random"), (300, 256, 16, 4, "ties"),
+                                          (90, 256, 128, 8, "ties")])
+def test_router_variant_bit_exact(variant, t, d, n, k, mode):
     env = dict(os.environ, CL_MOE_ROUTER=variant.rstrip("24"), PYTHONPATH=ROOT)
     if variant.startswith("big"):
         env["CL_MOE_BIG_TOK"] = variant[-1]  # 2 or 4 tokens x 4 experts per thread
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "helpers", "route_check.py"), str(t), str(d), str(n),
-                        str(k)], env=env, capture_output=True, text=True, timeout=300, cwd=ROOT)
+                        str(k), mode], env=env, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
