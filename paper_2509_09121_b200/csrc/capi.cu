@@ -576,8 +576,7 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, co
   return guarded(h, [&] {
     if (!hidden || !out) throw ConfigErr("null argument");
     CK(cudaSetDevice(h->cfg.device));
-    run_router(h, hidden, T, (cudaStream_t)stream);
-    run_experts(h, hidden, T, out, false, (cudaStream_t)stream);
+    run_forward(h, hidden, T, out, false, (cudaStream_t)stream);
     export_decision(h, T, decision, (cudaStream_t)stream);
   });
 }
@@ -594,12 +593,12 @@ cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* o
       if (g.x == hidden && g.out == out && g.T == T && g.precision == h->precision) exec = g.exec;
     if (!exec) {
       if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+      if (dense_ok(h, T)) ensure_dense(h);  // no allocation while capturing
       const bool prof = h->prof;
       h->prof = false;  // no timing events inside the graph
       CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
       try {
-        run_router(h, hidden, T, h->cap_stream);
-        run_experts(h, hidden, T, out, false, h->cap_stream);
+        run_forward(h, hidden, T, out, false, h->cap_stream);
       } catch (...) {
         cudaGraph_t g = nullptr;
         cudaStreamEndCapture(h->cap_stream, &g);
@@ -651,8 +650,7 @@ static void host_enqueue(cl_moe* h, const void* hidden_host, int64_t T, void* ou
     f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(sl.xf, n, static_cast<__nv_bfloat16*>(sl.x));
     CK(cudaGetLastError());
   }
-  run_router(h, sl.x, T, st);
-  run_experts(h, sl.x, T, sl.out, f32, st);
+  run_forward(h, sl.x, T, sl.out, f32, st);
   CK(cudaEventRecord(sl.done, st));
   CK(cudaStreamWaitEvent(h->s_d2h, sl.done, 0));
   CK(cudaMemcpyAsync(out_host, sl.out, n * (f32 ? 4 : 2), cudaMemcpyDeviceToHost, h->s_d2h));
@@ -749,15 +747,18 @@ cl_status cl_moe_profile_read(cl_moe* h, double* stage_ms, int64_t* calls) {
     calls[0] = calls[1] = 0;
     for (size_t c = 0; c < h->prof_used; ++c) {
       auto& ev = h->prof_sets[c];
-      const int kind = h->prof_kind[c];
-      const int n = kind == 0 ? kStages : kBwdStages;
+      const int kind = h->prof_kind[c];  // 0 forward, 1 backward, 2 dense-decode forward
+      const int n = kind == 1 ? kBwdStages : kStages;
       CK(cudaEventSynchronize(ev[n]));
       for (int s = 0; s < n; ++s) {
+        // dense decode: router + plan run on a side stream, so the dispatch stage is timed from
+        // the fork point (ev[0]) on the compute stream, not from the end of the plan
+        const int from = (kind == 2 && s == 2) ? 0 : s;
         float ms = 0.0f;
-        CK(cudaEventElapsedTime(&ms, ev[s], ev[s + 1]));
-        stage_ms[(kind == 0 ? 0 : kStages) + s] += ms;
+        CK(cudaEventElapsedTime(&ms, ev[from], ev[s + 1]));
+        stage_ms[(kind == 1 ? kStages : 0) + s] += ms;
       }
-      calls[kind] += 1;
+      calls[kind == 1 ? 1 : 0] += 1;
     }
     h->prof_used = 0;
   });

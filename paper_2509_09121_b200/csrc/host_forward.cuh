@@ -20,7 +20,8 @@ int m_group_for(int64_t k_bytes, int bm) {
 }
 
 template <int G, int EPI, bool F8, bool OF8, bool WG = false>
-void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st) {
+void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st,
+                 int grid_sms = 0) {
   if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
   GemmArgs args = args_in;
   args.tile_counter = h->tile_counter;
@@ -28,7 +29,7 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
   CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((h->num_sms / G) * G);
+  cfg.gridDim = dim3(((grid_sms > 0 ? std::min(grid_sms, h->num_sms) : h->num_sms) / G) * G);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = GemmCfg<G>::kSmem;
   cfg.stream = st;
@@ -43,7 +44,9 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
 }
 
 // route_tokens on device: K1 + K2.
-void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
+// dense = true (dense decode): the 128-thread warp-specialised router with the plan and the dense
+// row weights fused into its last CTA, when that variant applies (returns whether it did).
+bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_prof = true, bool dense = false) {
   if (T < 1) throw RunErr("route_tokens: B must be >= 1");
   if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
   const int N = static_cast<int>(h->N);
@@ -79,22 +82,27 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
     const int tp = RouterWsSmem(N, c).tpc;
     if (ws_cons == 128 && tp >= 1 && (T + tp - 1) / tp <= h->num_sms) ws_cons = c;
   }
+  if (dense) ws_cons = 128;  // dense decode: fewest CTAs (the router runs beside GEMM1)
+  const bool fuse = dense && ws && RouterWsSmem(N, 128).tpc >= 1 && h->route_ctr;  // (ensure_dense allocates)
+  int* tail = fuse ? h->route_ctr : nullptr;
+  float* rwd = fuse ? h->rwd : nullptr;
+  int32_t* invd = fuse ? h->invd : nullptr;
   const bool small = !big && !lat && !ws && router_smem_bytes(N, 32, 8) <= 220 * 1024;
   const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons).tpc : lat ? tpc_lat
                                  : router_tokens_per_cta(N, small ? 32 : 128);
   h->tpc_cur = tpc;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
-  prof_begin(h, st);
+  if (own_prof) prof_begin(h, st);
   if (ws && ws_cons == 32)
     router_ws_kernel<32><<<n_tiles, 32 + 64, RouterWsSmem(N, 32).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
   else if (ws && ws_cons == 64)
     router_ws_kernel<64><<<n_tiles, 64 + 64, RouterWsSmem(N, 64).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
   else if (ws)
     router_ws_kernel<128><<<n_tiles, 128 + 64, RouterWsSmem(N, 128).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
   else if (lat && lat_chunk == 256)
     router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
@@ -118,9 +126,10 @@ void run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
         static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
-  launch_plan(n_tiles, (int)T, N, (int)h->K, h->rb, st);
+  if (!fuse) launch_plan(n_tiles, (int)T, N, (int)h->K, h->rb, st);
   CK(cudaGetLastError());
   prof_mark(h, 1, st);
+  return fuse;
 }
 
 void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T, cudaStream_t st) {
@@ -145,7 +154,8 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
 // GEMM1 (+SwiGLU) and GEMM2 (+optional row weight) over the local expert segments `offsets`.
 void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
-               cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr) {
+               cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr,
+               cudaEvent_t g2_wait = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
@@ -187,22 +197,26 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   const int v = h->gemm_ctas == 2 ? 1 : 0;
   if (!fp8) {
     if (v) {
-      launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st, h->g1_grid);
       prof_mark(h, 3, st);
+      if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
       launch_gemm<2, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
     } else {
-      launch_gemm<1, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st);
+      launch_gemm<1, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st, h->g1_grid);
       prof_mark(h, 3, st);
+      if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
       launch_gemm<1, EPI_ROWSCALE, false, false>(h, mA2[v], h->mB2[v], g2, st);
     }
   } else {
     if (v) {
-      launch_gemm<2, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      launch_gemm<2, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st, h->g1_grid);
       prof_mark(h, 3, st);
+      if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
       launch_gemm<2, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
     } else {
-      launch_gemm<1, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st);
+      launch_gemm<1, EPI_SWIGLU, true, true>(h, mA1q[v], h->mB1q[v], g1, st, h->g1_grid);
       prof_mark(h, 3, st);
+      if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
       launch_gemm<1, EPI_ROWSCALE, true, false>(h, mA2q[v], h->mB2q[v], g2, st);
     }
   }
@@ -238,6 +252,93 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
     launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st);
   else
     launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
+                                  h->rb.finite_flag, st);
+  CK(cudaGetLastError());
+  prof_mark(h, 5, st);
+  h->cur_ev = nullptr;
+  h->last_rows = T * h->K;
+}
+
+// ---------------------------------------------------------------------------------------
+// Dense decode. At T <= kDenseMaxT tokens an M=128 GEMM tile holds every token, so running each
+// expert on all T tokens costs no extra tensor work while the weights stream from HBM anyway;
+// what it buys is independence from routing: GEMM1 (the longest stage) starts at once and the
+// router + plan run beside it on a high-priority stream (launched first, so their CTAs hold SMs
+// while GEMM1's persistent CTAs take the rest). GEMM2 waits for the routing decision: its row
+// weight is the combine weight of (t, e) for routed pairs and 0 otherwise, and the combine reads
+// the routed rows only. Every routed row sees exactly the sparse path's arithmetic, so outputs are
+// bit-identical to it (tests/test_gpu_dense_decode.py). The plan and the dense row weights run in
+// the router's last CTA, so nothing on the routing side has to find an SM while GEMM1's persistent
+// CTAs hold them. CL_MOE_DENSE_DECODE=0 disables the dense path.
+constexpr int kDenseMaxT = 128;
+
+bool dense_ok(const cl_moe* h, int64_t T) {
+  if (h->comm || h->cfg.ep_size > 1 || T < 1 || T > kDenseMaxT) return false;
+  const char* e = std::getenv("CL_MOE_DENSE_DECODE");
+  return !(e && e[0] == '0');
+}
+
+void ensure_dense(cl_moe* h) {
+  if (h->xd) return;
+  const uint64_t rows = static_cast<uint64_t>(h->N) * kDenseMaxT;
+  h->xd = dalloc<__nv_bfloat16>(rows * h->d);
+  h->actd = dalloc<__nv_bfloat16>(rows * h->f);
+  h->yd = dalloc<__nv_bfloat16>(rows * h->d);
+  h->rwd = dalloc<float>(rows);
+  h->invd = dalloc<int32_t>((size_t)kDenseMaxT * h->K);
+  h->offd = dalloc<int32_t>(h->N + 1);
+  for (int v = 0; v < 2; ++v) {
+    h->mA1d[v] = make_map(h->xd, false, h->d, rows, 128);
+    h->mA2d[v] = make_map(h->actd, false, h->f, rows, 128);
+    h->mA1dq[v] = make_map(h->xd, true, h->d, rows, 128);
+    h->mA2dq[v] = make_map(h->actd, true, h->f, rows, 128);
+  }
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CK(cudaStreamCreateWithPriority(&h->s_route, cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+  h->route_ctr = dalloc<int>(1);
+  CK(cudaMemset(h->route_ctr, 0, sizeof(int)));
+}
+
+// route_tokens + moe_forward of the single-GPU layer: dense decode when eligible, else the
+// sparse path (router, plan, dispatch, grouped GEMMs, combine).
+void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+  if (!dense_ok(h, T)) {
+    run_router(h, x, T, st);
+    run_experts(h, x, T, out, out_f32, st);
+    return;
+  }
+  ensure_dense(h);
+  const int N = static_cast<int>(h->N), K = static_cast<int>(h->K);
+  const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
+  prof_begin(h, st, 2);
+  CK(cudaEventRecord(h->ev_fork, st));
+  CK(cudaStreamWaitEvent(h->s_route, h->ev_fork, 0));
+  if (!run_router(h, x, T, h->s_route, false, true)) {  // plan + row weights not fused (other variant)
+    dense_weights_kernel<<<(int)((N * T + 255) / 256), 256, 0, h->s_route>>>(h->rb.topk_idx, h->rb.combine_w, (int)T,
+                                                                             N, K, h->rwd, h->invd);
+    CK(cudaGetLastError());
+    prof_mark(h, 1, h->s_route);
+  }
+  CK(cudaEventRecord(h->ev_join, h->s_route));
+  const int rb8 = static_cast<int>((N * T + 7) / 8);
+  const dim3 blocks(rb8, std::max(1, std::min(8, (8 * h->num_sms + rb8 - 1) / rb8)));  // ~8 CTAs per SM
+  if (fp8)
+    dense_dispatch_kernel<true><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                        h->xd, h->sx_in, h->offd);
+  else
+    dense_dispatch_kernel<false><<<blocks, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N,
+                                                         h->xd, nullptr, h->offd);
+  CK(cudaGetLastError());
+  prof_mark(h, 2, st);
+  run_gemms(h, h->offd, h->actd, h->yd, h->rwd, h->mA1d, h->mA2d, h->mA1dq, h->mA2dq, st, nullptr, nullptr, h->ev_join);
+  prof_mark(h, 4, st);
+  if (out_f32)
+    launch_combine<float>(h->yd, h->invd, (int)T, (int)h->d, K, static_cast<float*>(out), h->rb.finite_flag, st);
+  else
+    launch_combine<__nv_bfloat16>(h->yd, h->invd, (int)T, (int)h->d, K, static_cast<__nv_bfloat16*>(out),
                                   h->rb.finite_flag, st);
   CK(cudaGetLastError());
   prof_mark(h, 5, st);

@@ -205,6 +205,17 @@ struct cl_moe {
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
   bool maps_q = false;
 
+  // dense decode (host_forward.cuh run_forward): every expert runs all T <= kDenseMaxT tokens so
+  // the expert GEMMs start before routing is known; the router runs beside them on s_route
+  __nv_bfloat16 *xd = nullptr, *actd = nullptr, *yd = nullptr;  // [N * kDenseMaxT] rows
+  float* rwd = nullptr;                                          // [N * kDenseMaxT] row weights (0 = unrouted)
+  int32_t *invd = nullptr, *offd = nullptr;                      // [kDenseMaxT * K], [N + 1]
+  CUtensorMap mA1d[2], mA2d[2], mA1dq[2], mA2dq[2];
+  cudaStream_t s_route = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int g1_grid = 0;  // > 0: GEMM1 grid limit
+  int* route_ctr = nullptr;  // router_ws_kernel tail counter (dense decode)
+
   ~cl_moe() {
     void* ptrs[] = {sx_in_all, calib_all, calib_counts, calib_ch, smooth, wr64,   wr,     win,     wout,    win8,      wout8,        ws_in,        ws_out,
                     sx_in,  sx_mid,  calib,   xperm,     act,          y,            perm,
@@ -220,7 +231,7 @@ struct cl_moe {
                     (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
                     (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
-                    (void*)row_ptr_dx})
+                    (void*)row_ptr_dx, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr})
       if (p) cudaFree(p);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
@@ -231,6 +242,9 @@ struct cl_moe {
     if (own_stream) cudaStreamDestroy(own_stream);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
+    if (s_route) cudaStreamDestroy(s_route);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     for (auto& sl : slot)
       for (cudaEvent_t e : {sl.h2d, sl.done, sl.d2h})
         if (e) cudaEventDestroy(e);

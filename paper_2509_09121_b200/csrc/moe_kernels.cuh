@@ -427,6 +427,84 @@ __global__ void __launch_bounds__(128) router_lat_kernel(const __nv_bfloat16* __
 }
 
 // ---------------------------------------------------------------------------------------
+// K2 body (the dispatch plan; see plan_kernel below), shared by plan_kernel and router_ws_kernel's
+// fused tail: threads >= kThreads of a larger CTA only take part in the barriers.
+template <int kThreads>
+__device__ __forceinline__ void plan_body(int n_tiles, int T, int N, int K, const RouteBufs& rb) {
+  __shared__ int s_chunk[kThreads];
+  __shared__ double s_red[kThreads];
+  __shared__ double s_p[128];
+  __shared__ int s_counts[128];
+  const bool in = threadIdx.x < kThreads;
+  const int chunks = kThreads / N;  // chunks of tiles per expert
+  const int per = (n_tiles + chunks - 1) / chunks;
+  const int e = threadIdx.x % N;
+  const int c = threadIdx.x / N;
+  const bool act = in && c < chunks;
+  const int t_begin = act ? min(n_tiles, c * per) : 0;
+  const int t_end = act ? min(n_tiles, (c + 1) * per) : 0;
+  int sum = 0;
+  double ps = 0.0;
+#pragma unroll 8
+  for (int t = t_begin; t < t_end; ++t) {
+    sum += rb.tile_cnt[(size_t)t * N + e];
+    ps += rb.tile_psum[(size_t)t * N + e];
+  }
+  if (in) {
+    s_chunk[threadIdx.x] = sum;
+    s_red[threadIdx.x] = ps;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    int run = 0;
+    double p = 0.0;
+    for (int cc = 0; cc < chunks; ++cc) {
+      const int v = s_chunk[cc * N + threadIdx.x];
+      s_chunk[cc * N + threadIdx.x] = run;
+      run += v;
+      p += s_red[cc * N + threadIdx.x];
+    }
+    s_counts[threadIdx.x] = run;
+    s_p[threadIdx.x] = p;
+    rb.counts[threadIdx.x] = run;
+    rb.agg_prob[threadIdx.x] = static_cast<float>(p);
+  }
+  __syncthreads();
+  {
+    int run = act ? s_chunk[threadIdx.x] : 0;
+    for (int t = t_begin; t < t_end; ++t) {
+      const size_t i = (size_t)t * N + e;
+      const int v = rb.tile_cnt[i];
+      rb.tile_cnt[i] = run;
+      run += v;
+    }
+  }
+  // Z-loss: fixed-order two-level reduction of the per-tile lse^2 sums.
+  double z = 0.0;
+  for (int t = threadIdx.x; in && t < n_tiles; t += kThreads) z += rb.tile_lse2[t];
+  __syncthreads();  // s_red's tile partial sums above are consumed
+  if (in) s_red[threadIdx.x] = z;
+  __syncthreads();
+  for (int w = kThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int off = 0;
+    double aux = 0.0;
+    for (int x = 0; x < N; ++x) {
+      rb.offsets[x] = off;
+      off += s_counts[x];
+      aux += s_p[x] * static_cast<double>(s_counts[x]);
+    }
+    rb.offsets[N] = off;
+    const double coef = static_cast<double>(N) / (static_cast<double>(T) * T * static_cast<double>(K));
+    rb.losses[0] = static_cast<float>(coef * aux);
+    rb.losses[1] = static_cast<float>(s_red[0] / static_cast<double>(T));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // K1, warp-specialised latency variant (decode-size batches; replaces the barrier-paced ring of
 // router_lat_kernel). Same chains (one thread per (token, expert), ascending l), fed by a deep
 // ring so the chains never wait on global memory:
@@ -618,10 +696,15 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
   }
 }
 
+// tail_ctr (dense decode, nullable): the last CTA to finish also runs the plan (plan_body<128>)
+// and the dense row weights / combine rows, so nothing queues behind GEMM1's persistent CTAs.
 template <int kCons>
 __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfloat16* __restrict__ x,
                                                                  const double* __restrict__ wr64, int T, int d,
-                                                                 int N, int K, RouteBufs rb) {
+                                                                 int N, int K, RouteBufs rb,
+                                                                 int* __restrict__ tail_ctr = nullptr,
+                                                                 float* __restrict__ rwd = nullptr,
+                                                                 int32_t* __restrict__ invd = nullptr) {
   constexpr int kD = RouterWsSmem::kAhead, kB = 32;
   const RouterWsSmem L(N, kCons);
   const int N4 = L.N4, tpc = L.tpc, chunk = L.chunk, wpitch = L.wpitch, kStages = L.stages;
@@ -741,6 +824,26 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
   }
   __syncthreads();
   router_finish_warps(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
+  if (tail_ctr) {
+    __shared__ int s_last;
+    __threadfence();  // this CTA's tile statistics and decisions, before the counter
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(tail_ctr, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      plan_body<128>(gridDim.x, T, N, K, rb);
+      for (int i = threadIdx.x; i < N * T; i += blockDim.x) {  // = dense_weights_kernel
+        const int e = i / T, t = i % T;
+        float v = 0.0f;
+        for (int k = 0; k < K; ++k)
+          if (rb.topk_idx[(size_t)t * K + k] == e) v = rb.combine_w[(size_t)t * K + k];
+        rwd[i] = v;
+      }
+      for (int i = threadIdx.x; i < T * K; i += blockDim.x) invd[i] = rb.topk_idx[i] * T + i / K;
+      if (threadIdx.x == 0) *tail_ctr = 0;  // ready for the next launch (stream-ordered)
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -877,73 +980,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
 // and Z-loss reductions in a fixed order. One CTA; deterministic (no atomics).
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads) plan_kernel(int n_tiles, int T, int N, int K, RouteBufs rb) {
-  __shared__ int s_chunk[kThreads];
-  __shared__ double s_red[kThreads];
-  __shared__ double s_p[128];
-  __shared__ int s_counts[128];
-  const int chunks = kThreads / N;  // chunks of tiles per expert
-  const int per = (n_tiles + chunks - 1) / chunks;
-  const int e = threadIdx.x % N;
-  const int c = threadIdx.x / N;
-  const bool act = c < chunks;
-  const int t_begin = act ? min(n_tiles, c * per) : 0;
-  const int t_end = act ? min(n_tiles, (c + 1) * per) : 0;
-  int sum = 0;
-  double ps = 0.0;
-#pragma unroll 8
-  for (int t = t_begin; t < t_end; ++t) {
-    sum += rb.tile_cnt[(size_t)t * N + e];
-    ps += rb.tile_psum[(size_t)t * N + e];
-  }
-  s_chunk[threadIdx.x] = sum;
-  s_red[threadIdx.x] = ps;
-  __syncthreads();
-  if (threadIdx.x < N) {
-    int run = 0;
-    double p = 0.0;
-    for (int cc = 0; cc < chunks; ++cc) {
-      const int v = s_chunk[cc * N + threadIdx.x];
-      s_chunk[cc * N + threadIdx.x] = run;
-      run += v;
-      p += s_red[cc * N + threadIdx.x];
-    }
-    s_counts[threadIdx.x] = run;
-    s_p[threadIdx.x] = p;
-    rb.counts[threadIdx.x] = run;
-    rb.agg_prob[threadIdx.x] = static_cast<float>(p);
-  }
-  __syncthreads();
-  {
-    int run = act ? s_chunk[threadIdx.x] : 0;
-    for (int t = t_begin; t < t_end; ++t) {
-      const size_t i = (size_t)t * N + e;
-      const int v = rb.tile_cnt[i];
-      rb.tile_cnt[i] = run;
-      run += v;
-    }
-  }
-  // Z-loss: fixed-order two-level reduction of the per-tile lse^2 sums.
-  double z = 0.0;
-  for (int t = threadIdx.x; t < n_tiles; t += kThreads) z += rb.tile_lse2[t];
-  s_red[threadIdx.x] = z;
-  __syncthreads();
-  for (int w = kThreads / 2; w > 0; w >>= 1) {
-    if (threadIdx.x < w) s_red[threadIdx.x] += s_red[threadIdx.x + w];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int off = 0;
-    double aux = 0.0;
-    for (int x = 0; x < N; ++x) {
-      rb.offsets[x] = off;
-      off += s_counts[x];
-      aux += s_p[x] * static_cast<double>(s_counts[x]);
-    }
-    rb.offsets[N] = off;
-    const double coef = static_cast<double>(N) / (static_cast<double>(T) * T * static_cast<double>(K));
-    rb.losses[0] = static_cast<float>(coef * aux);
-    rb.losses[1] = static_cast<float>(s_red[0] / static_cast<double>(T));
-  }
+  plan_body<kThreads>(n_tiles, T, N, K, rb);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1056,6 +1093,71 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     }
   }
   if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
+}
+
+// ---------------------------------------------------------------------------------------
+// Dense decode (T <= 128 tokens, host_forward.cuh run_forward): every expert takes all T tokens,
+// so GEMM1 can start before routing is known. Row e*T + t of the GEMM1 operand is token t, as
+// bf16 or E4M3-quantised with expert e's activation scale exactly as dispatch_kernel does it.
+// One warp per row; block 0 also writes the expert offsets e*T.
+template <bool kFp8>
+__global__ void __launch_bounds__(256) dense_dispatch_kernel(const __nv_bfloat16* __restrict__ x, int T, int d, int N,
+                                                             void* __restrict__ xd, const float* __restrict__ act_scale,
+                                                             int32_t* __restrict__ offd) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x <= N) offd[threadIdx.x] = threadIdx.x * T;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= N * T) return;
+  const int e = row / T, t = row % T;
+  const int4* src = reinterpret_cast<const int4*>(x + (size_t)t * d);
+  // gridDim.y column slices, 4 independent 16-byte loads in flight per lane
+  const int nvec_all = d / 8;
+  const int per = (nvec_all + gridDim.y - 1) / gridDim.y;
+  const int vbeg = blockIdx.y * per, vend = min(nvec_all, vbeg + per);
+  for (int v0 = vbeg + lane; v0 < vend; v0 += 32 * 4) {
+    int4 buf[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + u * 32 < vend) buf[u] = ld_nc_v4(src + v0 + u * 32);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + u * 32;
+      if (v >= vend) break;
+      if constexpr (!kFp8) {
+        st_na_v4(reinterpret_cast<int4*>(static_cast<__nv_bfloat16*>(xd) + (size_t)row * d) + v, buf[u]);
+      } else {
+        const float sc = act_scale[e];
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&buf[u]);
+        uint32_t p[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {  // x / scale (IEEE division), RNE + saturate: as dispatch_kernel
+          const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+              make_float2(__fdiv_rn(__bfloat162float(h[4 * i]), sc), __fdiv_rn(__bfloat162float(h[4 * i + 1]), sc)),
+              __NV_SATFINITE, __NV_E4M3);
+          const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+              make_float2(__fdiv_rn(__bfloat162float(h[4 * i + 2]), sc), __fdiv_rn(__bfloat162float(h[4 * i + 3]), sc)),
+              __NV_SATFINITE, __NV_E4M3);
+          p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+        }
+        reinterpret_cast<uint2*>(static_cast<uint8_t*>(xd) + (size_t)row * d)[v] = make_uint2(p[0], p[1]);
+      }
+    }
+  }
+}
+
+// Dense decode, once routing is known: GEMM2 row weights (the combine weight of (t, e) when e is
+// among t's top-K, else 0) and the combine rows inv[t*K + k] = e_k*T + t.
+__global__ void dense_weights_kernel(const int32_t* __restrict__ idx, const float* __restrict__ w, int T, int N, int K,
+                                     float* __restrict__ rwd, int32_t* __restrict__ invd) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < N * T) {
+    const int e = i / T, t = i % T;
+    float v = 0.0f;
+    for (int k = 0; k < K; ++k)
+      if (idx[(size_t)t * K + k] == e) v = w[(size_t)t * K + k];
+    rwd[i] = v;
+  }
+  if (i < T * K) invd[i] = idx[i] * T + i / K;
 }
 
 // ---------------------------------------------------------------------------------------
