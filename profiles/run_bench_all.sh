@@ -7,7 +7,7 @@ run r01_c2_bf16 --config c2
 run r01_c2_fp8 --config c2 --precision fp8
 run r01_c1 --config c1
 run r01_c3 --config c3
-for t in 64 256 512; do
+for t in 64 128 256 512; do
   run r01_c4_bf16_T$t --config c4 --tokens $t
   run r01_c4_fp8_T$t --config c4 --tokens $t --precision fp8
 done
