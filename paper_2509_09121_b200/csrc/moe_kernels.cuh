@@ -1069,26 +1069,35 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
       }
     }
   } else {
-    for (int v = vbeg + lane; v < nvec; v += 32) {
-      const int4 raw = ld_nc_v4(src + v);
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
-      float f[8];
+    for (int v0 = vbeg + lane; v0 < nvec; v0 += 32 * 4) {  // 4 independent 16-byte loads in flight
+      int4 buf[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(h[i]);
-      for (int k = 0; k < K; ++k) {
-        uint32_t p[2];
+      for (int u = 0; u < 4; ++u)
+        if (v0 + u * 32 < nvec) buf[u] = ld_nc_v4(src + v0 + u * 32);
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          // x / scale with IEEE division, then RNE + saturate to E4M3 (SPEC.md:523-531 fp8_qdq)
-          const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-              make_float2(__fdiv_rn(f[4 * i], sc[k]), __fdiv_rn(f[4 * i + 1], sc[k])), __NV_SATFINITE, __NV_E4M3);
-          const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-              make_float2(__fdiv_rn(f[4 * i + 2], sc[k]), __fdiv_rn(f[4 * i + 3], sc[k])), __NV_SATFINITE, __NV_E4M3);
-          p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+      for (int u = 0; u < 4; ++u) {
+        const int v = v0 + u * 32;
+        if (v >= nvec) break;
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&buf[u]);
+        float f[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = __bfloat162float(h[i]);
+        for (int k = 0; k < K; ++k) {
+          uint32_t p[2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            // x / scale with IEEE division, then RNE + saturate to E4M3 (SPEC.md:523-531 fp8_qdq)
+            const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                make_float2(__fdiv_rn(f[4 * i], sc[k]), __fdiv_rn(f[4 * i + 1], sc[k])), __NV_SATFINITE, __NV_E4M3);
+            const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                make_float2(__fdiv_rn(f[4 * i + 2], sc[k]), __fdiv_rn(f[4 * i + 3], sc[k])), __NV_SATFINITE,
+                __NV_E4M3);
+            p[i] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+          }
+          if (!dsts[k]) continue;
+          uint2* dst = static_cast<uint2*>(dsts[k]) + v;
+          *dst = make_uint2(p[0], p[1]);
         }
-        if (!dsts[k]) continue;
-        uint2* dst = static_cast<uint2*>(dsts[k]) + v;
-        *dst = make_uint2(p[0], p[1]);
       }
     }
   }
