@@ -512,16 +512,18 @@ __device__ __forceinline__ void plan_body(int n_tiles, int T, int N, int K, cons
 //                   the padded expert-major layout widen_router_kernel writes) and of each token's
 //                   x chunk; completion on full[s]; sleeps while the ring is full;
 //   converter warp: widens the slot's x chunk to fp64 once for all experts (F2F runs at
-//                   15/clk/SM: kept off the chains' SM sub-partition) -> xready[s];
+//                   15/clk/SM: kept off the chains' SM sub-partition), then publishes it;
 //   chain warps:    per 256-step chunk, run the chain from a register ring filled 16 steps ahead
 //                   (two steps per 16-byte load of each operand), then publish the slot as free.
 //                   The next slot's flag is read when a chunk starts, so the check overlaps the
 //                   chain instead of stalling it.
-// The chain step is one asm block (the FMA, then on odd steps the two ring loads), which pins the
-// interleaving in PTX: measured 9.2 cycles per step against 8.5 for operands already in registers
-// and 11.9 for the [l][e] layout with a runtime stride (tools/chain_ring_probe.cu).
+// The chain step is one asm block (the FMA, then on odd steps the two ring loads): measured 9.2
+// cycles per step against 8.5 for operands already in registers and 11.9 for the [l][e] layout
+// with a runtime stride (tools/chain_ring_probe.cu). Slot hand-offs use CTA-scope release/acquire
+// flags in shared memory (mbarriers only for the TMA byte counts).
 // kCons (chain threads) is 32, 64 or 128: the host picks the smallest that keeps one CTA per SM, so
-// a decode batch spreads over the most SMs. The per-token softmax / top-K runs one warp per token.
+// a decode batch spreads over the most SMs (dense decode pins 128: the router then runs beside
+// GEMM1 and should hold few SMs). The per-token softmax / top-K runs one warp per token.
 struct RouterWsSmem {
   static constexpr int kMaxStages = 12;
   static constexpr int kAhead = 16;  // ring distance (steps); loads run up to kAhead past a row
