@@ -136,7 +136,11 @@ cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int
                              const float* combine_weights, void* out, void* stream);
 
 /* The fused layer: route_tokens + dispatch + expert FFN + combine. `out` bf16 [T x d].
- * `decision` may be NULL. */
+ * `decision` may be NULL. Single-GPU calls with T <= 128 take the dense-decode path (every
+ * expert runs all T tokens while routing runs beside GEMM1 on an internal high-priority stream
+ * joined back into `stream`); results are bit-identical to the sparse path. Its buffers
+ * (N x 128 rows of x, SwiGLU output and expert output) are allocated on the first such call.
+ * Environment: CL_MOE_DENSE_DECODE=0 disables it. */
 cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
                          const cl_moe_decision* decision, void* stream);
 /* cl_moe_forward without the decision outputs, captured into a CUDA graph on first use for each
