@@ -40,7 +40,8 @@ def _run(lay, x, dense, entry="device"):
 
 
 @pytest.mark.parametrize("t,d,n,k,f", [(1, 256, 8, 2, 128), (5, 256, 16, 2, 256), (64, 512, 16, 2, 256),
-                                       (128, 256, 4, 1, 128), (37, 256, 128, 8, 128), (100, 512, 32, 4, 384)])
+                                       (128, 256, 4, 1, 128), (37, 256, 128, 8, 128), (100, 512, 32, 4, 384),
+                                       (3, 256, 1, 1, 128)])
 def test_dense_decode_bit_identical_to_sparse(t, d, n, k, f):
     inp = make_inputs(t, d, n, f)
     lay = _layer(inp, t, k)
@@ -85,4 +86,24 @@ def test_dense_decode_fp8_bit_identical_to_sparse(t):
     assert torch.equal(ys.view(torch.int16), yd.view(torch.int16))
     for a, b in zip(ds, dd):
         assert torch.equal(a, b)
+    lay.close()
+
+
+def test_dense_decode_stage_profile():
+    """Per-stage timing events of the dense path (router/plan on the side stream) read back sanely."""
+    t, d, n, k, f = 64, 256, 16, 2, 256
+    inp = make_inputs(t, d, n, f)
+    lay = _layer(inp, t, k)
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    lay.forward(x)
+    lay.sync()
+    lay.profile(True)
+    for _ in range(3):
+        lay.forward(x)
+    lay.sync()
+    ms, calls = lay.profile_read()
+    lay.profile(False)
+    assert calls[0] == 3
+    for name in ("router", "plan", "dispatch", "gemm1", "gemm2", "combine"):
+        assert ms[name] > 0.0, (name, ms)
     lay.close()
