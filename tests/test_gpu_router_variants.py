@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 @pytest.mark.parametrize("t,d,n,k,mode", [(333, 256, 16, 2, "random"), (1000, 512, 8, 2, "random"),
                                           (257, 256, 32, 4, "random"), (70, 1024, 4, 1, "random"),
                                           (5, 256, 128, 8, "random"), (300, 256, 16, 4, "ties"),
-                                          (90, 256, 128, 8, "ties")])
+                                          (90, 256, 128, 8, "ties"), (2400, 256, 4, 2, "random")])
 def test_router_variant_bit_exact(variant, t, d, n, k, mode):
     env = dict(os.environ, CL_MOE_ROUTER=variant.rstrip("24"), PYTHONPATH=ROOT)
     if variant.startswith("big"):
