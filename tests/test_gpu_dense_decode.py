@@ -104,6 +104,7 @@ def test_dense_decode_stage_profile():
     ms, calls = lay.profile_read()
     lay.profile(False)
     assert calls[0] == 3
-    for name in ("router", "plan", "dispatch", "gemm1", "gemm2", "combine"):
+    for name in ("router", "dispatch", "gemm1", "gemm2", "combine"):
         assert ms[name] > 0.0, (name, ms)
+    assert ms["plan"] >= 0.0  # the plan runs inside the router's last CTA here: may read ~0
     lay.close()
