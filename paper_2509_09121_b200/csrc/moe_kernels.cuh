@@ -526,6 +526,7 @@ __device__ __forceinline__ void plan_body(int n_tiles, int T, int N, int K, cons
 // GEMM1 and should hold few SMs). The per-token softmax / top-K runs one warp per token.
 struct RouterWsSmem {
   static constexpr int kMaxStages = 12;
+  static constexpr int kMaxChainWarps = 8;  // kCons <= 256: one eflag slot per chain warp
   static constexpr int kAhead = 16;  // ring distance (steps); loads run up to kAhead past a row
   int tpc, N4, chunk, wpitch, stages;
   size_t sw, rx, xd, bars, slog, sidx, slse, total;
@@ -543,7 +544,9 @@ struct RouterWsSmem {
     rx = sw + (size_t)stages * N4 * wpitch * 8;                      // [stages][tpc][chunk] bf16
     xd = rx + ((size_t)stages * tpc * chunk * 2 + 15) / 16 * 16;     // [stages][tpc][chunk] fp64
     bars = xd + (size_t)stages * tpc * chunk * 8;                    // full[kMaxStages] + flags
-    slog = bars + kMaxStages * 8 + (kMaxStages + 4) * 4;
+    // flags: xflag[kMaxStages] + eflag[kMaxChainWarps] (round 1 reserved only 4 eflag slots, so a
+    // 256-thread instantiation's eflag[4..7] aliased slog[0..3]: the logits of the tile's token 0)
+    slog = bars + kMaxStages * 8 + (kMaxStages + kMaxChainWarps) * 4;
     sidx = slog + sizeof(float) * tpc * N4;
     slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
     total = slse + sizeof(double) * tpc + kAhead * 8;  // guard for the ring's overrun past the last row
@@ -708,6 +711,7 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
                                                                  float* __restrict__ rwd = nullptr,
                                                                  int32_t* __restrict__ invd = nullptr) {
   constexpr int kD = RouterWsSmem::kAhead, kB = 32;
+  static_assert(kCons % 32 == 0 && kCons / 32 <= RouterWsSmem::kMaxChainWarps, "eflag region holds one slot per chain warp");
   const RouterWsSmem L(N, kCons);
   const int N4 = L.N4, tpc = L.tpc, chunk = L.chunk, wpitch = L.wpitch, kStages = L.stages;
   const double* wt = wr64 + (size_t)d * N4;  // per chunk [N4][wpitch] (widen_router_kernel)
