@@ -131,6 +131,12 @@ cl_status cl_moe_synthetic_skew(cl_moe* h, double gamma);
 cl_status cl_moe_route_tokens(cl_moe* h, const void* hidden, int64_t T, const cl_moe_decision* out,
                               void* stream);
 
+/* route_tokens on the caller's fp32 hidden [T x d] (device): the gating is computed on the fp32
+ * values themselves, so the decision is bit-exact with the reference's
+ * route_tokens on the same Tensor (no bf16 rounding before the router). */
+cl_status cl_moe_route_tokens_f32(cl_moe* h, const float* hidden, int64_t T, const cl_moe_decision* out,
+                                  void* stream);
+
 /* moe_forward with a caller-supplied decision. */
 cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int32_t* topk_idx,
                              const float* combine_weights, void* out, void* stream);
@@ -143,13 +149,19 @@ cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int
  * Environment: CL_MOE_DENSE_DECODE=0 disables it. */
 cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
                          const cl_moe_decision* decision, void* stream);
+/* The fused layer on fp32 device tensors (the reference's Tensor dtype): routes on the fp32 hidden
+ * (as cl_moe_route_tokens_f32), runs the experts on its bf16 rounding, and writes fp32 `out`
+ * [T x d] (the combine's fp32 accumulators, unrounded). */
+cl_status cl_moe_forward_f32(cl_moe* h, const float* hidden, int64_t T, float* out, const cl_moe_decision* decision,
+                             void* stream);
 /* cl_moe_forward without the decision outputs, captured into a CUDA graph on first use for each
  * (hidden, out, T, precision) and replayed afterwards (one launch per call; decode-size steps).
  * Single-GPU layer only. The graph bakes in the buffer addresses: reuse the same buffers. */
 cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* out, void* stream);
 
 /* Same layer through HOST buffers (the reference-facing call): copies hidden in, runs the
- * layer and copies the output back; synchronous. io_dtype selects bf16 or fp32 host tensors. */
+ * layer and copies the output back; synchronous. io_dtype selects bf16 or fp32 host tensors;
+ * fp32 hidden is routed on its fp32 values (as cl_moe_forward_f32). */
 cl_status cl_moe_forward_host(cl_moe* h, const void* hidden_host, int64_t T, void* out_host,
                               int32_t io_dtype);
 
@@ -218,6 +230,29 @@ cl_status cl_moe_set_precision(cl_moe* h, int32_t precision);
  * [N_local] per-expert max |GEMM1 input| / |SwiGLU output|, ch_max[d] per-channel max |hidden|.
  * An empty calibration set (T = 0) leaves them unchanged (zero after a reset). */
 cl_status cl_moe_calibration_stats(cl_moe* h, int64_t* counts, float* x_max, float* mid_max, float* ch_max);
+/* The router under the FP8 scheme. SPEC.md:565 runs "all expert/router ... projection GEMMs"
+ * through fp8_qdq: with enable = 1 (the default) an FP8-precision forward routes on
+ * qdq(hidden, s_x) . qdq(W_r, s_w[i]) — s_x the per-tensor activation scale (calibration max |hidden|
+ * / 448, or act_scale > 0 given here), s_w[i] = absmax of expert column i of W_r / 448 — still with
+ * fp64 accumulation, so the decision is bit-exact with the oracle's route on those dequantised
+ * values. enable = 0 keeps fp32 gating in FP8 mode (PAPER §2.3.4's training-stability choice).
+ * Takes effect on the next forward; quantize_fp8 recomputes W_r's qdq. get: the mode, s_x and
+ * s_w [N] (the last two need a quantized scheme). */
+cl_status cl_moe_set_router_fp8(cl_moe* h, int32_t enable, float act_scale);
+/* QuantScheme file ("JSON manifest + binary scale arrays"; fields SPEC.md:520-523):
+ * `path` is the JSON manifest (layer shape, alpha_smooth, tau, router mode, one entry per array
+ * {name, dtype, shape, offset}), `path`.bin the little-endian fp32 arrays: smoothing [d] (the
+ * product of the folded smoothing vectors), act_scale_in [N], act_scale_mid [N_local], w_in_scale
+ * [N_local][2f] (reference W_in column order), w_out_scale [N_local][d], router_act_scale [1],
+ * router_w_scale [N]. save needs a quantized scheme. load applies a scheme to a layer holding the
+ * same weights: folds its smoothing vector (unless this layer already carries exactly that fold;
+ * a different fold -> CL_ERR_CONFIG), takes every scale from the file (no calibration), quantizes
+ * the weights with the stored weight scales and switches to FP8 — the FP8 forward is then
+ * bit-identical to the layer that saved it. Shape mismatch -> CL_ERR_CONFIG; unreadable or
+ * malformed files -> CL_ERR_RUN. */
+cl_status cl_moe_save_fp8_scheme(cl_moe* h, const char* path);
+cl_status cl_moe_load_fp8_scheme(cl_moe* h, const char* path);
+cl_status cl_moe_get_router_fp8(cl_moe* h, int32_t* enable, float* act_scale, float* w_scale);
 cl_status cl_moe_get_fp8_scales(cl_moe* h, float* act_in, float* act_mid, float* w_in_scale,
                                 float* w_out_scale);
 

@@ -345,6 +345,24 @@ def make_inputs(t: int, d: int, n: int, f: int, seed: int = ROOT_SEED, bf16: boo
     return out
 
 
+def router_fp8_sim(o: Oracle, x, wr, k: int, s_x: float):
+    """route_tokens of the quantized model (the router GEMM runs through fp8_qdq too):
+    x_hat = qdq(x, s_x) with the per-tensor activation scale, W_r_hat[:, i] = qdq(W_r[:, i], s_w[i])
+    with s_w[i] = absmax of expert column i / 448 (1 for an all-zero column); then the reference
+    route on those dequantised fp32 values. Returns (decision, s_w [N])."""
+    x = np.ascontiguousarray(x, np.float32)
+    wr = np.ascontiguousarray(wr, np.float32)
+    t, d = x.shape
+    n = wr.shape[1]
+    m = np.abs(wr).max(0)
+    s_w = np.where(m > 0, m / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    xq = o.fp8_qdq(x, float(s_x)).reshape(t, d)
+    wq = np.empty_like(wr)
+    for c in range(n):
+        wq[:, c] = o.fp8_qdq(wr[:, c], float(s_w[c]))
+    return o.route(xq, wq, k), s_w
+
+
 def moe_forward_fp8_sim(o: Oracle, x, w_in, w_out, idx, w, s_in, s_mid, ws_in=None, ws_out=None):
     """Expert-aware FP8 layer simulated with the oracle's E4M3 qdq:
     per expert e, X_e -> qdq(X_e, s_in[e]); every output channel of W_in[e] / W_out[e] -> qdq with

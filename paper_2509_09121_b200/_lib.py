@@ -90,6 +90,8 @@ _PROTOS = {
     "cl_moe_route_tokens": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Decision), C.c_void_p]),
     "cl_moe_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "cl_moe_forward": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(Decision), C.c_void_p]),
+    "cl_moe_route_tokens_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(Decision), C.c_void_p]),
+    "cl_moe_forward_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.POINTER(Decision), C.c_void_p]),
     "cl_moe_forward_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32]),
     "cl_moe_forward_host_async": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32]),
     "cl_moe_host_wait": (C.c_int, [C.c_void_p]),
@@ -121,6 +123,10 @@ _PROTOS = {
     "cl_moe_fold_smoothing": (C.c_int, [C.c_void_p, C.c_void_p]),
     "cl_moe_set_precision": (C.c_int, [C.c_void_p, C.c_int32]),
     "cl_moe_get_fp8_scales": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cl_moe_set_router_fp8": (C.c_int, [C.c_void_p, C.c_int32, C.c_float]),
+    "cl_moe_save_fp8_scheme": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "cl_moe_load_fp8_scheme": (C.c_int, [C.c_void_p, C.c_char_p]),
+    "cl_moe_get_router_fp8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 

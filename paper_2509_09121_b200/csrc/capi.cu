@@ -28,6 +28,7 @@
 #include "ep.cuh"
 #include "bwd_kernels.cuh"
 #include "ckpt.hpp"
+#include "scheme.hpp"
 
 using namespace cmoe;
 
@@ -382,6 +383,13 @@ cl_status cl_moe_balance_calibration(cl_moe* h, const void* base, int64_t T_base
     CK(cudaSetDevice(h->cfg.device));
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t N = h->N, K = h->K, d = h->d;
+    // pre-routing uses the full-precision router (calibration precedes quantization)
+    struct Restore {
+      cl_moe* h;
+      int p;
+      ~Restore() { h->precision = p; }
+    } restore{h, h->precision};
+    h->precision = CL_MOE_BF16;
     std::vector<int64_t> cnt(N, 0);
     std::vector<int32_t> c32(N);
     if (base && T_base > 0) {
@@ -421,6 +429,7 @@ cl_status cl_moe_balance_calibration(cl_moe* h, const void* base, int64_t T_base
       if (cnt[e] < tau)
         throw RunErr(fmt("balance_calibration: token pool exhausted with expert %lld at %lld < tau=%lld", (long long)e,
                          (long long)cnt[e], (long long)tau));
+    h->tau = tau;  // QuantScheme.tau (scheme file)
   });
 }
 
@@ -581,6 +590,33 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, co
   });
 }
 
+cl_status cl_moe_route_tokens_f32(cl_moe* h, const float* hidden, int64_t T, const cl_moe_decision* out,
+                                  void* stream) {
+  return guarded(h, [&] {
+    if (!hidden) throw ConfigErr("hidden is null");
+    CK(cudaSetDevice(h->cfg.device));
+    run_router(h, hidden, T, (cudaStream_t)stream, true, false, true);
+    export_decision(h, T, out, (cudaStream_t)stream);
+  });
+}
+
+cl_status cl_moe_forward_f32(cl_moe* h, const float* hidden, int64_t T, float* out, const cl_moe_decision* decision,
+                             void* stream) {
+  return guarded(h, [&] {
+    if (!hidden || !out) throw ConfigErr("null argument");
+    if (T < 1) throw RunErr("moe_forward: B must be >= 1");
+    if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
+    CK(cudaSetDevice(h->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!h->x16) h->x16 = dalloc<__nv_bfloat16>(h->cap * h->d);
+    const int64_t n = T * h->d;
+    f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(hidden, n, h->x16);  // the expert GEMMs' operand
+    CK(cudaGetLastError());
+    run_forward(h, h->x16, T, out, true, st, hidden, true);
+    export_decision(h, T, decision, st);
+  });
+}
+
 // The single-GPU forward captured once per (hidden, out, T, precision) into a CUDA graph and
 // replayed: the six kernels and two counter memsets go out as one launch.
 cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* out, void* stream) {
@@ -650,7 +686,9 @@ static void host_enqueue(cl_moe* h, const void* hidden_host, int64_t T, void* ou
     f32_to_bf16_kernel<<<grid_for(n), 256, 0, st>>>(sl.xf, n, static_cast<__nv_bfloat16*>(sl.x));
     CK(cudaGetLastError());
   }
-  run_forward(h, sl.x, T, sl.out, f32, st);
+  // fp32 host tensors: routed on their own fp32 values (bit-exact with the reference's gating on
+  // the same Tensor); the expert GEMMs take the bf16 rounding
+  run_forward(h, sl.x, T, sl.out, f32, st, f32 ? sl.xf : nullptr, f32);
   CK(cudaEventRecord(sl.done, st));
   CK(cudaStreamWaitEvent(h->s_d2h, sl.done, 0));
   CK(cudaMemcpyAsync(out_host, sl.out, n * (f32 ? 4 : 2), cudaMemcpyDeviceToHost, h->s_d2h));
@@ -843,16 +881,17 @@ cl_status cl_moe_compute_smoothing(cl_moe* h, float alpha, float* s_out) {
                                           std::pow(static_cast<double>(m), 1.0 - alpha))
                      : 1.0f;
     }
+    h->alpha_smooth = alpha;
   });
 }
 
-cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s) {
-  return guarded(h, [&] {
-    if (!s) throw ConfigErr("s is null");
+static void fold_smoothing_impl(cl_moe* h, const float* s) {
     const int64_t d = h->d, N = h->N;
     for (int64_t l = 0; l < d; ++l)
       if (!(s[l] > 0.0f) || !std::isfinite(s[l])) throw ConfigErr("smoothing factors must be finite and > 0");
     CK(cudaSetDevice(h->cfg.device));
+    if (h->smooth_applied.empty()) h->smooth_applied.assign(d, 1.0f);
+    for (int64_t l = 0; l < d; ++l) h->smooth_applied[l] *= s[l];
     CK(cudaMemcpy(h->smooth, s, sizeof(float) * d, cudaMemcpyHostToDevice));
     const int64_t n = (int64_t)h->n_local * 2 * h->f * d;
     scale_cols_bf16_kernel<<<grid_for(n), 256>>>(h->win, n, (int)d, h->smooth);
@@ -866,6 +905,12 @@ cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s) {
     h->train_ready = false;
     CK(cudaMemset(h->calib, 0, sizeof(float) * 2 * h->n_local));
     CK(cudaMemset(h->calib_ch, 0, sizeof(float) * d));
+}
+
+cl_status cl_moe_fold_smoothing(cl_moe* h, const float* s) {
+  return guarded(h, [&] {
+    if (!s) throw ConfigErr("s is null");
+    fold_smoothing_impl(h, s);
   });
 }
 
@@ -906,6 +951,28 @@ cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float*
       if (!(sin_all[g] > 0.0f)) throw ConfigErr("activation scales must be > 0");
     for (int e = 0; e < NL; ++e)
       if (!(smid[e] > 0.0f)) throw ConfigErr("activation scales must be > 0");
+    // router: per-tensor activation scale = max |hidden| over the calibration tokens
+    // / 448 (all ranks' maxima under EP), unless set explicitly; W_r per expert column
+    if (!h->sxr_explicit) {
+      std::vector<float> ch(h->d);
+      if (h->comm) {
+        cudaStream_t st = nullptr;
+        NCK(NcclApi::get().AllReduce(h->calib_ch, h->calib_ch, (size_t)h->d, NcclApi::kFloat32, NcclApi::kMax, h->comm,
+                                     st));
+        CK(cudaStreamSynchronize(st));
+      }
+      CK(cudaMemcpy(ch.data(), h->calib_ch, sizeof(float) * h->d, cudaMemcpyDeviceToHost));
+      float m = 0.0f;
+      for (float v : ch) m = std::max(m, v);
+      if (h->router_fp8 && !(m > 0.0f))
+        throw RunErr("quantize_model: missing calibration for the router (calibrate, or cl_moe_set_router_fp8 "
+                     "with an explicit activation scale)");
+      h->sxr = m > 0.0f ? m / 448.0f : 1.0f;
+    }
+    CK(cudaMemcpy(h->sxr_dev, &h->sxr, sizeof(float), cudaMemcpyHostToDevice));
+    router_qdq_w_kernel<<<(int)((N + 127) / 128), 128>>>(h->wr, (int)h->d, N, h->wrq, h->wsr);
+    widen_router_kernel<<<grid_for(h->d * N), 256>>>(h->wrq, (int)h->d, N, h->wr64q);
+    CK(cudaGetLastError());
     CK(cudaMemcpy(h->sx_in_all, sin_all.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->sx_in, sin_all.data() + h->e0, sizeof(float) * NL, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->sx_mid, smid.data(), sizeof(float) * NL, cudaMemcpyHostToDevice));
@@ -924,6 +991,150 @@ cl_status cl_moe_set_precision(cl_moe* h, int32_t precision) {
     if (precision != CL_MOE_BF16 && precision != CL_MOE_FP8_E4M3) throw ConfigErr("unknown precision");
     if (precision == CL_MOE_FP8_E4M3 && !h->fp8_ready) throw ConfigErr("FP8 scheme not quantized yet");
     h->precision = precision;
+  });
+}
+
+// ---- FP8 scheme file: JSON manifest + binary scale arrays (scheme.hpp) ----
+// W_in's packed row p of an expert (256-row n-blocks of 128 gate + 128 up rows) <-> reference column
+static int64_t win_col_of_packed_row(int64_t p, int64_t f) {
+  const int64_t b = p / 256, i = p % 256;
+  return i < 128 ? b * 128 + i : f + b * 128 + (i - 128);
+}
+
+cl_status cl_moe_save_fp8_scheme(cl_moe* h, const char* path) {
+  return guarded(h, [&] {
+    if (!path) throw ConfigErr("path is null");
+    if (!h->fp8_ready) throw ConfigErr("FP8 scheme not quantized yet");
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaDeviceSynchronize());
+    const int64_t d = h->d, N = h->N, NL = h->n_local, f = h->f;
+    Scheme sc;
+    sc.d = d;
+    sc.N = N;
+    sc.f = f;
+    sc.n_local = NL;
+    sc.expert0 = h->e0;
+    sc.ep_size = h->cfg.ep_size;
+    sc.alpha = h->alpha_smooth;
+    sc.tau = h->tau;
+    sc.router_fp8 = h->router_fp8;
+    auto add = [&](const char* name, std::vector<int64_t> shape, std::vector<float> v) {
+      sc.arrays.push_back(SchemeArray{name, std::move(shape), std::move(v)});
+    };
+    add("smoothing", {d}, h->smooth_applied.empty() ? std::vector<float>(d, 1.0f) : h->smooth_applied);
+    std::vector<float> v(N);
+    CK(cudaMemcpy(v.data(), h->sx_in_all, sizeof(float) * N, cudaMemcpyDeviceToHost));
+    add("act_scale_in", {N}, v);
+    v.resize(NL);
+    CK(cudaMemcpy(v.data(), h->sx_mid, sizeof(float) * NL, cudaMemcpyDeviceToHost));
+    add("act_scale_mid", {NL}, v);
+    std::vector<float> packed(NL * 2 * f);
+    CK(cudaMemcpy(packed.data(), h->ws_in, sizeof(float) * NL * 2 * f, cudaMemcpyDeviceToHost));
+    v.assign(NL * 2 * f, 0.0f);
+    for (int64_t e = 0; e < NL; ++e)
+      for (int64_t p = 0; p < 2 * f; ++p) v[e * 2 * f + win_col_of_packed_row(p, f)] = packed[e * 2 * f + p];
+    add("w_in_scale", {NL, 2 * f}, v);
+    v.resize(NL * d);
+    CK(cudaMemcpy(v.data(), h->ws_out, sizeof(float) * NL * d, cudaMemcpyDeviceToHost));
+    add("w_out_scale", {NL, d}, v);
+    add("router_act_scale", {1}, std::vector<float>{h->sxr});
+    v.resize(N);
+    CK(cudaMemcpy(v.data(), h->wsr, sizeof(float) * N, cudaMemcpyDeviceToHost));
+    add("router_w_scale", {N}, v);
+    write_scheme(path, sc);
+  });
+}
+
+cl_status cl_moe_load_fp8_scheme(cl_moe* h, const char* path) {
+  return guarded(h, [&] {
+    if (!path) throw ConfigErr("path is null");
+    const Scheme sc = read_scheme(path);
+    const int64_t d = h->d, N = h->N, NL = h->n_local, f = h->f;
+    if (sc.d != d || sc.N != N || sc.f != f || sc.n_local != NL || sc.expert0 != h->e0)
+      throw ConfigErr(fmt("scheme is for d=%lld N=%lld f=%lld experts [%lld, +%lld), this layer d=%lld N=%lld f=%lld "
+                          "[%d, +%d)", (long long)sc.d, (long long)sc.N, (long long)sc.f, (long long)sc.expert0,
+                          (long long)sc.n_local, (long long)d, (long long)N, (long long)f, h->e0, NL));
+    auto arr = [&](const char* name, int64_t n) -> const std::vector<float>& {
+      const SchemeArray& a = sc.get(name);
+      if ((int64_t)a.data.size() != n) throw ConfigErr(fmt("scheme array %s has %zu values, expected %lld", name,
+                                                           a.data.size(), (long long)n));
+      return a.data;
+    };
+    // smoothing: fold it unless this layer already carries exactly that fold
+    const std::vector<float>& s = arr("smoothing", d);
+    const bool ident = std::all_of(s.begin(), s.end(), [](float x) { return x == 1.0f; });
+    const bool have = !h->smooth_applied.empty() &&
+                      !std::all_of(h->smooth_applied.begin(), h->smooth_applied.end(), [](float x) { return x == 1.0f; });
+    if (have && h->smooth_applied != s)
+      throw ConfigErr("scheme smoothing vector differs from the one already folded into this layer");
+    if (!ident && !have) fold_smoothing_impl(h, s.data());
+    CK(cudaSetDevice(h->cfg.device));
+    ensure_fp8_storage(h);
+    const std::vector<float>& sin = arr("act_scale_in", N);
+    const std::vector<float>& smid = arr("act_scale_mid", NL);
+    const std::vector<float>& wi = arr("w_in_scale", NL * 2 * f);
+    const std::vector<float>& wo = arr("w_out_scale", NL * d);
+    const float sxr = arr("router_act_scale", 1)[0];
+    const std::vector<float>& wsr = arr("router_w_scale", N);
+    for (const auto* v : {&sin, &smid, &wi, &wo, &wsr})
+      for (float x : *v)
+        if (!(x > 0.0f) || !std::isfinite(x)) throw ConfigErr("scheme scales must be finite and > 0");
+    if (!(sxr > 0.0f) || !std::isfinite(sxr)) throw ConfigErr("scheme scales must be finite and > 0");
+    std::vector<float> packed(NL * 2 * f);
+    for (int64_t e = 0; e < NL; ++e)
+      for (int64_t p = 0; p < 2 * f; ++p) packed[e * 2 * f + p] = wi[e * 2 * f + win_col_of_packed_row(p, f)];
+    CK(cudaMemcpy(h->sx_in_all, sin.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sx_in, sin.data() + h->e0, sizeof(float) * NL, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->sx_mid, smid.data(), sizeof(float) * NL, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->ws_in, packed.data(), sizeof(float) * NL * 2 * f, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->ws_out, wo.data(), sizeof(float) * NL * d, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->wsr, wsr.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
+    h->sxr = sxr;
+    h->sxr_explicit = true;
+    h->router_fp8 = sc.router_fp8 ? 1 : 0;
+    CK(cudaMemcpy(h->sxr_dev, &h->sxr, sizeof(float), cudaMemcpyHostToDevice));
+    const int64_t r1 = NL * 2 * f, r2 = NL * d;
+    quantize_rows_e4m3_kernel<<<(int)((r1 + 7) / 8), 256>>>(h->win, r1, (int)d, h->win8, h->ws_in, true);
+    quantize_rows_e4m3_kernel<<<(int)((r2 + 7) / 8), 256>>>(h->wout, r2, (int)f, h->wout8, h->ws_out, true);
+    router_qdq_w_kernel<<<(int)((N + 127) / 128), 128>>>(h->wr, (int)d, (int)N, h->wrq, h->wsr, true);
+    widen_router_kernel<<<grid_for(d * N), 256>>>(h->wrq, (int)d, (int)N, h->wr64q);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    h->alpha_smooth = sc.alpha;
+    h->tau = sc.tau;
+    h->fp8_ready = true;
+    h->precision = CL_MOE_FP8_E4M3;
+  });
+}
+
+cl_status cl_moe_set_router_fp8(cl_moe* h, int32_t enable, float act_scale) {
+  return guarded(h, [&] {
+    if (enable != 0 && enable != 1) throw ConfigErr("enable must be 0 or 1");
+    if (act_scale < 0.0f || !std::isfinite(act_scale)) throw ConfigErr("act_scale must be finite and >= 0");
+    h->router_fp8 = enable;
+    h->sxr_explicit = act_scale > 0.0f;
+    if (h->sxr_explicit) {
+      h->sxr = act_scale;
+      if (h->sxr_dev) {
+        CK(cudaSetDevice(h->cfg.device));
+        CK(cudaMemcpy(h->sxr_dev, &h->sxr, sizeof(float), cudaMemcpyHostToDevice));
+      }
+    }
+  });
+}
+
+cl_status cl_moe_get_router_fp8(cl_moe* h, int32_t* enable, float* act_scale, float* w_scale) {
+  return guarded(h, [&] {
+    if (enable) *enable = h->router_fp8;
+    if (act_scale || w_scale) {
+      if (!h->fp8_ready) throw ConfigErr("FP8 scheme not quantized yet");
+      if (act_scale) *act_scale = h->sxr;
+      if (w_scale) {
+        CK(cudaSetDevice(h->cfg.device));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(w_scale, h->wsr, sizeof(float) * h->N, cudaMemcpyDeviceToHost));
+      }
+    }
   });
 }
 

@@ -43,13 +43,64 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG>, a, b, args));
 }
 
-// route_tokens on device: K1 + K2.
+// K1 launch for router input type XT (bf16 storage, or the caller's fp32 tensor): the variant and
+// tile geometry were chosen by run_router (tpc does not depend on XT).
+template <typename XT>
+void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, int n_tiles, int variant, int ws_cons,
+                   int big_tok, int lat_chunk, int* tail, float* rwd, int32_t* invd, cudaStream_t st) {
+  constexpr int xb = sizeof(XT);
+  const int d = (int)h->d, K = (int)h->K;
+  switch (variant) {
+    case 4:  // ws
+      if (ws_cons == 32)
+        router_ws_kernel<32, XT><<<n_tiles, 32 + 64, RouterWsSmem(N, 32, xb).total, st>>>(x, w64, (int)T, d, N, K,
+                                                                                          h->rb, tail, rwd, invd);
+      else if (ws_cons == 64)
+        router_ws_kernel<64, XT><<<n_tiles, 64 + 64, RouterWsSmem(N, 64, xb).total, st>>>(x, w64, (int)T, d, N, K,
+                                                                                          h->rb, tail, rwd, invd);
+      else
+        router_ws_kernel<128, XT><<<n_tiles, 128 + 64, RouterWsSmem(N, 128, xb).total, st>>>(x, w64, (int)T, d, N,
+                                                                                             K, h->rb, tail, rwd, invd);
+      break;
+    case 3:  // lat (bf16 only: the A/B variant kept from round 1)
+      if constexpr (xb == 2) {
+        if (lat_chunk == 256)
+          router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(x, w64, (int)T, d, N, K, h->rb);
+        else if (lat_chunk == 128)
+          router_lat_kernel<3, 128><<<n_tiles, 128, RouterLatSmem<3, 128>(N).total, st>>>(x, w64, (int)T, d, N, K, h->rb);
+        else
+          router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(x, w64, (int)T, d, N, K, h->rb);
+      }
+      break;
+    case 2:  // big
+      if (big_tok == 2)
+        router_big_kernel<32, 3, 2, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 2, xb).total, st>>>(x, w64, (int)T, d,
+                                                                                                  N, K, h->rb);
+      else
+        router_big_kernel<32, 3, 4, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 4, xb).total, st>>>(x, w64, (int)T, d,
+                                                                                                  N, K, h->rb);
+      break;
+    case 1:  // small
+      router_kernel<32, 8, XT><<<n_tiles, 32, router_smem_bytes(N, 32, 8, xb), st>>>(x, w64, (int)T, d, N, K, h->rb);
+      break;
+    default:
+      router_kernel<128, 3, XT><<<n_tiles, 128, router_smem_bytes(N, 128, 3, xb), st>>>(x, w64, (int)T, d, N, K,
+                                                                                       h->rb);
+  }
+}
+
+// route_tokens on device: K1 + K2. `xf32`: x is the caller's fp32 tensor (routing on the
+// reference's own values), else bf16.
 // dense = true (dense decode): the 128-thread warp-specialised router with the plan and the dense
 // row weights fused into its last CTA, when that variant applies (returns whether it did).
-bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_prof = true, bool dense = false) {
+bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_prof = true, bool dense = false,
+                bool xf32 = false) {
   if (T < 1) throw RunErr("route_tokens: B must be >= 1");
   if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
   const int N = static_cast<int>(h->N);
+  // FP8 scheme: the router consumes qdq(x) as fp32 (see below), so size the variants for fp32
+  const bool rq = h->precision == CL_MOE_FP8_E4M3 && h->router_fp8;
+  const int xb = xf32 || rq ? 4 : 2;
   // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
   // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
@@ -66,7 +117,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   const int tiles4 = (int)((T + RouterBigSmem(N, 32, 3, 4).tpc - 1) / RouterBigSmem(N, 32, 3, 4).tpc);
   const int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
   const int tpc_big = RouterBigSmem(N, 32, 3, big_tok).tpc;
-  const bool big_ok = RouterBigSmem(N, 32, 3, big_tok).total <= 220 * 1024;
+  const bool big_ok = RouterBigSmem(N, 32, 3, big_tok, xb).total <= 220 * 1024;
   const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
   // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
   const int N4r = (N + 3) / 4 * 4;
@@ -75,55 +126,48 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   const bool lat_size = (T + tpc_lat - 1) / tpc_lat <= h->num_sms;
   // decode-size batches: the warp-specialised chain kernel (ws), on the smallest CTA (32 / 64 / 128
   // chain threads) that still gives every CTA its own SM; CL_MOE_ROUTER=lat keeps the older variant
-  const bool ws = !big && (force == 4 || (force == 0 && lat_size));
+  // (bf16 input only; fp32 input takes ws)
+  const bool ws = !big && (force == 4 || (force == 0 && lat_size) || (force == 3 && xb == 4));
   const bool lat = !big && !ws && (force == 3 || (force == 0 && lat_size));
   int ws_cons = 128;
   for (int c : {32, 64}) {
-    const int tp = RouterWsSmem(N, c).tpc;
+    const int tp = RouterWsSmem(N, c, xb).tpc;
     if (ws_cons == 128 && tp >= 1 && (T + tp - 1) / tp <= h->num_sms) ws_cons = c;
   }
   if (dense) ws_cons = 128;  // dense decode: fewest CTAs (the router runs beside GEMM1)
-  const bool fuse = dense && ws && RouterWsSmem(N, 128).tpc >= 1 && h->route_ctr;  // (ensure_dense allocates)
+  const bool fuse = dense && ws && RouterWsSmem(N, 128, xb).tpc >= 1 && h->route_ctr;  // (ensure_dense allocates)
   int* tail = fuse ? h->route_ctr : nullptr;
   float* rwd = fuse ? h->rwd : nullptr;
   int32_t* invd = fuse ? h->invd : nullptr;
-  const bool small = !big && !lat && !ws && router_smem_bytes(N, 32, 8) <= 220 * 1024;
-  const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons).tpc : lat ? tpc_lat
+  const bool small = !big && !lat && !ws && router_smem_bytes(N, 32, 8, xb) <= 220 * 1024;
+  const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
                                  : router_tokens_per_cta(N, small ? 32 : 128);
+  const int variant = ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
   h->tpc_cur = tpc;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
   if (own_prof) prof_begin(h, st);
-  if (ws && ws_cons == 32)
-    router_ws_kernel<32><<<n_tiles, 32 + 64, RouterWsSmem(N, 32).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
-  else if (ws && ws_cons == 64)
-    router_ws_kernel<64><<<n_tiles, 64 + 64, RouterWsSmem(N, 64).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
-  else if (ws)
-    router_ws_kernel<128><<<n_tiles, 128 + 64, RouterWsSmem(N, 128).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb, tail, rwd, invd);
-  else if (lat && lat_chunk == 256)
-    router_lat_kernel<3, 256><<<n_tiles, 128, RouterLatSmem<3, 256>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (lat && lat_chunk == 128)
-    router_lat_kernel<3, 128><<<n_tiles, 128, RouterLatSmem<3, 128>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (lat)
-    router_lat_kernel<3, 64><<<n_tiles, 128, RouterLatSmem<3, 64>(N).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (big && big_tok == 2)
-    router_big_kernel<32, 3, 2><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 2).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (big)
-    router_big_kernel<32, 3><<<n_tiles, 32, RouterBigSmem(N, 32, 3).total, st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
-  else if (small)
-    router_kernel<32, 8><<<n_tiles, 32, router_smem_bytes(N, 32, 8), st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+  const double* w64 = h->wr64;
+  if (rq) {
+    // router GEMM under the FP8 scheme: x_hat = qdq(x, s_x) per tensor, W_r_hat per
+    // expert column (quantize time); the fp64 chains then run on x_hat exactly as on an fp32 input
+    const int64_t n = T * h->d;
+    if (xf32)
+      router_qdq_x_kernel<float><<<grid_for(n / 8), 256, 0, st>>>(static_cast<const float*>(x), n, h->sxr_dev, h->xq32);
+    else
+      router_qdq_x_kernel<__nv_bfloat16><<<grid_for(n / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n,
+                                                                           h->sxr_dev, h->xq32);
+    CK(cudaGetLastError());
+    x = h->xq32;
+    xf32 = true;
+    w64 = h->wr64q;
+  }
+  if (xf32)
+    launch_router<float>(h, static_cast<const float*>(x), w64, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail,
+                         rwd, invd, st);
   else
-    router_kernel<128, 3><<<n_tiles, 128, router_smem_bytes(N, 128, 3), st>>>(
-        static_cast<const __nv_bfloat16*>(x), h->wr64, (int)T, (int)h->d, N, (int)h->K, h->rb);
+    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), w64, T, N, n_tiles, variant, ws_cons, big_tok,
+                                 lat_chunk, tail, rwd, invd, st);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
   if (!fuse) launch_plan(n_tiles, (int)T, N, (int)h->K, h->rb, st);
@@ -304,9 +348,13 @@ void ensure_dense(cl_moe* h) {
 
 // route_tokens + moe_forward of the single-GPU layer: dense decode when eligible, else the
 // sparse path (router, plan, dispatch, grouped GEMMs, combine).
-void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st) {
+// xr (nullable): the router's input when it differs from the GEMM operand x — the caller's fp32
+// tensor (xr_f32), routed on its own values while the experts take its bf16 rounding.
+void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st,
+                 const void* xr = nullptr, bool xr_f32 = false) {
+  if (!xr) xr = x;
   if (!dense_ok(h, T)) {
-    run_router(h, x, T, st);
+    run_router(h, xr, T, st, true, false, xr_f32);
     run_experts(h, x, T, out, out_f32, st);
     return;
   }
@@ -316,7 +364,7 @@ void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   prof_begin(h, st, 2);
   CK(cudaEventRecord(h->ev_fork, st));
   CK(cudaStreamWaitEvent(h->s_route, h->ev_fork, 0));
-  if (!run_router(h, x, T, h->s_route, false, true)) {  // plan + row weights not fused (other variant)
+  if (!run_router(h, xr, T, h->s_route, false, true, xr_f32)) {  // plan + row weights not fused (other variant)
     dense_weights_kernel<<<(int)((N * T + 255) / 256), 256, 0, h->s_route>>>(h->rb.topk_idx, h->rb.combine_w, (int)T,
                                                                              N, K, h->rwd, h->invd);
     CK(cudaGetLastError());
@@ -364,6 +412,13 @@ void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_
 }
 
 void ensure_fp8_storage(cl_moe* h) {
+  if (!h->xq32) {  // router under the FP8 scheme
+    h->sxr_dev = dalloc<float>(1);
+    h->wrq = dalloc<float>(h->d * h->N);
+    h->wsr = dalloc<float>(h->N);
+    h->wr64q = dalloc<double>(3 * h->d * ((h->N + 3) / 4 * 4));
+    h->xq32 = dalloc<float>(h->cap * h->d);
+  }
   if (h->win8) return;
   h->win8 = dalloc<uint8_t>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout8 = dalloc<uint8_t>((size_t)h->n_local * h->d * h->f);

@@ -102,6 +102,19 @@ struct cl_moe {
   long long* calib_counts = nullptr;   // [N] routing counts over calibration tokens
   float* smooth = nullptr;             // [d] scratch for fold_smoothing
   bool fp8_ready = false;
+  // router under the FP8 scheme: qdq'd W_r and the per-tensor activation scale
+  int router_fp8 = 1;                  // 1: router GEMM through fp8_qdq in FP8 mode; 0: fp32 gating
+  float sxr = 0.0f;                    // router activation scale (host copy; 0 = from calibration)
+  bool sxr_explicit = false;
+  float* sxr_dev = nullptr;            // [1]
+  float* wrq = nullptr;                // [d][N] qdq(W_r) fp32
+  float* wsr = nullptr;                // [N] router weight scales (per expert column)
+  double* wr64q = nullptr;             // widened qdq(W_r), same layout as wr64
+  float* xq32 = nullptr;               // [cap][d] qdq(x) fp32 (router operand)
+  // QuantScheme bookkeeping (scheme file)
+  std::vector<float> smooth_applied;   // product of the folded smoothing vectors (empty: none)
+  double alpha_smooth = NAN;           // alpha of the last compute_smoothing
+  int64_t tau = -1;                    // tau of the last balance_calibration
 
   // workspaces
   RouteBufs rb{};
@@ -123,6 +136,7 @@ struct cl_moe {
   } slot[2];
   int next_slot = 0;
   void* io_out = nullptr;              // calibration output scratch
+  __nv_bfloat16* x16 = nullptr;        // [cap][d] bf16 GEMM operand of a device fp32 forward
   cudaStream_t own_stream = nullptr;   // compute stream of the host-buffer path
   // captured forwards (cl_moe_forward_graph), keyed by buffers, T and precision
   struct GraphEntry {
@@ -231,7 +245,8 @@ struct cl_moe {
                     (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
                     (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
-                    (void*)row_ptr_dx, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr})
+                    (void*)row_ptr_dx, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr, (void*)x16, (void*)sxr_dev, (void*)wrq,
+                    (void*)wsr, (void*)wr64q, (void*)xq32})
       if (p) cudaFree(p);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
@@ -397,6 +412,14 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_ws_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  // fp32-input instantiations (routing on the caller's fp32 tensor)
+  CK(cudaFuncSetAttribute(router_kernel<128, 3, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_kernel<32, 8, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 2, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<32, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<64, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<128, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);

@@ -39,12 +39,12 @@ __host__ __device__ inline int router_tokens_per_cta(int n_experts, int threads)
 struct RouterSmem {
   int tpc, N4, xs;
   size_t raw_x, sw, sx, slog, sidx, slse, total;
-  __host__ __device__ RouterSmem(int n_experts, int threads, int stages) {
+  __host__ __device__ RouterSmem(int n_experts, int threads, int stages, int xb = 2) {
     N4 = (n_experts + 3) / 4 * 4;
     tpc = router_tokens_per_cta(n_experts, threads);
     xs = kRouterChunk + 2;  // padded fp64 row of one token: 16-byte aligned, conflict-free double2 loads
     raw_x = 0;
-    sw = raw_x + (size_t)stages * tpc * kRouterChunk * 2;     // [stages][chunk][N4] fp64 (cp.async target)
+    sw = raw_x + (size_t)stages * tpc * kRouterChunk * xb;    // [stages][chunk][N4] fp64 (cp.async target)
     sx = sw + (size_t)stages * sizeof(double) * kRouterChunk * N4;  // [tpc][xs] fp64
     slog = sx + sizeof(double) * tpc * xs;
     sidx = slog + sizeof(float) * tpc * N4;
@@ -52,8 +52,8 @@ struct RouterSmem {
     total = slse + sizeof(double) * tpc;
   }
 };
-__host__ __device__ inline size_t router_smem_bytes(int n_experts, int threads, int stages) {
-  return RouterSmem(n_experts, threads, stages).total;
+__host__ __device__ inline size_t router_smem_bytes(int n_experts, int threads, int stages, int xb = 2) {
+  return RouterSmem(n_experts, threads, stages, xb).total;
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
@@ -63,6 +63,22 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Router input element: bf16 (the device path's storage type) or fp32 (the reference's own Tensor
+// values). Either widens exactly to fp64, and a float x float product is exact in
+// fp64, so the ascending-l chains stay bit-identical to gemm_nn for both.
+template <typename XT>
+__device__ __forceinline__ double x_to_f64(XT v) {
+  if constexpr (sizeof(XT) == 2) return static_cast<double>(__bfloat162float(v));
+  else return static_cast<double>(v);
+}
+// 16 bytes of raw x -> its 8 (bf16) or 4 (fp32) values in fp64
+template <typename XT>
+__device__ __forceinline__ void widen16(const int4& raw, double* out) {
+  const XT* v = reinterpret_cast<const XT*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 16 / (int)sizeof(XT); ++i) out[i] = x_to_f64<XT>(v[i]);
+}
 
 // Chunk length (steps) of router_ws_kernel's ring, by padded expert count.
 __host__ __device__ inline int router_ws_chunk(int N4) { return N4 <= 16 ? 256 : N4 <= 32 ? 128 : N4 <= 64 ? 64 : 32; }
@@ -166,11 +182,12 @@ __device__ __forceinline__ void router_finish(int tile, int tok0, int tpc, int T
 // (tensor.cpp:1046-1060), renormalised combine weights, per-tile expert counts
 // and local ranks for the stable dispatch permutation, and per-tile partial sums for agg_prob
 // (col_sums, tensor.cpp:545-565) and the Z-loss (tensor.cpp:1011-1040).
-template <int kRouterThreads, int kStages>
-__global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bfloat16* __restrict__ x,
+template <int kRouterThreads, int kStages, typename XT = __nv_bfloat16>
+__global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const XT* __restrict__ x,
                                                                 const double* __restrict__ wr64, int T, int d,
                                                                 int N, int K, RouteBufs rb) {
-  const RouterSmem L(N, kRouterThreads, kStages);
+  constexpr int kXB = sizeof(XT), kPerPiece = 16 / kXB;  // x elements per 16-byte cp.async piece
+  const RouterSmem L(N, kRouterThreads, kStages, kXB);
   const int groups = L.N4 / 4;
   const int N4 = L.N4;
   const int tg_per_cta = kRouterThreads / groups;
@@ -179,7 +196,7 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
   const int tile = blockIdx.x;
   const int tok0 = tile * tpc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  __nv_bfloat16* rawx = reinterpret_cast<__nv_bfloat16*>(smem_raw + L.raw_x);  // [2][tpc][chunk]
+  XT* rawx = reinterpret_cast<XT*>(smem_raw + L.raw_x);                        // [stages][tpc][chunk]
   double* sw = reinterpret_cast<double*>(smem_raw + L.sw);                     // [2][chunk][N4]
   double* sx = reinterpret_cast<double*>(smem_raw + L.sx);                     // [tpc][xs]
   float* slog = reinterpret_cast<float*>(smem_raw + L.slog);                   // [tpc][N4]
@@ -196,15 +213,15 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
   const int nchunks = d / kRouterChunk;
-  const int xpieces = tpc * kRouterChunk * 2 / 16;  // 16-byte pieces of one x chunk
+  const int xpieces = tpc * kRouterChunk * kXB / 16;  // 16-byte pieces of one x chunk
   const int wpieces = kRouterChunk * N4 * 8 / 16;
   auto issue = [&](int c, int buf) {
     const int c0 = c * kRouterChunk;
     for (int i = threadIdx.x; i < xpieces; i += kRouterThreads) {
-      const int r = i / (kRouterChunk / 8), q = i % (kRouterChunk / 8);
+      const int r = i / (kRouterChunk / kPerPiece), q = i % (kRouterChunk / kPerPiece);
       const bool ok = tok0 + r < T;
-      const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
-      cp_async16(rawx + (size_t)buf * tpc * kRouterChunk + r * kRouterChunk + q * 8, src, ok);
+      const XT* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * kPerPiece;
+      cp_async16(rawx + (size_t)buf * tpc * kRouterChunk + r * kRouterChunk + q * kPerPiece, src, ok);
     }
     const double* wsrc = wr64 + (size_t)c0 * N4;
     for (int i = threadIdx.x; i < wpieces; i += kRouterThreads)
@@ -222,12 +239,17 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const __nv_bf
     if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
     else cp_async_commit();
     // widen x to fp64, [tok][l] layout
-    const __nv_bfloat16* rx = rawx + (size_t)buf * tpc * kRouterChunk;
+    const XT* rx = rawx + (size_t)buf * tpc * kRouterChunk;
     for (int i = threadIdx.x; i < tpc * kRouterChunk / 2; i += kRouterThreads) {
       const int r = (2 * i) / kRouterChunk, l = (2 * i) % kRouterChunk;
-      const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(rx)[i];
-      *reinterpret_cast<double2*>(sx + r * xs + l) =
-          make_double2(static_cast<double>(__low2float(v)), static_cast<double>(__high2float(v)));
+      if constexpr (kXB == 2) {
+        const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(rx)[i];
+        *reinterpret_cast<double2*>(sx + r * xs + l) =
+            make_double2(static_cast<double>(__low2float(v)), static_cast<double>(__high2float(v)));
+      } else {
+        const float2 v = reinterpret_cast<const float2*>(rx)[i];
+        *reinterpret_cast<double2*>(sx + r * xs + l) = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+      }
     }
     __syncthreads();
     if (worker) {
@@ -530,19 +552,19 @@ struct RouterWsSmem {
   static constexpr int kAhead = 16;  // ring distance (steps); loads run up to kAhead past a row
   int tpc, N4, chunk, wpitch, stages;
   size_t sw, rx, xd, bars, slog, sidx, slse, total;
-  __host__ __device__ RouterWsSmem(int n_experts, int cons) {
+  __host__ __device__ RouterWsSmem(int n_experts, int cons, int xb = 2) {
     N4 = (n_experts + 3) / 4 * 4;
     tpc = cons / N4;
     chunk = router_ws_chunk(N4);
     wpitch = chunk + 2;  // doubles per expert row
     // as many ring slots as ~200 KB allow (the producer runs several L2 round trips ahead)
-    const size_t slot = (size_t)N4 * wpitch * 8 + ((size_t)tpc * chunk * 2 + 15) / 16 * 16 + (size_t)tpc * chunk * 8;
+    const size_t slot = (size_t)N4 * wpitch * 8 + ((size_t)tpc * chunk * xb + 15) / 16 * 16 + (size_t)tpc * chunk * 8;
     const size_t fixed = 4096;
     stages = (int)(((size_t)200 * 1024 - fixed) / slot);
     stages = stages < 2 ? 2 : stages > kMaxStages ? kMaxStages : stages;
     sw = 0;                                                          // [stages][N4][wpitch] fp64
-    rx = sw + (size_t)stages * N4 * wpitch * 8;                      // [stages][tpc][chunk] bf16
-    xd = rx + ((size_t)stages * tpc * chunk * 2 + 15) / 16 * 16;     // [stages][tpc][chunk] fp64
+    rx = sw + (size_t)stages * N4 * wpitch * 8;                      // [stages][tpc][chunk] bf16 / fp32
+    xd = rx + ((size_t)stages * tpc * chunk * xb + 15) / 16 * 16;    // [stages][tpc][chunk] fp64
     bars = xd + (size_t)stages * tpc * chunk * 8;                    // full[kMaxStages] + flags
     // flags: xflag[kMaxStages] + eflag[kMaxChainWarps] (round 1 reserved only 4 eflag slots, so a
     // 256-thread instantiation's eflag[4..7] aliased slog[0..3]: the logits of the tile's token 0)
@@ -703,8 +725,8 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
 
 // tail_ctr (dense decode, nullable): the last CTA to finish also runs the plan (plan_body<128>)
 // and the dense row weights / combine rows, so nothing queues behind GEMM1's persistent CTAs.
-template <int kCons>
-__global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfloat16* __restrict__ x,
+template <int kCons, typename XT = __nv_bfloat16>
+__global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const XT* __restrict__ x,
                                                                  const double* __restrict__ wr64, int T, int d,
                                                                  int N, int K, RouteBufs rb,
                                                                  int* __restrict__ tail_ctr = nullptr,
@@ -712,14 +734,15 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
                                                                  int32_t* __restrict__ invd = nullptr) {
   constexpr int kD = RouterWsSmem::kAhead, kB = 32;
   static_assert(kCons % 32 == 0 && kCons / 32 <= RouterWsSmem::kMaxChainWarps, "eflag region holds one slot per chain warp");
-  const RouterWsSmem L(N, kCons);
+  constexpr int kXB = sizeof(XT);
+  const RouterWsSmem L(N, kCons, kXB);
   const int N4 = L.N4, tpc = L.tpc, chunk = L.chunk, wpitch = L.wpitch, kStages = L.stages;
   const double* wt = wr64 + (size_t)d * N4;  // per chunk [N4][wpitch] (widen_router_kernel)
   const int tok0 = blockIdx.x * tpc;
   const int ntok = min(tpc, T - tok0);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   double* sw = reinterpret_cast<double*>(smem_raw + L.sw);
-  __nv_bfloat16* rawx = reinterpret_cast<__nv_bfloat16*>(smem_raw + L.rx);
+  XT* rawx = reinterpret_cast<XT*>(smem_raw + L.rx);
   double* xd = reinterpret_cast<double*>(smem_raw + L.xd);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.bars);
   // the chain side synchronises through chunk-granular flags (CTA-scope release stores / acquire
@@ -744,7 +767,7 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (warp == kCons / 32 + 1) {  // producer
     if (lane == 0) {
-      const uint32_t wbytes = N4 * wpitch * 8, xbytes = chunk * 2;
+      const uint32_t wbytes = N4 * wpitch * 8, xbytes = chunk * kXB;
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % kStages;
         if (c >= kStages)  // sleep-poll until every chain warp has finished chunk c - kStages
@@ -761,15 +784,14 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % kStages;
       mbar_wait(&full[s], (c / kStages) & 1);
-      const __nv_bfloat16* rx = rawx + (size_t)s * tpc * chunk;
+      const XT* rx = rawx + (size_t)s * tpc * chunk;
       double* xo = xd + (size_t)s * tpc * chunk;
-      for (int i = lane * 8; i < ntok * chunk; i += 32 * 8) {
-        const int4 raw = *reinterpret_cast<const int4*>(rx + i);
-        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+      constexpr int kV = 16 / kXB;  // values per 16-byte load
+      for (int i = lane * kV; i < ntok * chunk; i += 32 * kV) {
+        double v[kV];
+        widen16<XT>(*reinterpret_cast<const int4*>(rx + i), v);
 #pragma unroll
-        for (int j = 0; j < 8; j += 2)
-          *reinterpret_cast<double2*>(xo + i + j) = make_double2(static_cast<double>(__bfloat162float(hv[j])),
-                                                                 static_cast<double>(__bfloat162float(hv[j + 1])));
+        for (int j = 0; j < kV; j += 2) *reinterpret_cast<double2*>(xo + i + j) = make_double2(v[j], v[j + 1]);
       }
       __syncwarp();
       if (lane == 0) st_release_cta(&xflag[s], c + 1);  // publishes the widened x and, by cumulativity,
@@ -862,11 +884,11 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const __nv_bfl
 struct RouterBigSmem {
   int tpc, N4;
   size_t rx, sw, slog, sidx, slse, total;
-  __host__ __device__ RouterBigSmem(int n_experts, int threads, int stages, int tok = 4) {
+  __host__ __device__ RouterBigSmem(int n_experts, int threads, int stages, int tok = 4, int xb = 2) {
     N4 = (n_experts + 3) / 4 * 4;
     tpc = (threads / (N4 / 4)) * tok;
     rx = 0;
-    sw = rx + (size_t)stages * tpc * kRouterChunk * 2;
+    sw = rx + (size_t)stages * tpc * kRouterChunk * xb;
     slog = sw + (size_t)stages * sizeof(double) * kRouterChunk * N4;
     sidx = slog + sizeof(float) * tpc * N4;
     slse = (sidx + sizeof(int) * tpc * 8 + 7) / 8 * 8;
@@ -874,11 +896,13 @@ struct RouterBigSmem {
   }
 };
 
-template <int kThreads, int kStages, int kTok = 4>
-__global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bfloat16* __restrict__ x,
+template <int kThreads, int kStages, int kTok = 4, typename XT = __nv_bfloat16>
+__global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const XT* __restrict__ x,
                                                                  const double* __restrict__ wr64, int T, int d, int N,
                                                                  int K, RouteBufs rb) {
-  const RouterBigSmem L(N, kThreads, kStages, kTok);
+  // kXB = 2: a token's 64-column chunk is 8 x 16 B; fp32 x: 16 x 16 B, swizzled in 32-byte pairs
+  constexpr int kXB = sizeof(XT), kRowB = kRouterChunk * kXB, kP = kXB / 2;  // 16-byte pieces per 8 values
+  const RouterBigSmem L(N, kThreads, kStages, kTok, kXB);
   const int N4 = L.N4;
   const int groups = N4 / 4;
   const int tg_per_cta = kThreads / groups;
@@ -886,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
   const int tile = blockIdx.x;
   const int tok0 = tile * tpc;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* rawx = smem_raw + L.rx;                               // [stages][tpc][128 B] swizzled
+  uint8_t* rawx = smem_raw + L.rx;                               // [stages][tpc][kRowB] swizzled
   double* sw = reinterpret_cast<double*>(smem_raw + L.sw);       // [stages][chunk][N4]
   float* slog = reinterpret_cast<float*>(smem_raw + L.slog);
   int* sidx = reinterpret_cast<int*>(smem_raw + L.sidx);
@@ -901,16 +925,16 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
   const int nchunks = d / kRouterChunk;
-  const int xpieces = tpc * 8;  // 8 x 16-byte chunks per token row per stage
+  const int xpieces = tpc * 8 * kP;  // 16-byte pieces per token row per stage
   const int wpieces = kRouterChunk * N4 / 2;
   auto issue = [&](int c, int buf) {
     const int c0 = c * kRouterChunk;
     for (int i = threadIdx.x; i < xpieces; i += kThreads) {
-      const int r = i >> 3, q = i & 7;
+      const int r = i / (8 * kP), p = i % (8 * kP), q = p / kP, h = p % kP;  // 8-value group q, half h
       const bool ok = tok0 + r < T;
-      const __nv_bfloat16* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8;
+      const XT* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8 + h * (16 / kXB);
       const int qs = q ^ ((r / kTok) & 7);
-      cp_async16(rawx + ((size_t)buf * tpc + r) * 128 + qs * 16, src, ok);
+      cp_async16(rawx + ((size_t)buf * tpc + r) * kRowB + (qs * kP + h) * 16, src, ok);
     }
     const double* wsrc = wr64 + (size_t)c0 * N4;
     for (int i = threadIdx.x; i < wpieces; i += kThreads)
@@ -928,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
     if (c + kStages - 1 < nchunks) issue(c + kStages - 1, (c + kStages - 1) % kStages);
     else cp_async_commit();
     if (worker) {
-      const uint8_t* xb = rawx + (size_t)buf * tpc * 128;
+      const uint8_t* xb = rawx + (size_t)buf * tpc * kRowB;
       const double2* wv = reinterpret_cast<const double2*>(sw + (size_t)buf * kRouterChunk * N4 + g * 4);
 #pragma unroll 1
       for (int q = 0; q < kRouterChunk / 8; ++q) {
@@ -937,10 +961,9 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const __nv_bflo
 #pragma unroll
         for (int a = 0; a < kTok; ++a) {
           const int r = tg * kTok + a;
-          const int4 raw = *reinterpret_cast<const int4*>(xb + (size_t)r * 128 + ((q ^ ((r / kTok) & 7)) * 16));
-          const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+          const uint8_t* g8 = xb + (size_t)r * kRowB + (q ^ ((r / kTok) & 7)) * kP * 16;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) xd[a][i] = static_cast<double>(__bfloat162float(hv[i]));
+          for (int h = 0; h < kP; ++h) widen16<XT>(*reinterpret_cast<const int4*>(g8 + h * 16), &xd[a][h * (16 / kXB)]);
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {

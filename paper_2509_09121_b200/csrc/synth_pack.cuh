@@ -92,17 +92,23 @@ __global__ void pack_transpose_kernel(const float* __restrict__ src, int rows, i
 
 // Per-output-channel FP8 weight quantisation: scale = absmax/448 over the
 // packed row (a K-major row is one output channel), q = e4m3_satfinite(w / scale). One warp/row.
+// given = true: the scales are inputs (a loaded scheme file), not recomputed.
 __global__ void quantize_rows_e4m3_kernel(const __nv_bfloat16* __restrict__ w, int64_t rows, int kdim,
-                                          uint8_t* __restrict__ q, float* __restrict__ scale) {
+                                          uint8_t* __restrict__ q, float* __restrict__ scale, bool given = false) {
   const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
   const __nv_bfloat16* src = w + r * kdim;
-  float m = 0.0f;
-  for (int i = lane; i < kdim; i += 32) m = fmaxf(m, fabsf(__bfloat162float(src[i])));
-  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  const float s = m > 0.0f ? __fdiv_rn(m, 448.0f) : 1.0f;
-  if (lane == 0) scale[r] = s;
+  float s;
+  if (given) {
+    s = scale[r];
+  } else {
+    float m = 0.0f;
+    for (int i = lane; i < kdim; i += 32) m = fmaxf(m, fabsf(__bfloat162float(src[i])));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    s = m > 0.0f ? __fdiv_rn(m, 448.0f) : 1.0f;
+    if (lane == 0) scale[r] = s;
+  }
   uint8_t* dst = q + r * kdim;
   for (int i = lane; i < kdim; i += 32)
     dst[i] = static_cast<uint8_t>(__nv_cvt_float_to_fp8(__fdiv_rn(__bfloat162float(src[i]), s), __NV_SATFINITE, __NV_E4M3));
@@ -165,6 +171,60 @@ __global__ void scale_cols_bf16_kernel(__nv_bfloat16* __restrict__ m, int64_t n,
 __global__ void scale_rows_f32_kernel(float* __restrict__ m, int rows, int cols, const float* __restrict__ s) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < rows * cols) m[i] = m[i] * s[i / cols];
+}
+
+// E4M3 quantize-dequantize of one value (SPEC.md:523-531 fp8_qdq): q = RNE_satfinite(x / s) on the
+// E4M3 grid, x_hat = q * s in fp32 (the same float operations as the oracle's orc_fp8_qdq).
+__device__ __forceinline__ float qdq_e4m3(float x, float s) {
+  const __nv_fp8_storage_t q = __nv_cvt_float_to_fp8(__fdiv_rn(x, s), __NV_SATFINITE, __NV_E4M3);
+  const __half_raw hr = __nv_cvt_fp8_to_halfraw(q, __NV_E4M3);
+  return __fmul_rn(__half2float(__half(hr)), s);
+}
+
+// Router under the FP8 scheme ("all expert/router ... projection GEMMs run through
+// fp8_qdq on weights (per-output-channel scale = channel absmax/448)"): the router's output
+// channels are the N expert columns of W_r [d][N]. ws[c] = absmax/448 (1 for an all-zero column,
+// as the expert weights), wq = qdq(W_r, ws[c]) in fp32 — the values the router's fp64 chains
+// consume. One thread per column, once per quantize.
+__global__ void router_qdq_w_kernel(const float* __restrict__ wr, int d, int N, float* __restrict__ wq,
+                                    float* __restrict__ ws, bool given = false) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float s;
+  if (given) {
+    s = ws[c];
+  } else {
+    float m = 0.0f;
+    for (int l = 0; l < d; ++l) m = fmaxf(m, fabsf(wr[(size_t)l * N + c]));
+    s = m > 0.0f ? __fdiv_rn(m, 448.0f) : 1.0f;
+    ws[c] = s;
+  }
+  for (int l = 0; l < d; ++l) wq[(size_t)l * N + c] = qdq_e4m3(wr[(size_t)l * N + c], s);
+}
+
+// The router's activation operand under the FP8 scheme: x_hat = qdq(x, s_x) with the per-tensor
+// calibration scale s_x (device scalar), written as fp32 for the fp32-input router. 8 values per
+// thread per step (16-byte bf16 / 2 x 16-byte fp32 loads, 2 x 16-byte stores).
+template <typename XT>
+__global__ void router_qdq_x_kernel(const XT* __restrict__ x, int64_t n, const float* __restrict__ sx,
+                                    float* __restrict__ out) {
+  const float s = *sx;
+  const int64_t n8 = n / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    if constexpr (sizeof(XT) == 2) {
+      const int4 raw = *reinterpret_cast<const int4*>(x + i * 8);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(h[j]);
+    } else {
+      const float4 a = reinterpret_cast<const float4*>(x)[2 * i], b = reinterpret_cast<const float4*>(x)[2 * i + 1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+    float4* o = reinterpret_cast<float4*>(out + i * 8);
+    o[0] = make_float4(qdq_e4m3(v[0], s), qdq_e4m3(v[1], s), qdq_e4m3(v[2], s), qdq_e4m3(v[3], s));
+    o[1] = make_float4(qdq_e4m3(v[4], s), qdq_e4m3(v[5], s), qdq_e4m3(v[6], s), qdq_e4m3(v[7], s));
+  }
 }
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ in, int64_t n, __nv_bfloat16* __restrict__ out) {

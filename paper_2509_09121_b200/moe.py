@@ -102,21 +102,16 @@ class MoELayer:
 
     # ---------------------------------------------------------------- SPEC ops
     def route_tokens(self, hidden: torch.Tensor) -> RouterDecision:
+        """bf16 hidden, or fp32 hidden (the reference's Tensor dtype): fp32 is routed on its own
+        values, bit-exact with the reference's route_tokens on the same tensor."""
         t = hidden.shape[0]
-        n, k = self.cfg.n_experts, self.cfg.top_k
-        dev = self.device
-        dec = RouterDecision(
-            logits=torch.empty(t, n, dtype=torch.float32, device=dev),
-            probs=torch.empty(t, n, dtype=torch.float32, device=dev),
-            topk_idx=torch.empty(t, k, dtype=torch.int32, device=dev),
-            combine_weights=torch.empty(t, k, dtype=torch.float32, device=dev),
-            counts=torch.empty(n, dtype=torch.int64, device=dev),
-            agg_prob=torch.empty(n, dtype=torch.float32, device=dev),
-            aux=torch.empty(1, dtype=torch.float32, device=dev),
-            z=torch.empty(1, dtype=torch.float32, device=dev), B=t, K=k)
+        dec = self._new_decision(t)
         cd = self._decision_struct(dec)
-        self._check(self.L.cl_moe_route_tokens(self.h, _ptr(self._bf16(hidden)), t, C.byref(cd), _stream(dev)),
-                    "route_tokens")
+        if hidden.dtype == torch.float32:
+            rc = self.L.cl_moe_route_tokens_f32(self.h, _ptr(self._f32(hidden)), t, C.byref(cd), _stream(self.device))
+        else:
+            rc = self.L.cl_moe_route_tokens(self.h, _ptr(self._bf16(hidden)), t, C.byref(cd), _stream(self.device))
+        self._check(rc, "route_tokens")
         return dec
 
     def moe_forward(self, hidden: torch.Tensor, decision: RouterDecision) -> torch.Tensor:
@@ -129,25 +124,18 @@ class MoELayer:
         return out
 
     def forward(self, hidden: torch.Tensor, want_decision: bool = False):
-        """route_tokens + moe_forward fused on device. Returns out (and the decision)."""
-        hidden = self._bf16(hidden)
+        """route_tokens + moe_forward fused on device. Returns out (and the decision).
+        fp32 hidden: routed on the fp32 values, experts on their bf16 rounding, fp32 out."""
+        f32 = hidden.dtype == torch.float32
+        hidden = self._f32(hidden) if f32 else self._bf16(hidden)
         out = torch.empty_like(hidden)
         dec = None
         cd = None
         if want_decision:
-            t, n, k, dev = hidden.shape[0], self.cfg.n_experts, self.cfg.top_k, self.device
-            dec = RouterDecision(
-                logits=torch.empty(t, n, dtype=torch.float32, device=dev),
-                probs=torch.empty(t, n, dtype=torch.float32, device=dev),
-                topk_idx=torch.empty(t, k, dtype=torch.int32, device=dev),
-                combine_weights=torch.empty(t, k, dtype=torch.float32, device=dev),
-                counts=torch.empty(n, dtype=torch.int64, device=dev),
-                agg_prob=torch.empty(n, dtype=torch.float32, device=dev),
-                aux=torch.empty(1, dtype=torch.float32, device=dev),
-                z=torch.empty(1, dtype=torch.float32, device=dev), B=t, K=k)
+            dec = self._new_decision(hidden.shape[0])
             cd = C.byref(self._decision_struct(dec))
-        self._check(self.L.cl_moe_forward(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), cd, _stream(self.device)),
-                    "forward")
+        fn = self.L.cl_moe_forward_f32 if f32 else self.L.cl_moe_forward
+        self._check(fn(self.h, _ptr(hidden), hidden.shape[0], _ptr(out), cd, _stream(self.device)), "forward")
         return (out, dec) if want_decision else out
 
     def forward_graph(self, hidden: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -202,7 +190,11 @@ class MoELayer:
         self._check(self.L.cl_moe_calibrate(self.h, _ptr(self._bf16(hidden)), hidden.shape[0], int(reset),
                                             _stream(self.device)), "calibrate")
 
-    def quantize_fp8(self, act_scale_in=None, act_scale_mid=None):
+    def quantize_fp8(self, act_scale_in=None, act_scale_mid=None, router_act_scale=None):
+        """quantize_model. Explicit scales: act_scale_in [N], act_scale_mid
+        [N_local], router_act_scale (the router's per-tensor activation scale; else calibration)."""
+        if router_act_scale is not None:
+            self.set_router_fp8(True, router_act_scale)
         if act_scale_in is None:
             rc = self.L.cl_moe_quantize_fp8(self.h, None, None)
         else:
@@ -212,6 +204,27 @@ class MoELayer:
                 raise MoEConfigError("act_scale_in needs n_experts entries, act_scale_mid n_experts/ep_size")
             rc = self.L.cl_moe_quantize_fp8(self.h, a.ctypes.data, b.ctypes.data)
         self._check(rc, "quantize_fp8")
+
+    def set_router_fp8(self, enable: bool = True, act_scale: float = 0.0):
+        """Router GEMM through fp8_qdq in FP8 mode (default) or fp32 gating (False).
+        act_scale > 0 fixes the router's activation scale (else: calibration max / 448)."""
+        self._check(self.L.cl_moe_set_router_fp8(self.h, int(enable), float(act_scale)), "set_router_fp8")
+
+    def save_fp8_scheme(self, path: str) -> None:
+        """QuantScheme file: JSON manifest at `path`, fp32 scale arrays in `path`.bin."""
+        self._check(self.L.cl_moe_save_fp8_scheme(self.h, path.encode()), "save_fp8_scheme")
+
+    def load_fp8_scheme(self, path: str) -> None:
+        """Applies a saved scheme (fold, scales, weight quantization) and switches to FP8."""
+        self._check(self.L.cl_moe_load_fp8_scheme(self.h, path.encode()), "load_fp8_scheme")
+
+    def router_fp8_scales(self):
+        """(enabled, activation scale, weight scales [N]) of the router under the FP8 scheme."""
+        en = C.c_int32()
+        a = C.c_float()
+        w = np.empty(self.cfg.n_experts, np.float32)
+        self._check(self.L.cl_moe_get_router_fp8(self.h, C.byref(en), C.byref(a), w.ctypes.data), "router_fp8_scales")
+        return bool(en.value), a.value, w
 
     def calibration_stats(self):
         """collect_calibration statistics: dict(counts [N], x_max [N_local], mid_max [N_local], ch_max [d])."""
@@ -378,6 +391,13 @@ class MoELayer:
     def _bf16(self, x: torch.Tensor) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or not x.is_cuda or not x.is_contiguous():
             raise MoEConfigError("hidden must be a contiguous bf16 CUDA tensor [B x d]")
+        if x.shape[1] != self.cfg.d_model:
+            raise MoEConfigError(f"hidden has {x.shape[1]} columns, expected d_model={self.cfg.d_model}")
+        return x
+
+    def _f32(self, x: torch.Tensor) -> torch.Tensor:
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise MoEConfigError("hidden must be a contiguous fp32 CUDA tensor [B x d]")
         if x.shape[1] != self.cfg.d_model:
             raise MoEConfigError(f"hidden has {x.shape[1]} columns, expected d_model={self.cfg.d_model}")
         return x

@@ -9,8 +9,10 @@ from oracle.oracle import Oracle, make_inputs
 from paper_2509_09121_b200.moe import MoEConfig, MoELayer
 
 
-def main(t, d, n, k, mode="random"):
-    inp = make_inputs(t, d, n, 128, experts=False)
+def main(t, d, n, k, mode="random", dtype="bf16"):
+    # dtype "f32": unrounded fp32 tokens routed through the fp32 entry (cl_moe_route_tokens_f32)
+    f32 = dtype == "f32"
+    inp = make_inputs(t, d, n, 128, experts=False, bf16=not f32)
     if mode == "ties":
         # exact ties: odd router columns duplicate the even ones (equal logits -> equal probs, the
         # lowest index must win), every 7th token is all-zero (uniform probs -> experts 0..K-1),
@@ -21,7 +23,8 @@ def main(t, d, n, k, mode="random"):
         inp["x"][::7] = 0.0
     lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=128, max_tokens=t), inp["w_router"],
                    np.zeros((n, d, 256), np.float32), np.zeros((n, 128, d), np.float32))
-    dec = lay.route_tokens(torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16))
+    xd = torch.from_numpy(inp["x"]).cuda()
+    dec = lay.route_tokens(xd.contiguous() if f32 else xd.to(torch.bfloat16))
     lay.sync()
     ref = Oracle("port").route(inp["x"], inp["w_router"], k)
     ok = (np.array_equal(dec.logits.cpu().numpy(), ref["logits"]) and
@@ -32,4 +35,4 @@ def main(t, d, n, k, mode="random"):
 
 
 if __name__ == "__main__":
-    sys.exit(main(*map(int, sys.argv[1:5]), *sys.argv[5:6]))
+    sys.exit(main(*map(int, sys.argv[1:5]), *sys.argv[5:7]))

@@ -123,11 +123,12 @@ def test_group_forward_fp8_bit_identical_to_single_gpu(R, n, k, ts):
     full.calibrate(xall)
     full.quantize_fp8()
     s_in, s_mid, _, _ = full.fp8_scales()
+    s_r = full.router_fp8_scales()[1]  # every rank routes with the same router activation scale
     ranks = []
     for r in range(R):
         lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=cap, ep_size=R, ep_rank=r),
                        inp["w_router"], inp["w_in"][r * nl:(r + 1) * nl], inp["w_out"][r * nl:(r + 1) * nl])
-        lay.quantize_fp8(s_in, s_mid[r * nl:(r + 1) * nl])
+        lay.quantize_fp8(s_in, s_mid[r * nl:(r + 1) * nl], router_act_scale=s_r)
         ranks.append(lay)
     xs, a = [], 0
     for t in ts:

@@ -3,7 +3,10 @@
 Tolerances (declared): output vs the qdq-simulated fp32/fp64 oracle
 ||d||_F/||y||_F <= 2e-2; vs the unquantised oracle <= 8e-2 (reported, checked loosely).
 Scales: per-expert activation scale = calibration max / 448 (exact vs the oracle routing for the
-GEMM1 input), per-(expert, output channel) weight scale = channel absmax / 448 (exact)."""
+GEMM1 input), per-(expert, output channel) weight scale = channel absmax / 448 (exact).
+Router (the router GEMM through fp8_qdq too): activation scale = calibration max
+|hidden| / 448, per-expert-column W_r scale = absmax / 448 (exact); the FP8 layer's decision is
+bit-exact against the oracle's route on qdq(x) and qdq(W_r) (router_fp8_sim)."""
 import os
 
 import numpy as np
@@ -12,7 +15,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
-from oracle.oracle import Oracle, make_inputs, moe_forward_fp8_sim  # noqa: E402
+from oracle.oracle import Oracle, make_inputs, moe_forward_fp8_sim, router_fp8_sim  # noqa: E402
 
 JOBS = os.cpu_count() or 1
 
@@ -40,20 +43,40 @@ def test_fp8_layer_vs_qdq_oracle(gemm_ctas):
         rows = np.nonzero((r["topk_idx"] == e).any(1))[0]
         if len(rows):
             assert s_in[e] == np.float32(np.abs(inp["x"][rows]).max()) / np.float32(448)
+    # router scales: activation max|x| / 448 (per tensor), W_r columns absmax / 448
+    en, s_r, ws_r = lay.router_fp8_scales()
+    assert en and s_r == np.float32(np.abs(inp["x"]).max()) / np.float32(448)
+    rq, ws_r_ref = router_fp8_sim(o, inp["x"], inp["w_router"], k, s_r)
+    assert np.array_equal(ws_r, ws_r_ref)
+    assert not np.array_equal(rq["topk_idx"], r["topk_idx"])  # the quantized router decides differently
     # weight scales: packed row p of expert e is reference column c(p)
-    ref_out, ws_in_ref, ws_out_ref = moe_forward_fp8_sim(o, inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"],
-                                                         r["combine_weights"], s_in, s_mid)
+    ref_out, ws_in_ref, ws_out_ref = moe_forward_fp8_sim(o, inp["x"], inp["w_in"], inp["w_out"], rq["topk_idx"],
+                                                         rq["combine_weights"], s_in, s_mid)
     cols = np.array([_win_col_of_packed_row(p, f) for p in range(2 * f)])
     assert np.array_equal(ws_in_p, ws_in_ref[:, cols])
     assert np.array_equal(ws_out, ws_out_ref)
-    out = lay.forward(x)
+    out, dec = lay.forward(x, want_decision=True)
     lay.sync()
+    assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"])
+    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"])
+    assert np.array_equal(dec.counts.cpu().numpy(), rq["counts"])
     o32 = out.float().cpu().numpy().astype(np.float64)
     rel = np.linalg.norm(o32 - ref_out) / np.linalg.norm(ref_out)
     assert rel <= 2e-2, rel
     full = o.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"], jobs=JOBS)
     rel_full = np.linalg.norm(o32 - full) / np.linalg.norm(full)
-    assert rel_full <= 8e-2, rel_full
+    assert rel_full <= 3e-1, rel_full  # reported: ~7 % of the tokens take another expert under the quantized router
+    # fp32 gating kept as an option: the decision is the unquantized router's again
+    lay.set_router_fp8(False)
+    out_g, dec_g = lay.forward(x, want_decision=True)
+    lay.sync()
+    assert np.array_equal(dec_g.topk_idx.cpu().numpy().astype(np.int64), r["topk_idx"])
+    ref_g, _, _ = moe_forward_fp8_sim(o, inp["x"], inp["w_in"], inp["w_out"], r["topk_idx"], r["combine_weights"],
+                                      s_in, s_mid)
+    og = out_g.float().cpu().numpy().astype(np.float64)
+    assert np.linalg.norm(og - ref_g) / np.linalg.norm(ref_g) <= 2e-2
+    assert np.linalg.norm(og - full) / np.linalg.norm(full) <= 8e-2
+    lay.set_router_fp8(True)
     # dispatched e4m3 bytes equal the oracle's encoding of x / s_in[e]
     xp = lay.stage("x_perm", (t * k, d // 2), torch.bfloat16).view(torch.uint8).cpu().numpy().reshape(t * k, d)
     offsets = lay.stage("offsets", (n + 1,), torch.int32).cpu().numpy()
@@ -82,7 +105,9 @@ def test_fp8_requires_calibration():
         lay.set_precision("fp8")
     with pytest.raises(MoEError):
         lay.quantize_fp8()  # no calibration -> "missing calibration for expert"
-    lay.quantize_fp8(np.full(4, 0.01, np.float32), np.full(4, 0.01, np.float32))
+    with pytest.raises(MoEError, match="router"):
+        lay.quantize_fp8(np.full(4, 0.01, np.float32), np.full(4, 0.01, np.float32))  # router scale missing
+    lay.quantize_fp8(np.full(4, 0.01, np.float32), np.full(4, 0.01, np.float32), router_act_scale=0.01)
     x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
     out = lay.forward(x)
     lay.sync()
@@ -125,9 +150,11 @@ def test_smoothing_compute_fold_then_expert_aware_fp8():
     lay.calibrate(xd)
     lay.quantize_fp8()
     s_in, s_mid, _, _ = lay.fp8_scales()
-    outq = lay.forward(xd)
+    outq, decq = lay.forward(xd, want_decision=True)
     lay.sync()
-    refq, _, _ = moe_forward_fp8_sim(o, xs, wi_f, inp["w_out"], r["topk_idx"], r["combine_weights"], s_in, s_mid)
+    rq, _ = router_fp8_sim(o, xs, wr_f, k, lay.router_fp8_scales()[1])
+    assert np.array_equal(decq.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"])
+    refq, _, _ = moe_forward_fp8_sim(o, xs, wi_f, inp["w_out"], rq["topk_idx"], rq["combine_weights"], s_in, s_mid)
     q32 = outq.float().cpu().numpy().astype(np.float64)
     assert np.linalg.norm(q32 - refq) / np.linalg.norm(refq) <= 2e-2
     lay.close()

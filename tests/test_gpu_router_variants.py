@@ -1,7 +1,9 @@
 """Every K1 router variant (ws and lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4), forced through
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
 including ragged last tiles, shapes where the automatic choice would pick another variant, and exact
-ties (duplicated router columns, all-zero tokens: the lowest expert index must win)."""
+ties (duplicated router columns, all-zero tokens: the lowest expert index must win). Each case runs
+twice: bf16 tokens, and unrounded fp32 tokens through the fp32 router input (the "lat" variant is
+bf16-only; forced with fp32 input it runs ws)."""
 import os
 import subprocess
 import sys
@@ -18,10 +20,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                           (257, 256, 32, 4, "random"), (70, 1024, 4, 1, "random"),
                                           (5, 256, 128, 8, "random"), (300, 256, 16, 4, "ties"),
                                           (90, 256, 128, 8, "ties"), (2400, 256, 4, 2, "random")])
-def test_router_variant_bit_exact(variant, t, d, n, k, mode):
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_router_variant_bit_exact(variant, t, d, n, k, mode, dtype):
     env = dict(os.environ, CL_MOE_ROUTER=variant.rstrip("24"), PYTHONPATH=ROOT)
     if variant.startswith("big"):
         env["CL_MOE_BIG_TOK"] = variant[-1]  # 2 or 4 tokens x 4 experts per thread
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "helpers", "route_check.py"), str(t), str(d), str(n),
-                        str(k), mode], env=env, capture_output=True, text=True, timeout=300, cwd=ROOT)
+                        str(k), mode, dtype], env=env, capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
