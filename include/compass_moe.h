@@ -33,12 +33,21 @@
 #include <stddef.h>
 #include <stdint.h>
 
+/* cl_status is the reference's (compass_lab.h:23-27). When the reference header is on the include
+ * path, include it here so that either include order works (compass_lab.h defines cl_status
+ * unguarded); otherwise define the identical enum. */
+#if defined(__has_include)
+#if __has_include("compass_lab.h")
+#include "compass_lab.h"
+#endif
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
 
+/* otherwise: identical to compass_lab.h:23-27 */
 #ifndef COMPASS_LAB_H
-/* Identical to compass_lab.h:23-27 so both headers can be included together. */
 typedef enum cl_status {
   CL_OK = 0,        /* success */
   CL_ERR_RUN = 1,   /* validation or runtime failure */
@@ -107,6 +116,11 @@ cl_status cl_moe_create_from_checkpoint(const cl_moe_config* cfg, const char* pa
 /* Writes the layer's weights (as stored: bf16-valued fp32) in the same format and naming; the
  * file round-trips byte-exactly through the reference's load_checkpoint / save_checkpoint. */
 cl_status cl_moe_save_checkpoint(cl_moe* h, const char* path, const char* prefix);
+
+/* HOST copies of the weights the layer holds, in the reference layouts (as stored: bf16-valued
+ * fp32 for the experts): w_router [d x N], and local expert `expert`'s w_in [d x 2f] / w_out [f x d].
+ * Any pointer may be NULL. Synchronous. */
+cl_status cl_moe_get_weights(cl_moe* h, float* w_router, int64_t expert, float* w_in, float* w_out);
 
 /* Creates a layer whose weights are generated on the device from the reference counter PRNG
  * (proj/include/compasslab/prng.hpp) exactly as SURVEY.md §8(d) prescribes (root seed `seed`). */
@@ -178,7 +192,11 @@ cl_status cl_moe_host_wait(cl_moe* h);
  * output (the reference's check_finite, proj/src/tensor.cpp:35-41) -> CL_ERR_RUN. */
 cl_status cl_moe_sync(cl_moe* h, void* stream);
 
-/* Stage buffers of the last call (valid until the next call on the handle). */
+/* Stage buffers of the last call (valid until the next call on the handle). After a dense-decode
+ * forward (single GPU, T <= 128) they are the dense buffers: rows = N*T, row e*T + t = token t for
+ * expert e (offsets[e] = e*T), row_weight = the combine weight of (t, e) or 0 when e is not among
+ * t's top-K, inv[t*K + k] = the row of token t's k-th expert; perm = NULL (copy_stage(1) ->
+ * CL_ERR_RUN): no permutation is materialised. */
 cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* view);
 
 /* Copies stage buffer `which` (0 offsets, 1 perm, 2 inv, 3 row_weight, 4 x_perm, 5 act, 6 y)

@@ -331,6 +331,54 @@ cl_status cl_moe_create_from_checkpoint(const cl_moe_config* cfg, const char* pa
   }
 }
 
+// Local expert e's weights in the reference layouts (W_in [d][2f], W_out [f][d], fp32 host; either
+// may be null): packed bf16 -> reference order on the device (tmp: d*2f bf16), widened on the host.
+static void unpack_expert(cl_moe* h, int64_t e, __nv_bfloat16* tmp, std::vector<uint16_t>& hb, float* w_in,
+                          float* w_out) {
+  const int64_t d = h->d, f = h->f;
+  auto widen = [&](float* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+      const uint32_t u = static_cast<uint32_t>(hb[i]) << 16;
+      std::memcpy(dst + i, &u, 4);
+    }
+  };
+  hb.resize((size_t)d * 2 * f);
+  if (w_in) {
+    transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
+        h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, tmp);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * d * 2 * f, cudaMemcpyDeviceToHost));
+    widen(w_in, (size_t)d * 2 * f);
+  }
+  if (w_out) {
+    transpose_weight_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)(f / 32)), 256>>>(
+        h->wout + (size_t)e * d * f, (int)d, (int)f, (int)f, tmp);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * f * d, cudaMemcpyDeviceToHost));
+    widen(w_out, (size_t)f * d);
+  }
+}
+
+cl_status cl_moe_get_weights(cl_moe* h, float* w_router, int64_t expert, float* w_in, float* w_out) {
+  return guarded(h, [&] {
+    if ((w_in || w_out) && (expert < 0 || expert >= h->n_local)) throw ConfigErr("expert out of range");
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaDeviceSynchronize());
+    if (w_router) CK(cudaMemcpy(w_router, h->wr, sizeof(float) * h->d * h->N, cudaMemcpyDeviceToHost));
+    if (w_in || w_out) {
+      __nv_bfloat16* tmp = dalloc<__nv_bfloat16>((size_t)h->d * 2 * h->f);
+      std::vector<uint16_t> hb;
+      try {
+        unpack_expert(h, expert, tmp, hb, w_in, w_out);
+      } catch (...) {
+        cudaFree(tmp);
+        throw;
+      }
+      cudaFree(tmp);
+    }
+  });
+}
+
 cl_status cl_moe_save_checkpoint(cl_moe* h, const char* path, const char* prefix) {
   return guarded(h, [&] {
     if (!path) throw ConfigErr("path is null");
@@ -342,25 +390,8 @@ cl_status cl_moe_save_checkpoint(cl_moe* h, const char* path, const char* prefix
     CK(cudaMemcpy(wr.data(), h->wr, sizeof(float) * d * N, cudaMemcpyDeviceToHost));
     // packed bf16 -> reference layouts on device, then widen on the host
     __nv_bfloat16* tmp = dalloc<__nv_bfloat16>((size_t)d * 2 * f);
-    std::vector<uint16_t> hb((size_t)d * 2 * f);
-    auto widen = [&](const std::vector<uint16_t>& src, float* dst, size_t n) {
-      for (size_t i = 0; i < n; ++i) {
-        const uint32_t u = static_cast<uint32_t>(src[i]) << 16;
-        std::memcpy(dst + i, &u, 4);
-      }
-    };
-    for (int64_t e = 0; e < NL; ++e) {
-      transpose_weight_kernel<true><<<dim3((unsigned)(2 * f / 32), (unsigned)(d / 32)), 256>>>(
-          h->win + (size_t)e * 2 * f * d, (int)(2 * f), (int)d, (int)f, tmp);
-      CK(cudaGetLastError());
-      CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * d * 2 * f, cudaMemcpyDeviceToHost));
-      widen(hb, win.data() + e * d * 2 * f, (size_t)d * 2 * f);
-      transpose_weight_kernel<false><<<dim3((unsigned)(d / 32), (unsigned)(f / 32)), 256>>>(
-          h->wout + (size_t)e * d * f, (int)d, (int)f, (int)f, tmp);
-      CK(cudaGetLastError());
-      CK(cudaMemcpy(hb.data(), tmp, sizeof(uint16_t) * f * d, cudaMemcpyDeviceToHost));
-      widen(hb, wout.data() + e * f * d, (size_t)f * d);
-    }
+    std::vector<uint16_t> hb;
+    for (int64_t e = 0; e < NL; ++e) unpack_expert(h, e, tmp, hb, win.data() + e * d * 2 * f, wout.data() + e * f * d);
     cudaFree(tmp);
     std::map<std::string, std::pair<std::vector<int64_t>, const float*>> ts;
     ts[pre + "router"] = {{d, N}, wr.data()};
@@ -741,13 +772,23 @@ cl_status cl_moe_sync(cl_moe* h, void* stream) {
 cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* v) {
   return guarded(h, [&] {
     if (!v) throw ConfigErr("view is null");
-    v->offsets = h->rb.offsets;
-    v->perm = h->perm;
-    v->inv = h->inv;
-    v->row_weight = h->row_w;
-    v->x_perm = h->xperm;
-    v->act = h->act;
-    v->y = h->y;
+    if (h->last_dense) {  // dense decode: every expert x every token, row e*T + t
+      v->offsets = h->offd;
+      v->perm = nullptr;  // no permutation is materialised
+      v->inv = h->invd;
+      v->row_weight = h->rwd;
+      v->x_perm = h->xd;
+      v->act = h->actd;
+      v->y = h->yd;
+    } else {
+      v->offsets = h->rb.offsets;
+      v->perm = h->perm;
+      v->inv = h->inv;
+      v->row_weight = h->row_w;
+      v->x_perm = h->xperm;
+      v->act = h->act;
+      v->y = h->y;
+    }
     v->rows = h->last_rows;
   });
 }
@@ -755,14 +796,18 @@ cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* v) {
 cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, void* stream) {
   return guarded(h, [&] {
     const void* src = nullptr;
+    const bool dn = h->last_dense;
     switch (which) {
-      case 0: src = h->rb.offsets; break;
-      case 1: src = h->perm; break;
-      case 2: src = h->inv; break;
-      case 3: src = h->row_w; break;
-      case 4: src = h->xperm; break;
-      case 5: src = h->act; break;
-      case 6: src = h->y; break;
+      case 0: src = dn ? (const void*)h->offd : h->rb.offsets; break;
+      case 1:
+        if (dn) throw RunErr("perm is not materialised by a dense-decode forward (CL_MOE_DENSE_DECODE=0 for the sparse path)");
+        src = h->perm;
+        break;
+      case 2: src = dn ? (const void*)h->invd : h->inv; break;
+      case 3: src = dn ? (const void*)h->rwd : h->row_w; break;
+      case 4: src = dn ? (const void*)h->xd : h->xperm; break;
+      case 5: src = dn ? (const void*)h->actd : h->act; break;
+      case 6: src = dn ? (const void*)h->yd : h->y; break;
       default: throw ConfigErr("unknown stage buffer");
     }
     if (!dst || bytes < 0) throw ConfigErr("bad destination");

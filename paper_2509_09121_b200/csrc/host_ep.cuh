@@ -147,6 +147,7 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
+  h->last_dense = false;
   if (train) {
     h->train_T = T;
     h->cur_x = x;
@@ -234,6 +235,7 @@ void ep_peer_combine(cl_moe* h, const void* x, int64_t T, void* out, bool out_f3
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
+  h->last_dense = false;
 }
 
 // Multi-process forward over NVLink peer memory. NCCL carries only the R x N counts and two

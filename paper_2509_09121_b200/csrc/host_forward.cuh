@@ -301,6 +301,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
+  h->last_dense = false;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -391,7 +392,8 @@ void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   CK(cudaGetLastError());
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
-  h->last_rows = T * h->K;
+  h->last_rows = N * T;  // dense layout: row e*T + t = token t for expert e
+  h->last_dense = true;
 }
 
 void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_t st) {

@@ -150,6 +150,7 @@ struct cl_moe {
   cudaStream_t cap_stream = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   int64_t last_rows = 0;
+  bool last_dense = false;  // the last forward took the dense-decode path (stage view = dense buffers)
   int tpc_cur = 32;                    // router tile (tokens) of the last routing call
   int64_t last_tokens = 0;             // T of the current call
 

@@ -84,6 +84,7 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   prof_mark(h, 5, st);
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
+  h->last_dense = false;
   h->train_T = T;
   h->cur_x = x;
 }

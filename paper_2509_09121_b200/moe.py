@@ -210,6 +210,20 @@ class MoELayer:
         act_scale > 0 fixes the router's activation scale (else: calibration max / 448)."""
         self._check(self.L.cl_moe_set_router_fp8(self.h, int(enable), float(act_scale)), "set_router_fp8")
 
+    def router_weights(self) -> np.ndarray:
+        """Host copy of W_r [d x N] (fp32) as the layer holds it."""
+        w = np.empty((self.cfg.d_model, self.cfg.n_experts), np.float32)
+        self._check(self.L.cl_moe_get_weights(self.h, w.ctypes.data, 0, None, None), "get_weights")
+        return w
+
+    def expert_weights(self, e: int):
+        """Host copies of local expert e's (W_in [d x 2f], W_out [f x d]) in the reference layouts."""
+        d, f = self.cfg.d_model, self.cfg.d_ff
+        wi = np.empty((d, 2 * f), np.float32)
+        wo = np.empty((f, d), np.float32)
+        self._check(self.L.cl_moe_get_weights(self.h, None, e, wi.ctypes.data, wo.ctypes.data), "get_weights")
+        return wi, wo
+
     def save_fp8_scheme(self, path: str) -> None:
         """QuantScheme file: JSON manifest at `path`, fp32 scale arrays in `path`.bin."""
         self._check(self.L.cl_moe_save_fp8_scheme(self.h, path.encode()), "save_fp8_scheme")

@@ -108,3 +108,40 @@ def test_dense_decode_stage_profile():
         assert ms[name] > 0.0, (name, ms)
     assert ms["plan"] >= 0.0  # the plan runs inside the router's last CTA here: may read ~0
     lay.close()
+
+
+def test_dense_decode_stage_view():
+    """After a dense-decode forward the stage buffers are the dense ones (rows = N*T, row e*T + t =
+    token t for expert e), not stale buffers of an earlier sparse call; perm is not materialised."""
+    from paper_2509_09121_b200.moe import MoEError
+    t, d, n, k, f = 64, 256, 8, 2, 256
+    inp = make_inputs(t, d, n, f)
+    lay = _layer(inp, t, k)
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    os.environ["CL_MOE_DENSE_DECODE"] = "0"
+    try:
+        lay.forward(x)  # a sparse call first: its buffers must not leak into the dense view
+        lay.sync()
+        ys = lay.stage("y", (t * k, d), torch.bfloat16).clone()
+        inv_s = lay.stage("inv", (t * k,), torch.int32).clone()
+    finally:
+        del os.environ["CL_MOE_DENSE_DECODE"]
+    _, dec = lay.forward(x, want_decision=True)
+    lay.sync()
+    idx = dec.topk_idx.cpu().numpy()
+    w = dec.combine_weights.cpu().numpy()
+    assert np.array_equal(lay.stage("offsets", (n + 1,), torch.int32).cpu().numpy(), np.arange(n + 1) * t)
+    inv = lay.stage("inv", (t * k,), torch.int32).cpu().numpy().reshape(t, k)
+    assert np.array_equal(inv, idx * t + np.arange(t)[:, None])
+    rw = lay.stage("row_weight", (n * t,), torch.float32).cpu().numpy().reshape(n, t)
+    want = np.zeros((n, t), np.float32)
+    for j in range(t):
+        for kk in range(k):
+            want[idx[j, kk], j] = w[j, kk]
+    assert np.array_equal(rw, want)
+    # the routed dense rows carry exactly the sparse path's weighted expert outputs
+    yd = lay.stage("y", (n * t, d), torch.bfloat16)
+    assert torch.equal(yd[torch.from_numpy(inv.reshape(-1)).long().cuda()], ys[inv_s.long()])
+    with pytest.raises(MoEError, match="perm"):
+        lay.stage("perm", (t * k,), torch.int32)
+    lay.close()
