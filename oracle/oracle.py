@@ -81,6 +81,11 @@ class Oracle:
                                               C.c_float, C.c_float, _f32p, _f32p]
         else:
             L.ref_gradcheck.argtypes = [C.c_uint64, C.c_int, C.c_double, C.POINTER(C.c_int)]
+            L.ref_prng_split.restype = C.c_uint64
+            L.ref_prng_split.argtypes = [C.c_uint64, C.c_uint64]
+            L.ref_prng_u64.argtypes = [C.c_uint64, C.c_uint64, _i64, np.ctypeslib.ndpointer(np.uint64)]
+            L.ref_prng_doubles.argtypes = [C.c_uint64, _i64, np.ctypeslib.ndpointer(np.float64)]
+            L.ref_prng_normals.argtypes = [C.c_uint64, _i64, C.c_float, C.c_float, _f32p]
             L.ref_ckpt_resave.argtypes = [C.c_char_p, C.c_char_p]
             L.ref_ckpt_write.argtypes = [C.c_char_p, C.c_char_p, _i64p, _f32p]
             L.ref_moe_backward_full.argtypes = [_f32p, _f32p, _i64, _i64, _i64, _i64, _i64, _f32p, _f32p, _f32p,
@@ -253,11 +258,27 @@ class Oracle:
         return out
 
     def split_seed(self, root: int, stream: int) -> int:
+        if self.kind == "reference":
+            return self.lib.ref_prng_split(root, stream)
         return self.lib.orc_split_seed(root, stream)
 
     def normals(self, seed: int, n: int, stddev: float, mean: float = 0.0):
         out = np.empty(n, np.float32)
-        self.lib.orc_normals(seed, n, mean, stddev, out)
+        if self.kind == "reference":
+            self.lib.ref_prng_normals(seed, n, mean, stddev, out)
+        else:
+            self.lib.orc_normals(seed, n, mean, stddev, out)
+        return out
+
+    # ---- the reference Prng itself (kind "reference" only) ----
+    def prng_u64(self, seed: int, n: int, counter: int = 0):
+        out = np.empty(n, np.uint64)
+        self.lib.ref_prng_u64(seed, counter, n, out)
+        return out
+
+    def prng_doubles(self, seed: int, n: int):
+        out = np.empty(n, np.float64)
+        self.lib.ref_prng_doubles(seed, n, out)
         return out
 
     def round_bf16(self, x):

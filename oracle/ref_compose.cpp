@@ -20,6 +20,7 @@
 #include "compasslab/checkpoint.hpp"
 #include "compasslab/common.hpp"
 #include "compasslab/gradcheck.hpp"
+#include "compasslab/prng.hpp"
 #include "compasslab/tensor.hpp"
 
 using compasslab::Tape;
@@ -49,6 +50,24 @@ int guarded(Fn fn) {
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
+
+// The reference's own counter PRNG (proj/include/compasslab/prng.hpp), exported so the oracle's
+// restatement (orc_split_seed / orc_normals) and its replay properties can be pinned to it.
+std::uint64_t ref_prng_split(std::uint64_t seed, std::uint64_t stream) {
+  return compasslab::Prng(seed).split(stream).seed();
+}
+void ref_prng_u64(std::uint64_t seed, std::uint64_t counter, std::int64_t n, std::uint64_t* out) {
+  compasslab::Prng p(seed, counter);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = p.next_u64();
+}
+void ref_prng_doubles(std::uint64_t seed, std::int64_t n, double* out) {
+  compasslab::Prng p(seed);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = p.next_double();
+}
+void ref_prng_normals(std::uint64_t seed, std::int64_t n, float mean, float stddev, float* out) {
+  compasslab::Prng p(seed);
+  for (std::int64_t i = 0; i < n; ++i) out[i] = p.next_normal_f(mean, stddev);
+}
 
 // route_tokens from ops::matmul, ops::softmax_rows, ops::top_k, ops::col_sums.
 int ref_route(const float* x, const float* wr, std::int64_t T, std::int64_t d, std::int64_t N,

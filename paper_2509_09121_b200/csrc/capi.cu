@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cmath>
 #include <cstdarg>
@@ -19,6 +20,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "compass_moe.h"
@@ -65,6 +67,7 @@ cl_status cl_moe_ep_init(cl_moe* h, const uint8_t* id) {
       h->comm = nullptr;
     }
     NCK(NcclApi::get().CommInitRank(&h->comm, R, uid, h->cfg.ep_rank));
+    h->ep_abort_reason.clear();
     ep_alloc(h);
   });
 }
@@ -90,7 +93,7 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     cudaStream_t st = nullptr;
     CK(cudaMemcpy(dbuf, mine.data(), kB * kH, cudaMemcpyHostToDevice));
     NCK(NcclApi::get().AllGather(dbuf, dbuf + kB * kH, kB * kH, NcclApi::kUint8, h->comm, st));
-    CK(cudaStreamSynchronize(st));
+    ep_wait(h, st, "peer-init handle exchange");
     CK(cudaMemcpy(all.data(), dbuf + kB * kH, kB * kH * R, cudaMemcpyDeviceToHost));
     cudaFree(dbuf);
     std::vector<void*> peer[kB];
@@ -120,7 +123,7 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     const float bad = why.empty() ? 0.f : 1.f;
     CK(cudaMemcpy(okf, &bad, sizeof(float), cudaMemcpyHostToDevice));
     NCK(NcclApi::get().AllReduce(okf, okf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
-    CK(cudaStreamSynchronize(st));
+    ep_wait(h, st, "peer-init vote");
     float nbad = 0.f;
     CK(cudaMemcpy(&nbad, okf, sizeof(float), cudaMemcpyDeviceToHost));
     cudaFree(okf);
@@ -729,8 +732,8 @@ static void host_enqueue(cl_moe* h, const void* hidden_host, int64_t T, void* ou
 
 static void host_wait(cl_moe* h) {
   CK(cudaSetDevice(h->cfg.device));
-  CK(cudaStreamSynchronize(h->s_d2h));
-  CK(cudaStreamSynchronize(h->own_stream));
+  ep_wait(h, h->s_d2h, "host-buffer forward");
+  ep_wait(h, h->own_stream, "host-buffer forward");
   int flag = 0;
   CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (flag) {
@@ -758,7 +761,7 @@ cl_status cl_moe_host_wait(cl_moe* h) {
 cl_status cl_moe_sync(cl_moe* h, void* stream) {
   return guarded(h, [&] {
     CK(cudaSetDevice(h->cfg.device));
-    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    ep_wait(h, (cudaStream_t)stream, "forward");  // bounded when a communicator exists
     int flag = 0;
     CK(cudaMemcpy(&flag, h->rb.finite_flag, sizeof(int), cudaMemcpyDeviceToHost));
     if (flag) {
@@ -978,7 +981,7 @@ cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float*
         cudaStream_t st = nullptr;
         NCK(NcclApi::get().AllReduce(h->calib_all, h->calib_all, (size_t)N, NcclApi::kFloat32, NcclApi::kMax, h->comm,
                                      st));
-        CK(cudaStreamSynchronize(st));
+        ep_wait(h, st, "calibration all-reduce");
         CK(cudaMemcpy(call.data(), h->calib_all, sizeof(float) * N, cudaMemcpyDeviceToHost));
       } else {
         std::copy(c.begin(), c.begin() + NL, call.begin());
@@ -1004,7 +1007,7 @@ cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float*
         cudaStream_t st = nullptr;
         NCK(NcclApi::get().AllReduce(h->calib_ch, h->calib_ch, (size_t)h->d, NcclApi::kFloat32, NcclApi::kMax, h->comm,
                                      st));
-        CK(cudaStreamSynchronize(st));
+        ep_wait(h, st, "router calibration all-reduce");
       }
       CK(cudaMemcpy(ch.data(), h->calib_ch, sizeof(float) * h->d, cudaMemcpyDeviceToHost));
       float m = 0.0f;

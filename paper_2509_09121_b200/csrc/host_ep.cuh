@@ -37,6 +37,70 @@ void ep_alloc(cl_moe* h) {
     if (r_ != 0) throw RunErr(fmt("%s failed: %s", #x, NcclApi::get().GetErrorString(r_))); \
   } while (0)
 
+// Bounded wait for `st` on an expert-parallel handle (the reference's error contract,
+// capi.cpp:57-63: a failure returns CL_ERR_RUN, it does not hang the caller). Polls the stream and
+// ncclCommGetAsyncError; on an NCCL async error, or when the stream has not drained within
+// CL_MOE_EP_TIMEOUT_S seconds (default 600; a peer rank died or stalled), the communicator is
+// aborted (ncclCommAbort) and the call fails with CL_ERR_RUN; every later expert-parallel call on
+// the handle fails the same way until cl_moe_ep_init creates a new communicator.
+double ep_timeout_s() {
+  static const double t = [] {
+    const char* e = std::getenv("CL_MOE_EP_TIMEOUT_S");
+    return e ? std::atof(e) : 600.0;
+  }();
+  return t;
+}
+
+void ep_abort(cl_moe* h, const std::string& why) {
+  if (h->comm) NcclApi::get().CommAbort(h->comm);
+  h->comm = nullptr;
+  h->ep_abort_reason = why;
+  throw RunErr(why);
+}
+
+void ep_wait(cl_moe* h, cudaStream_t st, const char* what) {
+  if (!h->comm) {
+    CK(cudaStreamSynchronize(st));
+    return;
+  }
+  NcclApi& nc = NcclApi::get();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spins = 0;; ++spins) {
+    const cudaError_t e = cudaStreamQuery(st);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) CK(e);
+    int aerr = 0;
+    const int qr = nc.CommGetAsyncError(h->comm, &aerr);
+    if (qr != 0 || aerr != 0)
+      ep_abort(h, fmt("expert-parallel %s: NCCL async error (%s); communicator aborted", what,
+                      nc.GetErrorString(qr != 0 ? qr : aerr)));
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (el > ep_timeout_s())
+      ep_abort(h, fmt("expert-parallel %s timed out after %.0f s (a peer rank failed or stalled); communicator "
+                      "aborted", what, el));
+    if (spins > 64) std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
+// Test hook (CL_MOE_EP_TEST_STALL_MS): a kernel that spins that long at the end of an expert-
+// parallel forward, after its collectives — a stand-in for a stalled peer in the single-GPU test of
+// the timeout path (tests/test_gpu_ep.py).
+__global__ void ep_stall_kernel(long long ns) {
+  const long long t0 = clock64();
+  long long now = t0;
+  while (now - t0 < ns) {  // ~1 cycle per ns at ~1-2 GHz; the exact length does not matter
+    __nanosleep(1000);
+    now = clock64();
+  }
+}
+void ep_test_stall(cudaStream_t st) {
+  static const long long ms = [] {
+    const char* e = std::getenv("CL_MOE_EP_TEST_STALL_MS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  if (ms > 0) ep_stall_kernel<<<1, 1, 0, st>>>(ms * 1000000LL * 2);
+}
+
 // One direction of the expert-parallel row exchange (layout of the last EP forward).
 // to_experts: rows of this rank's source permutation `src` (piece g at my_off[g]) go to the
 // owner of expert g, landing at its (local expert, source) slot of `dst`; otherwise the reverse.
@@ -87,6 +151,7 @@ void ep_exchange(cl_moe* h, const void* src, void* dst, bool to_experts, cudaStr
 void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train);
 
 void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaStream_t st, bool train) {
+  if (!h->comm && !h->ep_abort_reason.empty()) throw RunErr(h->ep_abort_reason);
   if (!h->comm) throw ConfigErr("expert parallelism needs cl_moe_ep_init first");
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   if (fp8 && train) throw ConfigErr("training runs in bf16 (set_precision(BF16) first)");
@@ -114,7 +179,7 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   // ---- counts exchange ----
   NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)N, NcclApi::kInt32, h->comm, st));
   CK(cudaMemcpyAsync(h->ep_counts_host, h->ep_counts_dev, sizeof(int32_t) * R * N, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  ep_wait(h, st, "counts exchange");
   h->ep_C.assign((size_t)R * N, 0);
   h->ep_piece.assign((size_t)NL * R, 0);
   h->ep_myoff.assign((size_t)N + 1, 0);
@@ -137,6 +202,7 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   prof_mark(h, 4, st);
   // ---- reverse exchange into this rank's permutation slots ----
   ep_exchange(h, h->y_recv, h->y, false, st);
+  ep_test_stall(st);
   if (out_f32)
     launch_combine<float>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<float*>(out), h->rb.finite_flag, st,
                           h->rb.combine_w);
@@ -252,6 +318,7 @@ void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
   ep_peer_experts(h, st, train);
   NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+  ep_test_stall(st);
   ep_peer_combine(h, x, T, out, out_f32, st, train);
 }
 

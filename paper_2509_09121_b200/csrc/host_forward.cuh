@@ -274,6 +274,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
     run_ep(h, x, T, out, out_f32, st);
     return;
   }
+  if (!h->ep_abort_reason.empty()) throw RunErr(h->ep_abort_reason);  // communicator aborted (host_ep.cuh ep_wait)
   if (h->cfg.ep_size > 1) throw ConfigErr("ep_size > 1 needs cl_moe_ep_init (or cl_moe_ep_group_forward)");
   const int N = static_cast<int>(h->N);
   const int tpc = h->tpc_cur;

@@ -163,6 +163,7 @@ struct cl_moe {
 
   // expert parallelism (ep.cuh)
   NcclApi::Comm comm = nullptr;
+  std::string ep_abort_reason;          // set when a failed / stalled exchange aborted the communicator
   int64_t recv_cap = 0;                 // receive-buffer rows (worst case: every rank's every slot)
   __nv_bfloat16* x_recv = nullptr;      // [recv_cap][d]
   __nv_bfloat16* act_recv = nullptr;    // [recv_cap][f]

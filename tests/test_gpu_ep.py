@@ -65,3 +65,17 @@ def test_ep_loopback_training_matches_oracle():
     assert rel(dwi.cpu().numpy(), rdwi) <= 2e-2
     assert rel(dwo.cpu().numpy(), rdwo) <= 2e-2
     lay.close()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_ep_stalled_exchange_times_out(transport):
+    """A stalled expert-parallel exchange returns CL_ERR_RUN after CL_MOE_EP_TIMEOUT_S (bounded wait
+    polling ncclCommGetAsyncError; the communicator is aborted), instead of hanging the caller
+    (proj/src/capi.cpp:57-63: failures are status codes). Fresh process: the env is read once."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root, CL_MOE_EP_TIMEOUT_S="1", CL_MOE_EP_TEST_STALL_MS="4000")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "helpers", "ep_timeout_check.py"), transport],
+                       env=env, capture_output=True, text=True, timeout=300, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr

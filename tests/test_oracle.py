@@ -355,3 +355,41 @@ def test_spec_fold_smoothing_preserves_outputs(oracle_port):
     y0 = oracle_port.moe_forward(inp["x"], inp["w_in"], inp["w_out"], r0["topk_idx"], r0["combine_weights"])
     y1 = oracle_port.moe_forward(x2, wi, inp["w_out"], r0["topk_idx"], r0["combine_weights"])
     assert np.abs(y0 - y1).max() <= 1e-5 * np.abs(y0).max()
+
+
+# ---- the counter PRNG: restatement pinned to the reference's Prng (prng.hpp:15-70) ----
+def test_prng_split_and_normals_bit_exact_vs_reference(oracle_port, oracle_ref):
+    from oracle.oracle import ROOT_SEED
+    for root in (ROOT_SEED, 0, 1, 99, 1234, 2 ** 64 - 1):
+        for stream in (0, 1, 2, 3, 16, 31, 47, 2 ** 40 + 5):
+            assert oracle_port.split_seed(root, stream) == oracle_ref.split_seed(root, stream)
+    for seed in (oracle_ref.split_seed(ROOT_SEED, 1), oracle_ref.split_seed(ROOT_SEED, 16), 5):
+        for std, mean in ((1.0, 0.0), (1.0 / 64.0, 0.0), (0.5, 1.0)):
+            a = oracle_port.normals(seed, 200000, std, mean)
+            b = oracle_ref.normals(seed, 200000, std, mean)
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_prng_replay_properties_of_reference_tests(oracle_ref):
+    """The reference's own PRNG tests (proj/tests/tensor_test.cpp:38-64), run against its Prng."""
+    first = oracle_ref.prng_u64(1234, 16)
+    assert np.array_equal(oracle_ref.prng_u64(1234, 16), first)  # identical (seed, counter) replays
+    assert oracle_ref.prng_u64(1234, 1, counter=7)[0] == first[7]  # jump straight to a counter
+    s1, s2 = oracle_ref.split_seed(99, 1), oracle_ref.split_seed(99, 2)
+    assert oracle_ref.prng_u64(s1, 1)[0] != oracle_ref.prng_u64(s2, 1)[0]
+    assert oracle_ref.split_seed(99, 1) == s1
+    u = oracle_ref.prng_doubles(5, 1000)
+    assert (u >= 0.0).all() and (u < 1.0).all()
+
+
+def test_make_inputs_streams_are_the_reference_streams(oracle_ref):
+    """make_inputs draws x / W_r / W_in / W_out from the §8(d) split streams: the same arrays come
+    out of the reference's Prng."""
+    from oracle.oracle import ROOT_SEED, make_inputs
+    t, d, n, f = 16, 256, 4, 128
+    inp = make_inputs(t, d, n, f, bf16=False)
+    sd = float(np.float32(1.0 / np.sqrt(d)))
+    assert np.array_equal(inp["x"].ravel(), oracle_ref.normals(oracle_ref.split_seed(ROOT_SEED, 1), t * d, 1.0))
+    assert np.array_equal(inp["w_router"].ravel(), oracle_ref.normals(oracle_ref.split_seed(ROOT_SEED, 2), d * n, sd))
+    assert np.array_equal(inp["w_in"][2].ravel(),
+                          oracle_ref.normals(oracle_ref.split_seed(ROOT_SEED, 16 + 2), d * 2 * f, sd))
