@@ -106,7 +106,7 @@ def _win_col_of_packed_row(p, f):
     return np.where(i < 128, b * 128 + i, f + b * 128 + (i - 128))
 
 
-def _ref_rows(o, lay, x, idx, w, rows, n, fp8=None):
+def _ref_rows(o, lay, x, idx, w, rows, n):
     """Oracle output for tokens `rows`: sum_k w[j,k] * FFN_{idx[j,k]}(x_j), per expert in fp64."""
     d = x.shape[1]
     out = np.zeros((len(rows), d), np.float64)
@@ -117,19 +117,7 @@ def _ref_rows(o, lay, x, idx, w, rows, n, fp8=None):
             continue
         wi, wo = lay.expert_weights(e)
         xe = x[[rows[i] for i, _ in sel]]
-        if fp8 is None:
-            _, y = o.expert_ffn(xe, wi, wo)
-        else:
-            s_in, s_mid, wsi, wso = fp8
-            f = wo.shape[0]
-            wi_q = _qdq_cols(o, wi, wsi[e])
-            wo_q = _qdq_cols(o, wo, wso[e])
-            xq = _qdq(xe, s_in[e])
-            h = xq.astype(np.float64) @ wi_q.astype(np.float64)
-            g, u = h[:, :f], h[:, f:]
-            a = (g / (1.0 + np.exp(-g)) * u).astype(np.float32)
-            aq = _qdq(a, s_mid[e])
-            y = aq.astype(np.float64) @ wo_q.astype(np.float64)
+        _, y = o.expert_ffn(xe, wi, wo)
         for (i, kk), yr in zip(sel, y):
             out[i] += np.float64(w[rows[i], kk]) * yr
     return out
@@ -163,10 +151,10 @@ def test_bf16_layer_at_bench_shape(cfg):
     lay.close()
 
 
-@pytest.mark.parametrize("T", [64, 512])
-def test_fp8_decode_at_c2_layer_shape(T):
+def test_fp8_decode_at_c2_layer_shape():
     """BASELINE configs[3]: expert-aware FP8 at decode batch sizes on the C2 layer (T = 64 takes the
-    dense-decode path, T = 512 the sparse one), router through fp8_qdq."""
+    dense-decode path, T = 512 the sparse one), router through fp8_qdq. One layer,
+    one set of quantized reference weights for both batches."""
     from oracle.oracle import router_fp8_sim
     d, n, k, f = 4096, 16, 2, 14336
     o = Oracle("port")
@@ -174,21 +162,40 @@ def test_fp8_decode_at_c2_layer_shape(T):
     xc = lay.synthetic_tokens(2048, SEED + 1)
     lay.calibrate(xc)
     lay.quantize_fp8()
-    xd = lay.synthetic_tokens(T, SEED)
-    out, dec = lay.forward(xd, want_decision=True)
-    lay.sync()
-    x = _host(xd)
     _, s_r, _ = lay.router_fp8_scales()
-    rq, _ = router_fp8_sim(o, x, lay.router_weights(), k, s_r)
-    assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"])
-    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"])
+    wr = lay.router_weights()
     s_in, s_mid, wsi_p, wso = lay.fp8_scales()
     wsi = np.empty_like(wsi_p)
     wsi[:, _win_col_of_packed_row(np.arange(2 * f), f)] = wsi_p  # packed row order -> reference columns
-    rows = np.arange(T) if T <= 64 else _sample(rq["topk_idx"], n, per_expert=3, extra=16)
-    want = _ref_rows(o, lay, x, rq["topk_idx"], rq["combine_weights"], rows, n, fp8=(s_in, s_mid, wsi, wso))
-    rf, _ = _assert_close(_host(out)[rows], want, rf_tol=2e-2, rm_tol=1.0)
-    print(f"FP8 T={T}: {len(rows)} rows rel-F {rf:.2e}")
+    cases = []
+    for T in (64, 512):
+        xd = lay.synthetic_tokens(T, SEED + T)
+        out, dec = lay.forward(xd, want_decision=True)
+        lay.sync()
+        x = _host(xd)
+        rq, _ = router_fp8_sim(o, x, wr, k, s_r)
+        assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"]), T
+        assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"]), T
+        rows = np.arange(T) if T <= 64 else _sample(rq["topk_idx"], n, per_expert=3, extra=16)
+        cases.append((T, x, rq, rows, _host(out)[rows]))
+    want = {T: np.zeros((len(rows), d), np.float64) for T, _, _, rows, _ in cases}
+    for e in range(n):
+        wi, wo = lay.expert_weights(e)
+        wi_q, wo_q = _qdq_cols(o, wi, wsi[e]).astype(np.float64), _qdq_cols(o, wo, wso[e]).astype(np.float64)
+        for T, x, rq, rows, _ in cases:
+            sel = [(i, kk) for i, j in enumerate(rows) for kk in range(k) if rq["topk_idx"][j, kk] == e]
+            if not sel:
+                continue
+            xq = _qdq(x[[rows[i] for i, _ in sel]], s_in[e]).astype(np.float64)
+            h = xq @ wi_q
+            g, u = h[:, :f], h[:, f:]
+            aq = _qdq((g / (1.0 + np.exp(-g)) * u).astype(np.float32), s_mid[e]).astype(np.float64)
+            y = aq @ wo_q
+            for (i, kk), yr in zip(sel, y):
+                want[T][i] += np.float64(rq["combine_weights"][rows[i], kk]) * yr
+    for T, _, _, rows, got in cases:
+        rf, _ = _assert_close(got, want[T], rf_tol=2e-2, rm_tol=1.0)
+        print(f"FP8 T={T}: {len(rows)} rows rel-F {rf:.2e}")
     lay.close()
 
 
