@@ -31,7 +31,9 @@ def main(transport):
     except MoEError as e:
         msg = str(e)
     waited = time.time() - t0
-    if "timed out" not in msg or "aborted" not in msg or waited > 3.5:
+    # detected after the 1 s limit; the call returns once ncclCommAbort is done (it drains the
+    # device work queued behind the stalled kernel), well before any hang would be noticed
+    if "timed out after 1 s" not in msg or "aborted" not in msg or waited > 15.0:
         print("BAD", msg, waited)
         return 1
     try:

@@ -4,7 +4,7 @@
 # (shared-memory hazards) per kernel family, each router variant forced in its own process.
 out=gpurun_out/sanitizer
 mkdir -p $out
-CS=compute-sanitizer
+CS="timeout 900 compute-sanitizer"
 $CS --tool memcheck --leak-check no --error-exitcode 9 python tools/sanitize_run.py all > $out/memcheck.log 2>&1; echo "memcheck rc=$?" >> $out/summary.txt
 $CS --tool synccheck --error-exitcode 9 python tools/sanitize_run.py all > $out/synccheck.log 2>&1; echo "synccheck rc=$?" >> $out/summary.txt
 for v in ws lat small big; do
