@@ -192,6 +192,14 @@ cl_status cl_moe_host_wait(cl_moe* h);
  * output (the reference's check_finite, proj/src/tensor.cpp:35-41) -> CL_ERR_RUN. */
 cl_status cl_moe_sync(cl_moe* h, void* stream);
 
+/* Large-batch routing in the fused forward (no decision export) is certified (DESIGN.md §4 K1):
+ * fp32 logits with a rigorous error bound decide every token whose top-K order is unambiguous, the
+ * others are recomputed with the reference's exact fp64 chains; routing indices, counts and the
+ * permutation are bit-exact either way. cert_calls = certified routing calls so far,
+ * last_recomputed = tokens recomputed exactly in the last one. Synchronous.
+ * Environment: CL_MOE_ROUTER_CERT=0 routes every call with the exact kernels. */
+cl_status cl_moe_router_stats(cl_moe* h, int64_t* cert_calls, int64_t* last_recomputed);
+
 /* Stage buffers of the last call (valid until the next call on the handle). After a dense-decode
  * forward (single GPU, T <= 128) they are the dense buffers: rows = N*T, row e*T + t = token t for
  * expert e (offsets[e] = e*T), row_weight = the combine weight of (t, e) or 0 when e is not among

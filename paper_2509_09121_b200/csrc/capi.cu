@@ -26,6 +26,7 @@
 #include "compass_moe.h"
 #include "grouped_gemm.cuh"
 #include "moe_kernels.cuh"
+#include "router_cert.cuh"
 #include "synth_pack.cuh"
 #include "ep.cuh"
 #include "bwd_kernels.cuh"
@@ -260,6 +261,7 @@ cl_status cl_moe_ep_peer_layout(const int64_t* counts, int32_t R, int32_t N, int
 cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
                             void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, decision != nullptr);
     if (!hidden || !out) throw ConfigErr("null argument");
     CK(cudaSetDevice(h->cfg.device));
     run_router(h, hidden, T, (cudaStream_t)stream);
@@ -271,6 +273,7 @@ cl_status cl_moe_ep_forward(cl_moe* h, const void* hidden, int64_t T, void* out,
 cl_status cl_moe_forward_train(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
                                void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, true);
     if (!hidden || !out) throw ConfigErr("null argument");
     CK(cudaSetDevice(h->cfg.device));
     ensure_training(h);
@@ -306,6 +309,7 @@ cl_status cl_moe_backward_full(cl_moe* h, const void* d_out, float g_aux, float 
 // ---- reference checkpoint format (CLCKPT1, proj/include/compasslab/checkpoint.hpp:4-9) ----
 // Failures of the create entries (no handle exists yet) are kept per thread.
 static thread_local std::string g_create_error;
+
 
 cl_status cl_moe_create_from_checkpoint(const cl_moe_config* cfg, const char* path, const char* prefix, cl_moe** out) {
   if (!out || !cfg) return CL_ERR_CONFIG;
@@ -532,6 +536,7 @@ static cl_status create_common(const cl_moe_config* cfg, cl_moe** out, const flo
       cudaFree(tmp);
     }
     widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    ++h->wr_ver;
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     build_maps(h, false);
@@ -590,6 +595,7 @@ cl_status cl_moe_synthetic_skew(cl_moe* h, double gamma) {
       for (int64_t i = 0; i < N; ++i) wr[l * N + i] = wr[l * N + i] + add[i];
     CK(cudaMemcpy(h->wr, wr.data(), sizeof(float) * d * N, cudaMemcpyHostToDevice));
     widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    ++h->wr_ver;
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
   });
@@ -597,6 +603,7 @@ cl_status cl_moe_synthetic_skew(cl_moe* h, double gamma) {
 
 cl_status cl_moe_route_tokens(cl_moe* h, const void* hidden, int64_t T, const cl_moe_decision* out, void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, true);
     if (!hidden) throw ConfigErr("hidden is null");
     CK(cudaSetDevice(h->cfg.device));
     run_router(h, hidden, T, (cudaStream_t)stream);
@@ -617,6 +624,7 @@ cl_status cl_moe_moe_forward(cl_moe* h, const void* hidden, int64_t T, const int
 cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, const cl_moe_decision* decision,
                          void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, decision != nullptr);
     if (!hidden || !out) throw ConfigErr("null argument");
     CK(cudaSetDevice(h->cfg.device));
     run_forward(h, hidden, T, out, false, (cudaStream_t)stream);
@@ -627,6 +635,7 @@ cl_status cl_moe_forward(cl_moe* h, const void* hidden, int64_t T, void* out, co
 cl_status cl_moe_route_tokens_f32(cl_moe* h, const float* hidden, int64_t T, const cl_moe_decision* out,
                                   void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, true);
     if (!hidden) throw ConfigErr("hidden is null");
     CK(cudaSetDevice(h->cfg.device));
     run_router(h, hidden, T, (cudaStream_t)stream, true, false, true);
@@ -637,6 +646,7 @@ cl_status cl_moe_route_tokens_f32(cl_moe* h, const float* hidden, int64_t T, con
 cl_status cl_moe_forward_f32(cl_moe* h, const float* hidden, int64_t T, float* out, const cl_moe_decision* decision,
                              void* stream) {
   return guarded(h, [&] {
+    ExactRoute exact_route(h, decision != nullptr);
     if (!hidden || !out) throw ConfigErr("null argument");
     if (T < 1) throw RunErr("moe_forward: B must be >= 1");
     if (T > h->cap) throw ConfigErr(fmt("T=%lld exceeds max_tokens=%lld", (long long)T, (long long)h->cap));
@@ -664,6 +674,7 @@ cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* o
     if (!exec) {
       if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
       if (dense_ok(h, T)) ensure_dense(h);  // no allocation while capturing
+      cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);
       const bool prof = h->prof;
       h->prof = false;  // no timing events inside the graph
       CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -688,6 +699,7 @@ cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* o
       }
       h->graphs.push_back({hidden, out, T, h->precision, exec});
     }
+    cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);  // weights changed?
     CK(cudaGraphLaunch(exec, (cudaStream_t)stream));
   });
 }
@@ -945,6 +957,7 @@ static void fold_smoothing_impl(cl_moe* h, const float* s) {
     scale_cols_bf16_kernel<<<grid_for(n), 256>>>(h->win, n, (int)d, h->smooth);
     scale_rows_f32_kernel<<<(int)((d * N + 255) / 256), 256>>>(h->wr, (int)d, (int)N, h->smooth);
     widen_router_kernel<<<grid_for(d * N), 256>>>(h->wr, (int)d, (int)N, h->wr64);
+    ++h->wr_ver;
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     // derived copies are stale now
@@ -1020,6 +1033,7 @@ cl_status cl_moe_quantize_fp8(cl_moe* h, const float* act_scale_in, const float*
     CK(cudaMemcpy(h->sxr_dev, &h->sxr, sizeof(float), cudaMemcpyHostToDevice));
     router_qdq_w_kernel<<<(int)((N + 127) / 128), 128>>>(h->wr, (int)h->d, N, h->wrq, h->wsr);
     widen_router_kernel<<<grid_for(h->d * N), 256>>>(h->wrq, (int)h->d, N, h->wr64q);
+    ++h->wrq_ver;
     CK(cudaGetLastError());
     CK(cudaMemcpy(h->sx_in_all, sin_all.data(), sizeof(float) * N, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->sx_in, sin_all.data() + h->e0, sizeof(float) * NL, cudaMemcpyHostToDevice));
@@ -1146,12 +1160,26 @@ cl_status cl_moe_load_fp8_scheme(cl_moe* h, const char* path) {
     quantize_rows_e4m3_kernel<<<(int)((r2 + 7) / 8), 256>>>(h->wout, r2, (int)f, h->wout8, h->ws_out, true);
     router_qdq_w_kernel<<<(int)((N + 127) / 128), 128>>>(h->wr, (int)d, (int)N, h->wrq, h->wsr, true);
     widen_router_kernel<<<grid_for(d * N), 256>>>(h->wrq, (int)d, (int)N, h->wr64q);
+    ++h->wrq_ver;
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     h->alpha_smooth = sc.alpha;
     h->tau = sc.tau;
     h->fp8_ready = true;
     h->precision = CL_MOE_FP8_E4M3;
+  });
+}
+
+cl_status cl_moe_router_stats(cl_moe* h, int64_t* cert_calls, int64_t* last_recomputed) {
+  return guarded(h, [&] {
+    CK(cudaSetDevice(h->cfg.device));
+    CK(cudaDeviceSynchronize());
+    if (cert_calls) *cert_calls = h->cert_calls;
+    if (last_recomputed) {
+      int n = 0;
+      if (h->cert_count) CK(cudaMemcpy(&n, h->cert_count, sizeof(int), cudaMemcpyDeviceToHost));
+      *last_recomputed = n;
+    }
   });
 }
 

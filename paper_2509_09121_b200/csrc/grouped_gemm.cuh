@@ -62,6 +62,9 @@ struct GemmArgs {
   int64_t group_bytes;      // kWgrad tile order: L2 budget of a resident A group (0 = m fastest)
   int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
                             // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
+  int32_t prefetch_kb;      // row-grouped: k-blocks of the NEXT tile prefetched into L2 (0 = off) ...
+  int32_t prefetch_lead;    // ... issued this many k-blocks before the end of the current tile, where
+                            // the producer also claims the next tile index
 };
 
 constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
@@ -311,8 +314,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (elect_one()) {
       int s = 0;
       uint32_t ph = 0;
-      TileInfo ti;
-      for (int i = 0;; ++i) {
+      TileInfo ti, tn;
+      // tile index i: the leader takes it from the global counter and publishes it to every
+      // consumer (and the peer CTA); the peer's producer reads it from the ring
+      auto claim = [&](int i) -> int {
         int tile;
         if (kCtaGroup == 1 || cta_rank == 0) {
           const int slot = i % kTileSlots;
@@ -326,11 +331,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tile = take_tile(i, true);
           free_tile(i, tile);
         }
+        return tile;
+      };
+      // Next-tile prefetch (row-grouped): at prefetch_lead k-blocks before the end of a tile the
+      // producer claims the next tile and asks L2 for its first prefetch_kb k-blocks (this CTA's
+      // A rows and B rows), so the first stages of the next tile do not wait a DRAM round trip at
+      // the tile boundary (where the ring's few stages of slack run out).
+      const bool pf = !kWgrad && args.prefetch_kb > 0;
+      int tile = claim(0);
+      for (int i = 0;; ++i) {
         if (tile >= total_tiles || !decode(tile, ti)) break;
         const bool half_t = kCtaGroup == 2 && ti.half;
         const int a_row = ti.a_row + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
+        int next = -1;
+        const int claim_kb = pf ? ti.kb0 + max(0, ti.nkb - args.prefetch_lead) : 1 << 30;
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
+          if (kb == claim_kb) {
+            next = claim(i + 1);
+            if (next < total_tiles && decode(next, tn)) {
+              const int na = tn.a_row + cta_rank * Cfg::kRowsPerCta, nb = tn.b_row + cta_rank * Cfg::kBRowsPerCta;
+              for (int k = tn.kb0; k < tn.kb0 + min(tn.nkb, args.prefetch_kb); ++k) {
+                tma_prefetch_2d(&tmA, k * kBKElems, na);
+                tma_prefetch_2d(&tmB, k * kBKElems, nb);
+              }
+            }
+          }
           mbar_wait(&empty[s], ph ^ 1);
           if constexpr (kWgrad) {
             // MN-major operands: boxes {64 columns, 64 rows} of the padded row-major buffers;
@@ -362,6 +388,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }
+        tile = next >= 0 ? next : claim(i + 1);
       }
     }
     __syncwarp();

@@ -13,6 +13,11 @@ int64_t l2_group_budget() {
   }();
   return budget;
 }
+// Next-tile L2 prefetch of the row-grouped GEMMs (GemmArgs::prefetch_kb / prefetch_lead).
+int gemm_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
 int m_group_for(int64_t k_bytes, int bm) {
   const int64_t budget = l2_group_budget();
   if (budget <= 0) return 0;
@@ -27,6 +32,11 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   args.tile_counter = h->tile_counter;
   if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
   if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
+  static const int pf_kb = gemm_env("CL_MOE_GEMM_PREFETCH_KB", 0), pf_lead = gemm_env("CL_MOE_GEMM_PREFETCH_LEAD", 12);
+  if (!WG) {
+    args.prefetch_kb = pf_kb;
+    args.prefetch_lead = pf_lead;
+  }
   CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(((grid_sms > 0 ? std::min(grid_sms, h->num_sms) : h->num_sms) / G) * G);
@@ -47,20 +57,21 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
 // tile geometry were chosen by run_router (tpc does not depend on XT).
 template <typename XT>
 void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, int n_tiles, int variant, int ws_cons,
-                   int big_tok, int lat_chunk, int* tail, float* rwd, int32_t* invd, cudaStream_t st) {
+                   int big_tok, int lat_chunk, int* tail, float* rwd, int32_t* invd, cudaStream_t st,
+                   const float* xs = nullptr) {
   constexpr int xb = sizeof(XT);
   const int d = (int)h->d, K = (int)h->K;
   switch (variant) {
     case 4:  // ws
       if (ws_cons == 32)
         router_ws_kernel<32, XT><<<n_tiles, 32 + 64, RouterWsSmem(N, 32, xb).total, st>>>(x, w64, (int)T, d, N, K,
-                                                                                          h->rb, tail, rwd, invd);
+                                                                                          h->rb, tail, rwd, invd, xs);
       else if (ws_cons == 64)
         router_ws_kernel<64, XT><<<n_tiles, 64 + 64, RouterWsSmem(N, 64, xb).total, st>>>(x, w64, (int)T, d, N, K,
-                                                                                          h->rb, tail, rwd, invd);
+                                                                                          h->rb, tail, rwd, invd, xs);
       else
         router_ws_kernel<128, XT><<<n_tiles, 128 + 64, RouterWsSmem(N, 128, xb).total, st>>>(x, w64, (int)T, d, N,
-                                                                                             K, h->rb, tail, rwd, invd);
+                                                                                             K, h->rb, tail, rwd, invd, xs);
       break;
     case 3:  // lat (bf16 only: the A/B variant kept from round 1)
       if constexpr (xb == 2) {
@@ -73,20 +84,77 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
       }
       break;
     case 2:  // big
-      if (big_tok == 2)
+      if (big_tok == 64)  // experiment: 64-thread CTAs (CL_MOE_BIG_THREADS=64)
+        router_big_kernel<64, 3, 4, XT><<<n_tiles, 64, RouterBigSmem(N, 64, 3, 4, xb).total, st>>>(x, w64, (int)T, d,
+                                                                                                  N, K, h->rb, xs);
+      else if (big_tok == 128)  // experiment: 128-thread CTAs
+        router_big_kernel<128, 3, 4, XT><<<n_tiles, 128, RouterBigSmem(N, 128, 3, 4, xb).total, st>>>(x, w64, (int)T,
+                                                                                                     d, N, K, h->rb, xs);
+      else if (big_tok == 5)  // experiment: 4-deep ring
+        router_big_kernel<32, 4, 4, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 4, 4, xb).total, st>>>(x, w64, (int)T, d,
+                                                                                                  N, K, h->rb, xs);
+      else if (big_tok == 2)
         router_big_kernel<32, 3, 2, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 2, xb).total, st>>>(x, w64, (int)T, d,
-                                                                                                  N, K, h->rb);
+                                                                                                  N, K, h->rb, xs);
       else
         router_big_kernel<32, 3, 4, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 4, xb).total, st>>>(x, w64, (int)T, d,
-                                                                                                  N, K, h->rb);
+                                                                                                  N, K, h->rb, xs);
       break;
     case 1:  // small
-      router_kernel<32, 8, XT><<<n_tiles, 32, router_smem_bytes(N, 32, 8, xb), st>>>(x, w64, (int)T, d, N, K, h->rb);
+      router_kernel<32, 8, XT><<<n_tiles, 32, router_smem_bytes(N, 32, 8, xb), st>>>(x, w64, (int)T, d, N, K, h->rb, xs);
       break;
     default:
       router_kernel<128, 3, XT><<<n_tiles, 128, router_smem_bytes(N, 128, 3, xb), st>>>(x, w64, (int)T, d, N, K,
-                                                                                       h->rb);
+                                                                                       h->rb, xs);
   }
+}
+
+// Certified large-batch K1 (router_cert.cuh): approximate fp32 logits + bound, exact fp64 chains for
+// the tokens whose decision is not certified, then softmax / top-K / tile statistics. Fused forward
+// without a decision export only (h->need_exact false); CL_MOE_ROUTER_CERT=0 disables it.
+bool cert_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CL_MOE_ROUTER_CERT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Allocates the certified router's buffers and rebuilds its fp32 W_r copy when the weights changed
+// (also called before a CUDA-graph capture: no allocation while capturing).
+void cert_prepare(cl_moe* h, bool fp8, cudaStream_t st) {
+  const int N = static_cast<int>(h->N), d = static_cast<int>(h->d);
+  if (!h->cert_count) h->cert_count = dalloc<int>(1);
+  float*& w8 = fp8 ? h->cert_w8q : h->cert_w8;
+  float*& wn = fp8 ? h->cert_wnq : h->cert_wn;
+  int64_t& ver = fp8 ? h->cert_verq : h->cert_ver;
+  const int64_t cur = fp8 ? h->wrq_ver : h->wr_ver;
+  if (!w8) {
+    w8 = dalloc<float>((size_t)d * ((N + 7) / 8 * 8));
+    wn = dalloc<float>((N + 7) / 8 * 8);
+  }
+  if (ver != cur) {
+    router_cert_prep_kernel<<<grid_for((int64_t)d * 8), 256, 0, st>>>(fp8 ? h->wrq : h->wr, d, N, w8, wn);
+    CK(cudaGetLastError());
+    ver = cur;
+  }
+}
+
+template <typename XT>
+void launch_router_cert(cl_moe* h, const XT* x, const float* xs, bool fp8, int64_t T, cudaStream_t st) {
+  const int N = static_cast<int>(h->N), d = static_cast<int>(h->d);
+  cert_prepare(h, fp8, st);
+  float* w8 = fp8 ? h->cert_w8q : h->cert_w8;
+  float* wn = fp8 ? h->cert_wnq : h->cert_wn;
+  CK(cudaMemsetAsync(h->cert_count, 0, sizeof(int), st));
+  const RouterCertSmem L(N, sizeof(XT));
+  router_approx_kernel<XT><<<(int)((T + L.tpc - 1) / L.tpc), kCertThreads, L.total, st>>>(
+      x, xs, w8, wn, fp8 ? h->wr64q : h->wr64, (int)T, d, N, (int)h->K, h->rb.logits, h->cert_count,
+      h->rb.finite_flag);
+  CK(cudaGetLastError());
+  router_finish_tiles_kernel<<<(int)((T + kCertFinTpc - 1) / kCertFinTpc), 256, 0, st>>>((int)T, N, (int)h->K, h->rb);
+  CK(cudaGetLastError());
+  ++h->cert_calls;
 }
 
 // route_tokens on device: K1 + K2. `xf32`: x is the caller's fp32 tensor (routing on the
@@ -100,7 +168,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   const int N = static_cast<int>(h->N);
   // FP8 scheme: the router consumes qdq(x) as fp32 (see below), so size the variants for fp32
   const bool rq = h->precision == CL_MOE_FP8_E4M3 && h->router_fp8;
-  const int xb = xf32 || rq ? 4 : 2;
+  const int xb = rq ? 1 : xf32 ? 4 : 2;  // router input bytes per value (FP8 scheme: E4M3 codes)
   // small batches: 1 token x 4 experts per thread, 32-thread CTAs, 8-deep prefetch ring (latency);
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
   // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
@@ -115,9 +183,16 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
     return e ? std::atoi(e) : 0;
   }();
   const int tiles4 = (int)((T + RouterBigSmem(N, 32, 3, 4).tpc - 1) / RouterBigSmem(N, 32, 3, 4).tpc);
-  const int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
-  const int tpc_big = RouterBigSmem(N, 32, 3, big_tok).tpc;
-  const bool big_ok = RouterBigSmem(N, 32, 3, big_tok, xb).total <= 220 * 1024;
+  static const int big_thr_env = [] {
+    const char* e = std::getenv("CL_MOE_BIG_THREADS");  // experiment: 64 | 128 (4 x 4 per thread), 5 = 4-deep ring
+    return e ? std::atoi(e) : 0;
+  }();
+  int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
+  int big_thr = 32, big_st = 3;
+  if (big_tok == 4 && (big_thr_env == 64 || big_thr_env == 128)) big_thr = big_tok = big_thr_env;
+  if (big_tok == 4 && big_thr_env == 5) big_st = 4, big_tok = 5;
+  const int tpc_big = RouterBigSmem(N, big_thr, big_st, big_tok >= 4 ? 4 : 2).tpc;
+  const bool big_ok = RouterBigSmem(N, big_thr, big_st, big_tok >= 4 ? 4 : 2, xb).total <= 220 * 1024;
   const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
   // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
   const int N4r = (N + 3) / 4 * 4;
@@ -127,7 +202,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   // decode-size batches: the warp-specialised chain kernel (ws), on the smallest CTA (32 / 64 / 128
   // chain threads) that still gives every CTA its own SM; CL_MOE_ROUTER=lat keeps the older variant
   // (bf16 input only; fp32 input takes ws)
-  const bool ws = !big && (force == 4 || (force == 0 && lat_size) || (force == 3 && xb == 4));
+  const bool ws = !big && (force == 4 || (force == 0 && lat_size) || (force == 3 && xb != 2));
   const bool lat = !big && !ws && (force == 3 || (force == 0 && lat_size));
   int ws_cons = 128;
   for (int c : {32, 64}) {
@@ -143,30 +218,36 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
                                  : router_tokens_per_cta(N, small ? 32 : 128);
   const int variant = ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
-  h->tpc_cur = tpc;
+  const bool cert = big && !h->need_exact && !dense && N <= 32 && cert_enabled() && force == 0;
+  const int tpc_eff = cert ? kCertFinTpc : tpc;
+  h->tpc_cur = tpc_eff;
   h->last_tokens = T;
-  const int n_tiles = static_cast<int>((T + tpc - 1) / tpc);
+  const int n_tiles = static_cast<int>((T + tpc_eff - 1) / tpc_eff);
   if (own_prof) prof_begin(h, st);
-  const double* w64 = h->wr64;
   if (rq) {
-    // router GEMM under the FP8 scheme: x_hat = qdq(x, s_x) per tensor, W_r_hat per
-    // expert column (quantize time); the fp64 chains then run on x_hat exactly as on an fp32 input
+    // router GEMM under the FP8 scheme: x_hat = qdq(x, s_x) per tensor (E4M3 codes,
+    // widened as code * s_x inside K1), W_r_hat per expert column (quantize time)
     const int64_t n = T * h->d;
     if (xf32)
-      router_qdq_x_kernel<float><<<grid_for(n / 8), 256, 0, st>>>(static_cast<const float*>(x), n, h->sxr_dev, h->xq32);
+      router_qdq8_kernel<float><<<grid_for(n / 16), 256, 0, st>>>(static_cast<const float*>(x), n, h->sxr_dev, h->xq8);
     else
-      router_qdq_x_kernel<__nv_bfloat16><<<grid_for(n / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n,
-                                                                           h->sxr_dev, h->xq32);
+      router_qdq8_kernel<__nv_bfloat16><<<grid_for(n / 16), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), n,
+                                                                           h->sxr_dev, h->xq8);
     CK(cudaGetLastError());
-    x = h->xq32;
-    xf32 = true;
-    w64 = h->wr64q;
-  }
-  if (xf32)
-    launch_router<float>(h, static_cast<const float*>(x), w64, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail,
+    if (cert)
+      launch_router_cert<uint8_t>(h, h->xq8, h->sxr_dev, true, T, st);
+    else
+      launch_router<uint8_t>(h, h->xq8, h->wr64q, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail, rwd, invd,
+                             st, h->sxr_dev);
+  } else if (cert && xf32) {
+    launch_router_cert<float>(h, static_cast<const float*>(x), nullptr, false, T, st);
+  } else if (cert) {
+    launch_router_cert<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), nullptr, false, T, st);
+  } else if (xf32)
+    launch_router<float>(h, static_cast<const float*>(x), h->wr64, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail,
                          rwd, invd, st);
   else
-    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), w64, T, N, n_tiles, variant, ws_cons, big_tok,
+    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), h->wr64, T, N, n_tiles, variant, ws_cons, big_tok,
                                  lat_chunk, tail, rwd, invd, st);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
@@ -415,12 +496,12 @@ void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_
 }
 
 void ensure_fp8_storage(cl_moe* h) {
-  if (!h->xq32) {  // router under the FP8 scheme
+  if (!h->xq8) {  // router under the FP8 scheme
     h->sxr_dev = dalloc<float>(1);
     h->wrq = dalloc<float>(h->d * h->N);
     h->wsr = dalloc<float>(h->N);
     h->wr64q = dalloc<double>(3 * h->d * ((h->N + 3) / 4 * 4));
-    h->xq32 = dalloc<float>(h->cap * h->d);
+    h->xq8 = dalloc<uint8_t>(h->cap * h->d);
   }
   if (h->win8) return;
   h->win8 = dalloc<uint8_t>((size_t)h->n_local * 2 * h->f * h->d);

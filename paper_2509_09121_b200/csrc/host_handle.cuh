@@ -110,7 +110,17 @@ struct cl_moe {
   float* wrq = nullptr;                // [d][N] qdq(W_r) fp32
   float* wsr = nullptr;                // [N] router weight scales (per expert column)
   double* wr64q = nullptr;             // widened qdq(W_r), same layout as wr64
-  float* xq32 = nullptr;               // [cap][d] qdq(x) fp32 (router operand)
+  uint8_t* xq8 = nullptr;              // [cap][d] E4M3 codes of x / s_x (router operand, FP8 scheme)
+  // certified large-batch router (router_cert.cuh): fp32 padded W_r copies [d][N8] + ||w_i|| bounds
+  // of the plain and of the FP8-scheme router, rebuilt when the weights change (version counters)
+  float* cert_w8 = nullptr;
+  float* cert_wn = nullptr;
+  float* cert_w8q = nullptr;
+  float* cert_wnq = nullptr;
+  int* cert_count = nullptr;           // [1] tokens recomputed exactly by the last certified call
+  int64_t wr_ver = 0, wrq_ver = 0, cert_ver = -1, cert_verq = -1;
+  bool need_exact = false;             // the current call exports the decision (or trains): exact K1 only
+  int64_t cert_calls = 0;
   // QuantScheme bookkeeping (scheme file)
   std::vector<float> smooth_applied;   // product of the folded smoothing vectors (empty: none)
   double alpha_smooth = NAN;           // alpha of the last compute_smoothing
@@ -248,7 +258,8 @@ struct cl_moe {
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
                     (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
                     (void*)row_ptr_dx, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr, (void*)x16, (void*)sxr_dev, (void*)wrq,
-                    (void*)wsr, (void*)wr64q, (void*)xq32})
+                    (void*)wsr, (void*)wr64q, (void*)xq8, (void*)cert_w8, (void*)cert_wn,
+                    (void*)cert_w8q, (void*)cert_wnq, (void*)cert_count})
       if (p) cudaFree(p);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     if (ep_counts_host) cudaFreeHost(ep_counts_host);
@@ -271,6 +282,19 @@ struct cl_moe {
 };
 
 namespace {
+
+// The call exports the routing decision (or trains on it): K1 must produce the reference's exact
+// logits / probabilities, not only a certified decision (router_cert.cuh).
+struct ExactRoute {
+  cl_moe* h;
+  bool prev;
+  ExactRoute(cl_moe* hh, bool on) : h(hh), prev(hh ? hh->need_exact : false) {
+    if (h) h->need_exact = prev || on;
+  }
+  ~ExactRoute() {
+    if (h) h->need_exact = prev;
+  }
+};
 
 template <typename Fn>
 cl_status guarded(cl_moe* h, Fn fn) {
@@ -408,6 +432,14 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  for (const void* fn : {(const void*)router_big_kernel<64, 3, 4, __nv_bfloat16>,
+                         (const void*)router_big_kernel<128, 3, 4, __nv_bfloat16>,
+                         (const void*)router_big_kernel<32, 4, 4, __nv_bfloat16>,
+                         (const void*)router_big_kernel<64, 3, 4, float>, (const void*)router_big_kernel<128, 3, 4, float>,
+                         (const void*)router_big_kernel<32, 4, 4, float>, (const void*)router_big_kernel<64, 3, 4, uint8_t>,
+                         (const void*)router_big_kernel<128, 3, 4, uint8_t>,
+                         (const void*)router_big_kernel<32, 4, 4, uint8_t>})
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -422,6 +454,17 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_ws_kernel<32, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<64, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<128, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  for (const void* fn : {(const void*)router_approx_kernel<__nv_bfloat16>, (const void*)router_approx_kernel<float>,
+                         (const void*)router_approx_kernel<uint8_t>})
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  // E4M3-code instantiations (the router under the FP8 scheme)
+  CK(cudaFuncSetAttribute(router_kernel<128, 3, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_kernel<32, 8, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 4, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 2, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<32, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<64, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  CK(cudaFuncSetAttribute(router_ws_kernel<128, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   h->win = dalloc<__nv_bfloat16>((size_t)h->n_local * 2 * h->f * h->d);
   h->wout = dalloc<__nv_bfloat16>((size_t)h->n_local * h->d * h->f);
   h->sx_in = dalloc<float>(h->n_local);

@@ -64,21 +64,29 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Router input element: bf16 (the device path's storage type) or fp32 (the reference's own Tensor
-// values). Either widens exactly to fp64, and a float x float product is exact in
-// fp64, so the ascending-l chains stay bit-identical to gemm_nn for both.
+// Router input element: bf16 (the device path's storage type), fp32 (the reference's own Tensor
+// values), or uint8 = E4M3 codes of the FP8 scheme's router operand, whose value
+// is code * s (fp32 multiply: exactly qdq_e4m3's x_hat). Each widens exactly to fp64, and a
+// float x float product is exact in fp64, so the ascending-l chains stay bit-identical to gemm_nn.
 template <typename XT>
-__device__ __forceinline__ double x_to_f64(XT v) {
-  if constexpr (sizeof(XT) == 2) return static_cast<double>(__bfloat162float(v));
-  else return static_cast<double>(v);
+__device__ __forceinline__ double x_to_f64(XT v, float xs = 1.0f) {
+  if constexpr (sizeof(XT) == 1) {
+    const __half_raw hr = __nv_cvt_fp8_to_halfraw(static_cast<__nv_fp8_storage_t>(v), __NV_E4M3);
+    return static_cast<double>(__fmul_rn(__half2float(__half(hr)), xs));
+  } else if constexpr (sizeof(XT) == 2) {
+    return static_cast<double>(__bfloat162float(v));
+  } else {
+    return static_cast<double>(v);
+  }
 }
-// 16 bytes of raw x -> its 8 (bf16) or 4 (fp32) values in fp64
+// 16 bytes of raw x -> its 16 (e4m3), 8 (bf16) or 4 (fp32) values in fp64
 template <typename XT>
-__device__ __forceinline__ void widen16(const int4& raw, double* out) {
+__device__ __forceinline__ void widen16(const int4& raw, double* out, float xs = 1.0f) {
   const XT* v = reinterpret_cast<const XT*>(&raw);
 #pragma unroll
-  for (int i = 0; i < 16 / (int)sizeof(XT); ++i) out[i] = x_to_f64<XT>(v[i]);
+  for (int i = 0; i < 16 / (int)sizeof(XT); ++i) out[i] = x_to_f64<XT>(v[i], xs);
 }
+__device__ __forceinline__ float router_xscale(const float* p) { return p ? *p : 1.0f; }
 
 // Chunk length (steps) of router_ws_kernel's ring, by padded expert count.
 __host__ __device__ inline int router_ws_chunk(int N4) { return N4 <= 16 ? 256 : N4 <= 32 ? 128 : N4 <= 64 ? 64 : 32; }
@@ -185,8 +193,10 @@ __device__ __forceinline__ void router_finish(int tile, int tok0, int tpc, int T
 template <int kRouterThreads, int kStages, typename XT = __nv_bfloat16>
 __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const XT* __restrict__ x,
                                                                 const double* __restrict__ wr64, int T, int d,
-                                                                int N, int K, RouteBufs rb) {
+                                                                int N, int K, RouteBufs rb,
+                                                                const float* __restrict__ xscale = nullptr) {
   constexpr int kXB = sizeof(XT), kPerPiece = 16 / kXB;  // x elements per 16-byte cp.async piece
+  const float xsc = router_xscale(xscale);
   const RouterSmem L(N, kRouterThreads, kStages, kXB);
   const int groups = L.N4 / 4;
   const int N4 = L.N4;
@@ -246,9 +256,11 @@ __global__ void __launch_bounds__(kRouterThreads, 1) router_kernel(const XT* __r
         const __nv_bfloat162 v = reinterpret_cast<const __nv_bfloat162*>(rx)[i];
         *reinterpret_cast<double2*>(sx + r * xs + l) =
             make_double2(static_cast<double>(__low2float(v)), static_cast<double>(__high2float(v)));
-      } else {
+      } else if constexpr (kXB == 4) {
         const float2 v = reinterpret_cast<const float2*>(rx)[i];
         *reinterpret_cast<double2*>(sx + r * xs + l) = make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+      } else {
+        *reinterpret_cast<double2*>(sx + r * xs + l) = make_double2(x_to_f64<XT>(rx[2 * i], xsc), x_to_f64<XT>(rx[2 * i + 1], xsc));
       }
     }
     __syncthreads();
@@ -731,7 +743,8 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const XT* __re
                                                                  int N, int K, RouteBufs rb,
                                                                  int* __restrict__ tail_ctr = nullptr,
                                                                  float* __restrict__ rwd = nullptr,
-                                                                 int32_t* __restrict__ invd = nullptr) {
+                                                                 int32_t* __restrict__ invd = nullptr,
+                                                                 const float* __restrict__ xscale = nullptr) {
   constexpr int kD = RouterWsSmem::kAhead, kB = 32;
   static_assert(kCons % 32 == 0 && kCons / 32 <= RouterWsSmem::kMaxChainWarps, "eflag region holds one slot per chain warp");
   constexpr int kXB = sizeof(XT);
@@ -781,6 +794,7 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const XT* __re
       }
     }
   } else if (warp == kCons / 32) {  // converter
+    const float xsc = router_xscale(xscale);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % kStages;
       mbar_wait(&full[s], (c / kStages) & 1);
@@ -789,7 +803,7 @@ __global__ void __launch_bounds__(kCons + 64, 1) router_ws_kernel(const XT* __re
       constexpr int kV = 16 / kXB;  // values per 16-byte load
       for (int i = lane * kV; i < ntok * chunk; i += 32 * kV) {
         double v[kV];
-        widen16<XT>(*reinterpret_cast<const int4*>(rx + i), v);
+        widen16<XT>(*reinterpret_cast<const int4*>(rx + i), v, xsc);
 #pragma unroll
         for (int j = 0; j < kV; j += 2) *reinterpret_cast<double2*>(xo + i + j) = make_double2(v[j], v[j + 1]);
       }
@@ -899,9 +913,14 @@ struct RouterBigSmem {
 template <int kThreads, int kStages, int kTok = 4, typename XT = __nv_bfloat16>
 __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const XT* __restrict__ x,
                                                                  const double* __restrict__ wr64, int T, int d, int N,
-                                                                 int K, RouteBufs rb) {
-  // kXB = 2: a token's 64-column chunk is 8 x 16 B; fp32 x: 16 x 16 B, swizzled in 32-byte pairs
-  constexpr int kXB = sizeof(XT), kRowB = kRouterChunk * kXB, kP = kXB / 2;  // 16-byte pieces per 8 values
+                                                                 int K, RouteBufs rb,
+                                                                 const float* __restrict__ xscale = nullptr) {
+  // a token's 64-column chunk: bf16 8 x 16 B (16-byte pieces swizzled by token group); fp32 16 x
+  // 16 B swizzled in 32-byte pairs; e4m3 codes 4 x 16 B (each piece = two 8-value groups)
+  constexpr int kXB = sizeof(XT), kRowB = kRouterChunk * kXB;
+  constexpr int kP = kXB >= 2 ? kXB / 2 : 1;     // 16-byte pieces per 8-value group (e4m3: per 2 groups)
+  constexpr int kPieces = kRowB / 16;            // pieces per row
+  const float xsc = router_xscale(xscale);
   const RouterBigSmem L(N, kThreads, kStages, kTok, kXB);
   const int N4 = L.N4;
   const int groups = N4 / 4;
@@ -925,16 +944,22 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const XT* __res
     for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
 
   const int nchunks = d / kRouterChunk;
-  const int xpieces = tpc * 8 * kP;  // 16-byte pieces per token row per stage
+  const int xpieces = tpc * kPieces;  // 16-byte pieces per token row per stage
   const int wpieces = kRouterChunk * N4 / 2;
   auto issue = [&](int c, int buf) {
     const int c0 = c * kRouterChunk;
     for (int i = threadIdx.x; i < xpieces; i += kThreads) {
-      const int r = i / (8 * kP), p = i % (8 * kP), q = p / kP, h = p % kP;  // 8-value group q, half h
+      const int r = i / kPieces, p = i % kPieces;
       const bool ok = tok0 + r < T;
-      const XT* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * 8 + h * (16 / kXB);
-      const int qs = q ^ ((r / kTok) & 7);
-      cp_async16(rawx + ((size_t)buf * tpc + r) * kRowB + (qs * kP + h) * 16, src, ok);
+      const XT* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + p * (16 / kXB);
+      int ps;
+      if constexpr (kXB == 1) {
+        ps = p ^ ((r / kTok) & 3);
+      } else {
+        const int q = p / kP, h = p % kP;  // 8-value group q, half h
+        ps = (q ^ ((r / kTok) & 7)) * kP + h;
+      }
+      cp_async16(rawx + ((size_t)buf * tpc + r) * kRowB + ps * 16, src, ok);
     }
     const double* wsrc = wr64 + (size_t)c0 * N4;
     for (int i = threadIdx.x; i < wpieces; i += kThreads)
@@ -961,9 +986,18 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const XT* __res
 #pragma unroll
         for (int a = 0; a < kTok; ++a) {
           const int r = tg * kTok + a;
-          const uint8_t* g8 = xb + (size_t)r * kRowB + (q ^ ((r / kTok) & 7)) * kP * 16;
+          if constexpr (kXB == 1) {
+            const uint2 raw = *reinterpret_cast<const uint2*>(xb + (size_t)r * kRowB + ((q >> 1) ^ ((r / kTok) & 3)) * 16 +
+                                                              (q & 1) * 8);
+            const uint8_t* cb = reinterpret_cast<const uint8_t*>(&raw);
 #pragma unroll
-          for (int h = 0; h < kP; ++h) widen16<XT>(*reinterpret_cast<const int4*>(g8 + h * 16), &xd[a][h * (16 / kXB)]);
+            for (int i = 0; i < 8; ++i) xd[a][i] = x_to_f64<XT>(cb[i], xsc);
+          } else {
+            const uint8_t* g8 = xb + (size_t)r * kRowB + (q ^ ((r / kTok) & 7)) * kP * 16;
+#pragma unroll
+            for (int h = 0; h < kP; ++h)
+              widen16<XT>(*reinterpret_cast<const int4*>(g8 + h * 16), &xd[a][h * (16 / kXB)]);
+          }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {

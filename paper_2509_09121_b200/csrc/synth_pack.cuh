@@ -202,28 +202,44 @@ __global__ void router_qdq_w_kernel(const float* __restrict__ wr, int d, int N, 
   for (int l = 0; l < d; ++l) wq[(size_t)l * N + c] = qdq_e4m3(wr[(size_t)l * N + c], s);
 }
 
-// The router's activation operand under the FP8 scheme: x_hat = qdq(x, s_x) with the per-tensor
-// calibration scale s_x (device scalar), written as fp32 for the fp32-input router. 8 values per
-// thread per step (16-byte bf16 / 2 x 16-byte fp32 loads, 2 x 16-byte stores).
+// The router's activation operand under the FP8 scheme: the E4M3 codes of x / s_x (per-tensor
+// calibration scale s_x, a device scalar); the router widens code * s_x, which is exactly
+// qdq_e4m3(x, s_x). 16 values per thread per step (one 16-byte store).
 template <typename XT>
-__global__ void router_qdq_x_kernel(const XT* __restrict__ x, int64_t n, const float* __restrict__ sx,
-                                    float* __restrict__ out) {
+__global__ void router_qdq8_kernel(const XT* __restrict__ x, int64_t n, const float* __restrict__ sx,
+                                   uint8_t* __restrict__ out) {
   const float s = *sx;
-  const int64_t n8 = n / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    float v[8];
+  const int64_t n16 = n / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+    float v[16];
     if constexpr (sizeof(XT) == 2) {
-      const int4 raw = *reinterpret_cast<const int4*>(x + i * 8);
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(h[j]);
+      for (int h = 0; h < 2; ++h) {
+        const int4 raw = reinterpret_cast<const int4*>(x + i * 16)[h];
+        const __nv_bfloat16* b = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[8 * h + j] = __bfloat162float(b[j]);
+      }
     } else {
-      const float4 a = reinterpret_cast<const float4*>(x)[2 * i], b = reinterpret_cast<const float4*>(x)[2 * i + 1];
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float4 f = reinterpret_cast<const float4*>(x + i * 16)[h];
+        v[4 * h] = f.x;
+        v[4 * h + 1] = f.y;
+        v[4 * h + 2] = f.z;
+        v[4 * h + 3] = f.w;
+      }
     }
-    float4* o = reinterpret_cast<float4*>(out + i * 8);
-    o[0] = make_float4(qdq_e4m3(v[0], s), qdq_e4m3(v[1], s), qdq_e4m3(v[2], s), qdq_e4m3(v[3], s));
-    o[1] = make_float4(qdq_e4m3(v[4], s), qdq_e4m3(v[5], s), qdq_e4m3(v[6], s), qdq_e4m3(v[7], s));
+    uint32_t p[4];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+          make_float2(__fdiv_rn(v[4 * w], s), __fdiv_rn(v[4 * w + 1], s)), __NV_SATFINITE, __NV_E4M3);
+      const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+          make_float2(__fdiv_rn(v[4 * w + 2], s), __fdiv_rn(v[4 * w + 3], s)), __NV_SATFINITE, __NV_E4M3);
+      p[w] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
+    }
+    reinterpret_cast<int4*>(out)[i] = make_int4((int)p[0], (int)p[1], (int)p[2], (int)p[3]);
   }
 }
 

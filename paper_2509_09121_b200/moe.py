@@ -210,6 +210,12 @@ class MoELayer:
         act_scale > 0 fixes the router's activation scale (else: calibration max / 448)."""
         self._check(self.L.cl_moe_set_router_fp8(self.h, int(enable), float(act_scale)), "set_router_fp8")
 
+    def router_stats(self):
+        """(certified routing calls so far, tokens recomputed exactly in the last one)."""
+        a, b = C.c_int64(), C.c_int64()
+        self._check(self.L.cl_moe_router_stats(self.h, C.byref(a), C.byref(b)), "router_stats")
+        return a.value, b.value
+
     def router_weights(self) -> np.ndarray:
         """Host copy of W_r [d x N] (fp32) as the layer holds it."""
         w = np.empty((self.cfg.d_model, self.cfg.n_experts), np.float32)

@@ -2,8 +2,9 @@
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
 including ragged last tiles, shapes where the automatic choice would pick another variant, and exact
 ties (duplicated router columns, all-zero tokens: the lowest expert index must win). Each case runs
-twice: bf16 tokens, and unrounded fp32 tokens through the fp32 router input (the "lat" variant is
-bf16-only; forced with fp32 input it runs ws)."""
+three times: bf16 tokens; unrounded fp32 tokens through the fp32 router input; and the router of the
+FP8 scheme (E4M3 codes of x / s_x widened in K1, qdq'd W_r) against router_fp8_sim. The "lat"
+variant is bf16-only; forced with another input it runs ws."""
 import os
 import subprocess
 import sys
@@ -20,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
                                           (257, 256, 32, 4, "random"), (70, 1024, 4, 1, "random"),
                                           (5, 256, 128, 8, "random"), (300, 256, 16, 4, "ties"),
                                           (90, 256, 128, 8, "ties"), (2400, 256, 4, 2, "random")])
-@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32", "fp8"])
 def test_router_variant_bit_exact(variant, t, d, n, k, mode, dtype):
     env = dict(os.environ, CL_MOE_ROUTER=variant.rstrip("24"), PYTHONPATH=ROOT)
     if variant.startswith("big"):
