@@ -111,27 +111,25 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
 
 // Certified large-batch K1 (router_cert.cuh): approximate fp32 logits + bound, exact fp64 chains for
 // the tokens whose decision is not certified, then softmax / top-K / tile statistics. Fused forward
-// without a decision export only (h->need_exact false); CL_MOE_ROUTER_CERT=0 disables it.
+// without a decision export only (h->need_exact false). Opt-in (CL_MOE_ROUTER_CERT=1, read per call):
+// on this B200 it did not beat the exact large-batch kernel (DESIGN.md §4 K1).
 bool cert_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("CL_MOE_ROUTER_CERT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+  const char* e = std::getenv("CL_MOE_ROUTER_CERT");
+  return e && e[0] == '1';
 }
 
 // Allocates the certified router's buffers and rebuilds its fp32 W_r copy when the weights changed
 // (also called before a CUDA-graph capture: no allocation while capturing).
 void cert_prepare(cl_moe* h, bool fp8, cudaStream_t st) {
-  const int N = static_cast<int>(h->N), d = static_cast<int>(h->d);
+  const int N = static_cast<int>(h->N), d = static_cast<int>(h->d), N8 = cert_n8(N);
   if (!h->cert_count) h->cert_count = dalloc<int>(1);
   float*& w8 = fp8 ? h->cert_w8q : h->cert_w8;
   float*& wn = fp8 ? h->cert_wnq : h->cert_wn;
   int64_t& ver = fp8 ? h->cert_verq : h->cert_ver;
   const int64_t cur = fp8 ? h->wrq_ver : h->wr_ver;
   if (!w8) {
-    w8 = dalloc<float>((size_t)d * ((N + 7) / 8 * 8));
-    wn = dalloc<float>((N + 7) / 8 * 8);
+    w8 = dalloc<float>((size_t)d * N8);
+    wn = dalloc<float>(N8);
   }
   if (ver != cur) {
     router_cert_prep_kernel<<<grid_for((int64_t)d * 8), 256, 0, st>>>(fp8 ? h->wrq : h->wr, d, N, w8, wn);
@@ -140,19 +138,17 @@ void cert_prepare(cl_moe* h, bool fp8, cudaStream_t st) {
   }
 }
 
+int cert_tpc(int N, int xb) { return RouterCertSmem(N, xb).tpc; }
+
 template <typename XT>
 void launch_router_cert(cl_moe* h, const XT* x, const float* xs, bool fp8, int64_t T, cudaStream_t st) {
   const int N = static_cast<int>(h->N), d = static_cast<int>(h->d);
   cert_prepare(h, fp8, st);
-  float* w8 = fp8 ? h->cert_w8q : h->cert_w8;
-  float* wn = fp8 ? h->cert_wnq : h->cert_wn;
   CK(cudaMemsetAsync(h->cert_count, 0, sizeof(int), st));
   const RouterCertSmem L(N, sizeof(XT));
-  router_approx_kernel<XT><<<(int)((T + L.tpc - 1) / L.tpc), kCertThreads, L.total, st>>>(
-      x, xs, w8, wn, fp8 ? h->wr64q : h->wr64, (int)T, d, N, (int)h->K, h->rb.logits, h->cert_count,
-      h->rb.finite_flag);
-  CK(cudaGetLastError());
-  router_finish_tiles_kernel<<<(int)((T + kCertFinTpc - 1) / kCertFinTpc), 256, 0, st>>>((int)T, N, (int)h->K, h->rb);
+  router_cert_kernel<XT><<<(int)((T + L.tpc - 1) / L.tpc), kCertThreads, L.total, st>>>(
+      x, xs, fp8 ? h->cert_w8q : h->cert_w8, fp8 ? h->cert_wnq : h->cert_wn, fp8 ? h->wr64q : h->wr64, (int)T, d, N,
+      (int)h->K, h->rb, h->cert_count);
   CK(cudaGetLastError());
   ++h->cert_calls;
 }
@@ -219,7 +215,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
                                  : router_tokens_per_cta(N, small ? 32 : 128);
   const int variant = ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
   const bool cert = big && !h->need_exact && !dense && N <= 32 && cert_enabled() && force == 0;
-  const int tpc_eff = cert ? kCertFinTpc : tpc;
+  const int tpc_eff = cert ? cert_tpc(N, xb) : tpc;
   h->tpc_cur = tpc_eff;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc_eff - 1) / tpc_eff);

@@ -454,8 +454,8 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_ws_kernel<32, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<64, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_ws_kernel<128, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  for (const void* fn : {(const void*)router_approx_kernel<__nv_bfloat16>, (const void*)router_approx_kernel<float>,
-                         (const void*)router_approx_kernel<uint8_t>})
+  for (const void* fn : {(const void*)router_cert_kernel<__nv_bfloat16>, (const void*)router_cert_kernel<float>,
+                         (const void*)router_cert_kernel<uint8_t>})
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   // E4M3-code instantiations (the router under the FP8 scheme)
   CK(cudaFuncSetAttribute(router_kernel<128, 3, uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
