@@ -129,6 +129,36 @@ __device__ __forceinline__ bool decode_tile(int tile, const int* mt_prefix, cons
   return true;
 }
 
+// Row-grouped decode with clusters of two CTA pairs (kCM == 2): a tile is an m-tile PAIR x one
+// n-block; pair p of the cluster takes m-tile 2 mp + p (inactive when the expert has no such
+// m-tile: it still streams its share of the shared B tile). mp_prefix = expert prefix of m-pairs;
+// m_group counts m-pairs.
+__device__ __forceinline__ bool decode_tile_mc(int tile, const int* mp_prefix, const int* s_off, const GemmArgs& a,
+                                               int bm, int pair, TileInfo& ti, bool& active) {
+  if (tile >= mp_prefix[a.n_experts] * a.n_tiles_n) return false;
+  int e = 0;
+  while (tile >= mp_prefix[e + 1] * a.n_tiles_n) ++e;
+  const int local = tile - mp_prefix[e] * a.n_tiles_n;
+  const int mpairs = mp_prefix[e + 1] - mp_prefix[e];
+  const int gm = (a.m_group > 0 && a.m_group < mpairs) ? a.m_group : mpairs;
+  const int g = local / (gm * a.n_tiles_n);
+  const int within = local - g * gm * a.n_tiles_n;
+  const int gsz = min(gm, mpairs - g * gm);
+  ti.e = e;
+  ti.nt = within / gsz;
+  const int mp = g * gm + (within - ti.nt * gsz);
+  ti.mt = 2 * mp + pair;
+  const int mtiles = (s_off[e + 1] - s_off[e] + bm - 1) / bm;
+  active = ti.mt < mtiles;
+  ti.a_row = s_off[e] + ti.mt * bm;
+  ti.b_row = e * a.b_rows_per_expert + ti.nt * kBN;
+  ti.row_end = s_off[e + 1];
+  ti.kb0 = 0;
+  ti.nkb = a.num_kb;
+  ti.half = active && a.half_tail && ti.row_end - ti.a_row <= bm / 2;
+  return true;
+}
+
 // K-grouped decode (weight gradients): every expert has m_tiles x n_tiles_n tiles; the K range
 // is the expert's padded row range, so its operand slabs grow with its row count. m-tiles go in
 // groups whose A slabs fit `group_bytes` of L2 (m fastest inside, sweeping every n-block), as in
@@ -207,11 +237,18 @@ __device__ __forceinline__ void store_t_bf16x32(__nv_bfloat16* dst, int64_t stri
   for (int i = 0; i < 32; ++i) dst[(size_t)i * stride] = __float2bfloat16_rn(v[i]);
 }
 
-template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8, bool kWgrad = false>
+// kCM (CTA pairs per cluster, 1 or 2; 2 needs kCtaGroup == 2 and a row-grouped mode): with 2, the
+// two pairs of a cluster compute adjacent m-tiles of the same n-block and share its B tile through
+// TMA multicast — each CTA loads one 64-row quarter box and multicasts it to the same-half CTA of
+// the other pair — halving the B operand's L2 -> SM traffic; a stage slot is refilled only when
+// both pairs' MMAs have released it (tcgen05.commit multicast to all four CTAs, empty count 2).
+template <int kCtaGroup, int kEpi, bool kFp8, bool kOutFp8, bool kWgrad = false, int kCM = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const GemmArgs args) {
+  static_assert(kCM == 1 || (kCM == 2 && kCtaGroup == 2 && !kWgrad), "multicast clusters: pair mode, row-grouped");
   using Cfg = GemmCfg<kCtaGroup>;
+  constexpr int kCS = kCtaGroup * kCM;  // cluster size
   constexpr int S = Cfg::kStages;
   constexpr int kUmmaKBytes = 32;                    // 16 bf16 or 32 e4m3 per MMA
   constexpr int kMmaPerKb = kBKBytes / kUmmaKBytes;  // 4
@@ -242,17 +279,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const uint32_t cta_rank = kCtaGroup == 1 ? 0 : cluster_ctarank();
-  const int cluster = kCtaGroup == 1 ? blockIdx.x : cluster_id_x();
-  const int nclusters = kCtaGroup == 1 ? gridDim.x : nclusters_x();
+  const uint32_t crank = kCS == 1 ? 0 : cluster_ctarank();  // rank in the cluster
+  const uint32_t cta_rank = crank & (kCtaGroup - 1);          // rank in the CTA pair
+  const uint32_t pair = crank / kCtaGroup;                      // pair in the cluster (kCM == 2)
+  const uint32_t pleader = crank & ~(uint32_t)(kCtaGroup - 1);  // the pair leader's cluster rank
+  const bool sched = crank == 0;                                // the cluster's tile scheduler
+  const uint16_t pair_mask = (uint16_t)(((1u << kCtaGroup) - 1) << pleader);
+  const uint16_t all_mask = (uint16_t)((1u << kCS) - 1);
 
   for (int i = threadIdx.x; i <= args.n_experts; i += blockDim.x) s_off[i] = kWgrad ? args.kb_off[i] : args.offsets[i];
-  if (!kWgrad && threadIdx.x == 0) {
+  if (!kWgrad && threadIdx.x == 0) {  // (kCM == 2: prefix of m-tile pairs)
     int acc = 0;
     mt_prefix[0] = 0;
     for (int e = 0; e < args.n_experts; ++e) {
       const int cnt = args.offsets[e + 1] - args.offsets[e];
-      acc += (cnt + Cfg::kBM - 1) / Cfg::kBM;
+      acc += ((cnt + Cfg::kBM - 1) / Cfg::kBM + kCM - 1) / kCM;
       mt_prefix[e + 1] = acc;
     }
   }
@@ -263,28 +304,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kCM);  // released by every pair's MMA (kCM == 2: the slot is shared)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * kCtaGroup);
     }
-    // consumers of a tile index: MMA issuer + epilogue warps of the leader, and (pair) the peer's
-    // producer + epilogue warps
+    // consumers of a tile index: every pair leader's MMA issuer, every other CTA's producer and
+    // every CTA's epilogue warps
     for (int i = 0; i < kTileSlots; ++i) {
       mbar_init(&tfill[i], 1);
-      mbar_init(&tfree[i], kCtaGroup == 1 ? 1 + kEpiWarps : 2 + 2 * kEpiWarps);
+      mbar_init(&tfree[i], kCM + (kCS - 1) + kCS * kEpiWarps);
     }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kCtaGroup>(tmem_slot, 512);
   tc_fence_before();
-  if constexpr (kCtaGroup == 2) cluster_sync(); else __syncthreads();
+  if constexpr (kCS > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  auto decode = [&](int tile, TileInfo& ti) -> bool {
+  // `active`: this pair has a tile (kCM == 2: the cluster's second m-tile may not exist)
+  auto decode = [&](int tile, TileInfo& ti, bool& active) -> bool {
+    active = true;
     if constexpr (kWgrad) return decode_tile_wgrad(tile, s_off, args, Cfg::kBM, ti);
+    else if constexpr (kCM == 2) return decode_tile_mc(tile, mt_prefix, s_off, args, Cfg::kBM, pair, ti, active);
     else return decode_tile(tile, mt_prefix, s_off, args, Cfg::kBM, ti);
   };
   const int total_tiles = kWgrad ? args.n_experts * args.m_tiles * args.n_tiles_n : mt_prefix[args.n_experts] * args.n_tiles_n;
@@ -305,7 +349,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   auto free_tile = [&](int i, int tile) {
     const int slot = i % kTileSlots;
     if (tile < 0) return;
-    if (kCtaGroup == 1 || cta_rank == 0) mbar_arrive_relaxed(&tfree[slot]);
+    if (sched) mbar_arrive_relaxed(&tfree[slot]);
     else mbar_arrive_cluster_relaxed(&tfree[slot], 0);
   };
 
@@ -319,14 +363,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // consumer (and the peer CTA); the peer's producer reads it from the ring
       auto claim = [&](int i) -> int {
         int tile;
-        if (kCtaGroup == 1 || cta_rank == 0) {
+        if (sched) {
           const int slot = i % kTileSlots;
           mbar_wait(&tfree[slot], ((i / kTileSlots) & 1) ^ 1);
           tile = min(atomicAdd(args.tile_counter, 1), total_tiles);
           tile_ring[slot] = tile;
-          if constexpr (kCtaGroup == 2) st_shared_cluster_u32(mapa(smem_u32(&tile_ring[slot]), 1), (uint32_t)tile);
+#pragma unroll
+          for (int r = 1; r < kCS; ++r) st_shared_cluster_u32(mapa(smem_u32(&tile_ring[slot]), r), (uint32_t)tile);
           mbar_arrive(&tfill[slot]);
-          if constexpr (kCtaGroup == 2) mbar_arrive_cluster(&tfill[slot], 1);
+#pragma unroll
+          for (int r = 1; r < kCS; ++r) mbar_arrive_cluster(&tfill[slot], r);
         } else {
           tile = take_tile(i, true);
           free_tile(i, tile);
@@ -337,10 +383,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // producer claims the next tile and asks L2 for its first prefetch_kb k-blocks (this CTA's
       // A rows and B rows), so the first stages of the next tile do not wait a DRAM round trip at
       // the tile boundary (where the ring's few stages of slack run out).
-      const bool pf = !kWgrad && args.prefetch_kb > 0;
+      const bool pf = !kWgrad && kCM == 1 && args.prefetch_kb > 0;
       int tile = claim(0);
       for (int i = 0;; ++i) {
-        if (tile >= total_tiles || !decode(tile, ti)) break;
+        bool active, nactive;
+        if (tile >= total_tiles || !decode(tile, ti, active)) break;
         const bool half_t = kCtaGroup == 2 && ti.half;
         const int a_row = ti.a_row + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
@@ -349,7 +396,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           if (kb == claim_kb) {
             next = claim(i + 1);
-            if (next < total_tiles && decode(next, tn)) {
+            if (next < total_tiles && decode(next, tn, nactive)) {
               const int na = tn.a_row + cta_rank * Cfg::kRowsPerCta, nb = tn.b_row + cta_rank * Cfg::kBRowsPerCta;
               for (int k = tn.kb0; k < tn.kb0 + min(tn.nkb, args.prefetch_kb); ++k) {
                 tma_prefetch_2d(&tmA, k * kBKElems, na);
@@ -381,6 +428,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
             tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
             tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
+          } else if constexpr (kCM == 2) {
+            // A: this CTA's rows of its pair's m-tile; B: one 64-row quarter of the n-block's
+            // 256 rows (this CTA's half, the pair's share), multicast to the same-half CTA of
+            // both pairs. Each pair leader's barrier counts what lands in its two CTAs.
+            if (cta_rank == 0) mbar_arrive_expect_tx(&full[s], (active ? 2 * Cfg::kStageA : 0) + 2 * Cfg::kStageB);
+            if (active) tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint, pleader);
+            tma_load_2d_pair_mc(&tmB, &full[s], sB + s * Cfg::kStageB + pair * (Cfg::kStageB / 2), kb * kBKElems,
+                                b_row + pair * (Cfg::kBRowsPerCta / 2), (uint16_t)((1u << cta_rank) | (4u << cta_rank)),
+                                kEvictNormal, pleader);
           } else {
             if (cta_rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
             tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
@@ -401,9 +457,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t aph = 0;
       TileInfo ti;
       for (int i = 0;; ++i) {
-        const int tile = take_tile(i, false);
+        const int tile = take_tile(i, !sched);
         free_tile(i, tile);
-        if (tile >= total_tiles || !decode(tile, ti)) break;
+        bool active;
+        if (tile >= total_tiles || !decode(tile, ti, active)) break;
+        if (kCM == 2 && !active) {  // no m-tile for this pair: release the stages the B multicast filled
+          for (int kb = 0; kb < ti.nkb; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            mma_commit<kCtaGroup>(&empty[s], all_mask);
+            if (++s == S) { s = 0; ph ^= 1; }
+          }
+          continue;
+        }
         mbar_wait(&tempty[acc], aph ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kBN;
@@ -422,11 +488,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const uint64_t koff = static_cast<uint64_t>((k * kStepBytes) >> 4);
             mma_ss<kCtaGroup, kFp8>(d_tmem, adesc + koff, bdesc + koff, idesc, (kb | k) != 0);
           }
-          mma_commit<kCtaGroup>(&empty[s]);
+          mma_commit<kCtaGroup>(&empty[s], kCM == 2 ? all_mask : pair_mask);
           if (++s == S) { s = 0; ph ^= 1; }
         }
         // (an empty k-range commits with no MMA outstanding: the epilogue then writes zeros)
-        mma_commit<kCtaGroup>(&tfull[acc]);
+        mma_commit<kCtaGroup>(&tfull[acc], pair_mask);
         if (++acc == 2) { acc = 0; aph ^= 1; }
       }
     }
@@ -440,10 +506,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t aph = 0;
     TileInfo ti;
     for (int i = 0;; ++i) {
-      const int tile = take_tile(i, kCtaGroup == 2 && cta_rank != 0);
+      const int tile = take_tile(i, !sched);
       __syncwarp();
       if (lane == 0) free_tile(i, tile);
-      if (tile >= total_tiles || !decode(tile, ti)) break;
+      bool active;
+      if (tile >= total_tiles || !decode(tile, ti, active)) break;
+      if (!active) continue;  // (kCM == 2) this pair has no m-tile here
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
       const int row = ti.a_row + cta_rank * Cfg::kRowsPerCta + row_in_cta;
@@ -670,7 +738,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // relaxed: the tcgen05 fence above orders the TMEM reads; the tile's global stores need
         // not be complete before the accumulator is reused
         if constexpr (kCtaGroup == 1) mbar_arrive_relaxed(&tempty[acc]);
-        else mbar_arrive_cluster_relaxed(&tempty[acc], 0);
+        else mbar_arrive_cluster_relaxed(&tempty[acc], pleader);
       }
       if (++acc == 2) { acc = 0; aph ^= 1; }
     }
@@ -679,7 +747,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if constexpr (kEpi == EPI_ROWSCALE)
     if (args.row_ptr && warp >= 4) __threadfence_system();  // peer rows visible before the exchange barrier
   tc_fence_before();
-  if constexpr (kCtaGroup == 2) cluster_sync(); else __syncthreads();
+  if constexpr (kCS > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<kCtaGroup>(tmem_base, 512);
 }

@@ -24,13 +24,13 @@ int m_group_for(int64_t k_bytes, int bm) {
   return static_cast<int>(std::max<int64_t>(1, budget / (k_bytes * bm)));
 }
 
-template <int G, int EPI, bool F8, bool OF8, bool WG = false>
+template <int G, int EPI, bool F8, bool OF8, bool WG = false, int CM = 1>
 void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const GemmArgs& args_in, cudaStream_t st,
                  int grid_sms = 0) {
   if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
   GemmArgs args = args_in;
   args.tile_counter = h->tile_counter;
-  if (!WG && args.m_group == 0) args.m_group = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
+  if (!WG && args.m_group == 0) args.m_group = std::max(1, m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G) / CM);
   if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
   static const int pf_kb = gemm_env("CL_MOE_GEMM_PREFETCH_KB", 0), pf_lead = gemm_env("CL_MOE_GEMM_PREFETCH_LEAD", 12);
   if (!WG) {
@@ -39,18 +39,18 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   }
   CK(cudaMemsetAsync(h->tile_counter, 0, sizeof(int), st));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(((grid_sms > 0 ? std::min(grid_sms, h->num_sms) : h->num_sms) / G) * G);
+  cfg.gridDim = dim3(((grid_sms > 0 ? std::min(grid_sms, h->num_sms) : h->num_sms) / (G * CM)) * (G * CM));
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = GemmCfg<G>::kSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.x = G * CM;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG>, a, b, args));
+  CK(cudaLaunchKernelEx(&cfg, grouped_gemm_kernel<G, EPI, F8, OF8, WG, CM>, a, b, args));
 }
 
 // K1 launch for router input type XT (bf16 storage, or the caller's fp32 tensor): the variant and
@@ -316,7 +316,23 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g2.act_scale = h->sx_mid;
   g2.w_scale = h->ws_out;
   const int v = h->gemm_ctas == 2 ? 1 : 0;
-  if (!fp8) {
+  // clusters of two CTA pairs sharing the B tile by TMA multicast (CL_MOE_GEMM_MC=1)
+  static const bool mc_env = [] {
+    const char* e = std::getenv("CL_MOE_GEMM_MC");
+    return e && e[0] == '1';
+  }();
+  const bool mc = mc_env && v && !h_save && h->g1_grid == 0 && h->num_sms % 4 == 0;
+  if (mc && !fp8) {
+    launch_gemm<2, EPI_SWIGLU, false, false, false, 2>(h, mA1[v], h->mB1m, g1, st);
+    prof_mark(h, 3, st);
+    if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
+    launch_gemm<2, EPI_ROWSCALE, false, false, false, 2>(h, mA2[v], h->mB2m, g2, st);
+  } else if (mc) {
+    launch_gemm<2, EPI_SWIGLU, true, true, false, 2>(h, mA1q[v], h->mB1qm, g1, st);
+    prof_mark(h, 3, st);
+    if (g2_wait) CK(cudaStreamWaitEvent(st, g2_wait, 0));
+    launch_gemm<2, EPI_ROWSCALE, true, false, false, 2>(h, mA2q[v], h->mB2qm, g2, st);
+  } else if (!fp8) {
     if (v) {
       launch_gemm<2, EPI_SWIGLU, false, false>(h, mA1[v], h->mB1[v], g1, st, h->g1_grid);
       prof_mark(h, 3, st);

@@ -229,6 +229,7 @@ struct cl_moe {
 
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
+  CUtensorMap mB1m, mB2m, mB1qm, mB2qm;            // 64-row B boxes (multicast clusters, kCM == 2)
   bool maps_q = false;
 
   // dense decode (host_forward.cuh run_forward): every expert runs all T <= kDenseMaxT tokens so
@@ -364,6 +365,13 @@ void build_maps(cl_moe* h, bool fp8) {
       h->mB2q[v] = make_map(h->wout8, true, h->f, (uint64_t)h->n_local * h->d, brow);
     }
   }
+  if (!fp8) {
+    h->mB1m = make_map(h->win, false, h->d, (uint64_t)h->n_local * 2 * h->f, 64);
+    h->mB2m = make_map(h->wout, false, h->f, (uint64_t)h->n_local * h->d, 64);
+  } else {
+    h->mB1qm = make_map(h->win8, true, h->d, (uint64_t)h->n_local * 2 * h->f, 64);
+    h->mB2qm = make_map(h->wout8, true, h->f, (uint64_t)h->n_local * h->d, 64);
+  }
 }
 
 void init_handle(cl_moe* h, const cl_moe_config* c) {
@@ -493,6 +501,14 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<1, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<1>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_SWIGLU, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
   CK(cudaFuncSetAttribute(grouped_gemm_kernel<2, EPI_ROWSCALE, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+  // clusters of two CTA pairs sharing B by multicast (GemmArgs / kCM == 2)
+  for (const void* fn : {(const void*)grouped_gemm_kernel<2, EPI_SWIGLU, false, false, false, 2>,
+                         (const void*)grouped_gemm_kernel<2, EPI_ROWSCALE, false, false, false, 2>,
+                         (const void*)grouped_gemm_kernel<2, EPI_SWIGLU, true, true, false, 2>,
+                         (const void*)grouped_gemm_kernel<2, EPI_ROWSCALE, true, false, false, 2>}) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<2>::kSmem));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 0));
+  }
 }
 
 }  // namespace

@@ -182,10 +182,10 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar,
       : "memory");
 }
 // 2D tile load for a CTA pair: data lands in this CTA's smem, the byte count completes on the
-// barrier at the same offset in the leader CTA (rank 0) of the pair.
+// barrier at the same offset in the pair's leader CTA (cluster rank `leader`, the even rank).
 __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* m, uint64_t* bar, void* dst,
-                                                 int32_t c0, int32_t c1, uint64_t hint) {
-  const uint32_t leader_bar = mapa(smem_u32(bar), 0);
+                                                 int32_t c0, int32_t c1, uint64_t hint, uint32_t leader = 0) {
+  const uint32_t leader_bar = mapa(smem_u32(bar), leader);
   asm volatile(
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
@@ -197,6 +197,18 @@ __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t c0
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
                "r"(c0), "r"(c1)
                : "memory");
+}
+// 2D tile load of a CTA pair multicast to the CTAs of `mask` (same smem offset in each); each
+// destination's byte count completes on the barrier at `bar`'s offset in that destination's pair
+// leader (the peer bit of the barrier address cleared: cta_group::2 semantics).
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int32_t c0,
+                                                    int32_t c1, uint16_t mask, uint64_t hint, uint32_t leader) {
+  const uint32_t leader_bar = mapa(smem_u32(bar), leader);
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(leader_bar), "r"(c0), "r"(c1), "h"(mask), "l"(hint)
+      : "memory");
 }
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
