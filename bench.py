@@ -194,8 +194,12 @@ def cpu_step(o, inp, w_in, w_out, k, jobs):
 
 
 def pick_cpu_tokens(cfg):
-    # ~45 GFLOP per 64 tokens at the C2 shape; aim for ~5-20 s of CPU work per sample.
+    # ~45 GFLOP per 64 tokens at the C2 shape; aim for ~5-20 s of CPU work per sample. A config
+    # whose whole batch is <= 160 GFLOP (C1: 4096 tokens, 142 GFLOP, ~8-10 s on the box's host
+    # threads) runs in full, as SURVEY.md §8(d) asks for the reference's own CPU shape.
     flop_per_tok = 2 * cfg["K"] * 3 * cfg["d"] * cfg["f"]
+    if cfg["T"] * flop_per_tok <= 160e9:
+        return int(cfg["T"])
     return int(max(8, min(cfg["T"], round(60e9 / flop_per_tok / 8) * 8)))
 
 
