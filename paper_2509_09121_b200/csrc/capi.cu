@@ -81,8 +81,8 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     ep_peer_alloc(h);
     // exchange the IPC handles of x_recv and y over the communicator
     constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
-    constexpr int kB = 5;  // x_recv, y, w_recv, and for training dYbuf, dXsrc
-    void* const own[kB] = {h->x_recv, h->y, h->w_recv, h->dYbuf, h->dXsrc};
+    constexpr int kB = 6;  // x_recv, y, w_recv, for training dYbuf, dXsrc, and the arrival counters
+    void* const own[kB] = {h->x_recv, h->y, h->w_recv, h->dYbuf, h->dXsrc, h->arrive};
     std::vector<uint8_t> mine(kB * kH, 0), all(kB * kH * R);
     for (int b = 0; b < kB; ++b) {
       if (!own[b]) continue;  // not training-capable (d_ff % 256): an all-zero handle
@@ -136,6 +136,7 @@ cl_status cl_moe_ep_peer_init(cl_moe* h) {
     CK(cudaMemcpy(h->peer_x_dev, peer[0].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_y_dev, peer[1].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_w_dev, peer[2].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->peer_a_dev, peer[5].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_dy_dev, peer[3].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->peer_dx_dev, peer[4].data(), sizeof(void*) * R, cudaMemcpyHostToDevice));
     h->ep_transport = 1;
@@ -162,7 +163,7 @@ static void group_check(cl_moe* const* hs, int R) {
 static void group_forward(cl_moe* const* hs, int R, const void* const* hidden, const int64_t* T, void* const* out,
                           cudaStream_t st, bool train) {
   const int N = static_cast<int>(hs[0]->N);
-  std::vector<char*> px(R), py(R), pdy(R), pdx(R);
+  std::vector<char*> px(R), py(R), pdy(R), pdx(R), pa(R);
   std::vector<float*> pw(R);
   for (int r = 0; r < R; ++r) {
     cl_moe* h = hs[r];
@@ -175,6 +176,7 @@ static void group_forward(cl_moe* const* hs, int R, const void* const* hidden, c
     pw[r] = h->w_recv;
     pdy[r] = reinterpret_cast<char*>(h->dYbuf);
     pdx[r] = reinterpret_cast<char*>(h->dXsrc);
+    pa[r] = reinterpret_cast<char*>(h->arrive);
   }
   for (int r = 0; r < R; ++r) {
     CK(cudaMemcpyAsync(hs[r]->peer_x_dev, px.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
@@ -182,6 +184,7 @@ static void group_forward(cl_moe* const* hs, int R, const void* const* hidden, c
     CK(cudaMemcpyAsync(hs[r]->peer_w_dev, pw.data(), sizeof(float*) * R, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(hs[r]->peer_dy_dev, pdy.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(hs[r]->peer_dx_dev, pdx.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(hs[r]->peer_a_dev, pa.data(), sizeof(char*) * R, cudaMemcpyHostToDevice, st));
   }
   for (int r = 0; r < R; ++r) run_router(hs[r], hidden[r], T[r], st);
   for (int r = 0; r < R; ++r)
@@ -779,6 +782,7 @@ cl_status cl_moe_sync(cl_moe* h, void* stream) {
     if (flag) {
       CK(cudaMemset(h->rb.finite_flag, 0, sizeof(int)));
       if (flag & 2) throw RunErr("expert-parallel receive buffer overflow");
+      if (flag & 4) throw RunErr("expert-parallel rows did not arrive within 20 s (a peer rank failed)");
       throw RunErr("non-finite value produced by op 'moe_forward'");
     }
   });

@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __re
                                                              float** expert_dst_w, int32_t* ep_off, void** row_ptr,
                                                              int32_t* flag, char* const* __restrict__ peer_dy,
                                                              char* const* __restrict__ peer_dx, void** expert_dst_dy,
-                                                             void** row_ptr_dx) {
+                                                             void** row_ptr_dx, char* const* __restrict__ peer_a = nullptr,
+                                                             uint32_t** expert_arrive = nullptr,
+                                                             uint32_t* arrive_tgt = nullptr, int K = 1) {
   const int NL = N / R;
   if (blockIdx.x < (unsigned)(NL * R)) {
     const int e = blockIdx.x / R, s = blockIdx.x % R, g = rank * NL + e;
@@ -177,6 +179,22 @@ __global__ void __launch_bounds__(256) ep_peer_layout_kernel(const int32_t* __re
   }
   for (int e = threadIdx.x; e <= NL; e += blockDim.x)
     ep_off[e] = ok ? static_cast<int32_t>(ep_piece_row(C, R, N, rank, e, 0)) : 0;
+  if (peer_a) {  // dispatch overlap: where this rank's pieces are counted, and what this rank awaits
+    for (int g = threadIdx.x; g < N; g += blockDim.x)
+      expert_arrive[g] = ok ? reinterpret_cast<uint32_t*>(peer_a[g / NL]) + g % NL : nullptr;
+    for (int e = threadIdx.x; e < NL && ok; e += blockDim.x) {
+      uint32_t add = 0;
+      for (int s = 0; s < R; ++s) {  // source s writes each row in token_grid(T_s).y column slices
+        int64_t ts = 0;
+        for (int g = 0; g < N; ++g) ts += C[(int64_t)s * N + g];
+        ts /= K;
+        const int64_t blocks = (ts + 7) / 8;
+        const int64_t slices = blocks ? (int64_t)max(1LL, min(8LL, (4LL * kTargetSms + blocks - 1) / blocks)) : 1;
+        add += (uint32_t)(C[(int64_t)s * N + rank * NL + e] * slices);
+      }
+      arrive_tgt[e] += add;
+    }
+  }
 }
 #endif
 

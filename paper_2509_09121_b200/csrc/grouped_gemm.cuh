@@ -62,6 +62,9 @@ struct GemmArgs {
   int64_t group_bytes;      // kWgrad tile order: L2 budget of a resident A group (0 = m fastest)
   int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
                             // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
+  const uint32_t* arrive;       // EP dispatch overlap (row-grouped, nullable): per local expert, pieces of
+  const uint32_t* arrive_tgt;   // rows stored by the sources; the producer waits arrive >= target
+  int32_t* err_flag;            // bit 2: rows did not arrive within the device-side timeout
   int32_t prefetch_kb;      // row-grouped: k-blocks of the NEXT tile prefetched into L2 (0 = off) ...
   int32_t prefetch_lead;    // ... issued this many k-blocks before the end of the current tile, where
                             // the producer also claims the next tile index
@@ -384,10 +387,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // A rows and B rows), so the first stages of the next tile do not wait a DRAM round trip at
       // the tile boundary (where the ring's few stages of slack run out).
       const bool pf = !kWgrad && kCM == 1 && args.prefetch_kb > 0;
+      int ready_e = -1;  // EP overlap: the last expert whose rows were all seen arriving
       int tile = claim(0);
       for (int i = 0;; ++i) {
         bool active, nactive;
         if (tile >= total_tiles || !decode(tile, ti, active)) break;
+        if (!kWgrad && args.arrive && active && ti.e != ready_e) {
+          // the sources' dispatch kernels publish their pieces with system-scope releases; once
+          // all arrived, order the TMA (async-proxy) reads after them
+          const uint64_t t0 = globaltimer_ns();
+          while ((int32_t)(ld_acquire_sys(args.arrive + ti.e) - args.arrive_tgt[ti.e]) < 0) {
+            __nanosleep(256);
+            if (globaltimer_ns() - t0 > 20000000000ull) {  // 20 s: a peer died; fail loudly, do not hang
+              atomicOr(args.err_flag, 4);
+              break;
+            }
+          }
+          fence_proxy_async_global();
+          ready_e = ti.e;
+        }
         const bool half_t = kCtaGroup == 2 && ti.half;
         const int a_row = ti.a_row + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;

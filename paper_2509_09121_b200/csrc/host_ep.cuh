@@ -242,6 +242,19 @@ void ep_peer_alloc(cl_moe* h) {
   }
   h->bar_buf = dalloc<float>(1);
   CK(cudaMemset(h->bar_buf, 0, sizeof(float)));
+  h->arrive = dalloc<uint32_t>(h->n_local);
+  h->arrive_tgt = dalloc<uint32_t>(h->n_local);
+  CK(cudaMemset(h->arrive, 0, sizeof(uint32_t) * h->n_local));
+  CK(cudaMemset(h->arrive_tgt, 0, sizeof(uint32_t) * h->n_local));
+  h->peer_a_dev = dalloc<char*>(R);
+  h->expert_arrive = dalloc<uint32_t*>(h->N);
+}
+
+// Dispatch overlapped with the owners' GEMM1 (CL_MOE_EP_OVERLAP=1, read per call): no barrier
+// between dispatch and GEMM1; the owner's GEMM1 producer waits on per-expert arrival counters.
+bool ep_overlap() {
+  const char* e = std::getenv("CL_MOE_EP_OVERLAP");
+  return e && e[0] == '1';
 }
 
 void ep_peer_layout(cl_moe* h, cudaStream_t st) {
@@ -251,7 +264,9 @@ void ep_peer_layout(cl_moe* h, cudaStream_t st) {
                                                              xrb, h->d * 2, h->peer_x_dev, h->peer_y_dev, h->peer_w_dev,
                                                              h->expert_dst, h->expert_dst_w, h->ep_off_dev, h->row_ptr,
                                                              h->rb.finite_flag, h->peer_dy_dev, h->peer_dx_dev,
-                                                             h->expert_dst_dy, h->row_ptr_dx);
+                                                             h->expert_dst_dy, h->row_ptr_dx,
+                                                             ep_overlap() ? h->peer_a_dev : nullptr, h->expert_arrive,
+                                                             h->arrive_tgt, (int)h->K);
   CK(cudaGetLastError());
 }
 
@@ -261,12 +276,12 @@ void ep_peer_dispatch(cl_moe* h, const void* x, int64_t T, cudaStream_t st) {
     dispatch_kernel<true><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
                                                   (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
                                                   h->xperm, h->perm, h->inv, h->row_w, h->sx_in_all, h->expert_dst,
-                                                  h->expert_dst_w);
+                                                  h->expert_dst_w, ep_overlap() ? h->expert_arrive : nullptr);
   else
     dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, (int)h->N,
                                                    (int)h->K, h->tpc_cur, h->rb, h->rb.topk_idx, h->rb.combine_w,
                                                    h->xperm, h->perm, h->inv, h->row_w, nullptr, h->expert_dst,
-                                                   h->expert_dst_w);
+                                                   h->expert_dst_w, ep_overlap() ? h->expert_arrive : nullptr);
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
 }
@@ -278,8 +293,10 @@ void ep_peer_experts(cl_moe* h, cudaStream_t st, bool train = false) {
     CK(cudaGetLastError());
   }
   // inference: rows return weighted (as on one GPU); training keeps Y unweighted for the backward
+  const bool ov = ep_overlap();
   run_gemms(h, h->ep_off_dev, h->act_recv, h->y_recv, train ? nullptr : h->w_recv, h->mA1e, h->mA2e, h->mA1eq,
-            h->mA2eq, st, train ? h->Hbuf : nullptr, h->row_ptr);
+            h->mA2eq, st, train ? h->Hbuf : nullptr, h->row_ptr, nullptr, ov ? h->arrive : nullptr,
+            ov ? h->arrive_tgt : nullptr);
   prof_mark(h, 4, st);
 }
 
@@ -315,7 +332,9 @@ void run_ep_peer(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   NCK(nc.AllGather(h->rb.counts, h->ep_counts_dev, (size_t)h->N, NcclApi::kInt32, h->comm, st));
   ep_peer_layout(h, st);
   ep_peer_dispatch(h, x, T, st);
-  NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
+  // overlap: no barrier — GEMM1 starts on the local rows while the peers' rows stream in, expert by
+  // expert (its producer waits on the arrival counters the dispatch kernels bump)
+  if (!ep_overlap()) NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
   ep_peer_experts(h, st, train);
   NCK(nc.AllReduce(h->bar_buf, h->bar_buf, 1, NcclApi::kFloat32, NcclApi::kSum, h->comm, st));
   ep_test_stall(st);

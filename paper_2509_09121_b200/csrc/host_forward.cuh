@@ -276,7 +276,8 @@ void plan_from_decision(cl_moe* h, const int32_t* idx, const float* w, int64_t T
 void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, const float* row_w,
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
                cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr,
-               cudaEvent_t g2_wait = nullptr) {
+               cudaEvent_t g2_wait = nullptr, const uint32_t* g1_arrive = nullptr,
+               const uint32_t* g1_arrive_tgt = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
@@ -287,6 +288,9 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
     h->gemm_ctas = rows_per_expert >= 1024 ? 2 : 1;
   }
   g1.n_experts = h->n_local;
+  g1.arrive = g1_arrive;  // EP dispatch overlap: wait for the peers' rows per expert
+  g1.arrive_tgt = g1_arrive_tgt;
+  g1.err_flag = h->rb.finite_flag;
   g1.n_tiles_n = static_cast<int>(2 * h->f / kBN);
   g1.num_kb = static_cast<int>(h->d * (fp8 ? 1 : 2) / kBKBytes);
   g1.b_rows_per_expert = static_cast<int>(2 * h->f);

@@ -199,6 +199,13 @@ struct cl_moe {
   void** row_ptr = nullptr;             // [recv_cap] return address of every received row
   char** peer_dy_dev = nullptr;         // [R] every rank's dYbuf (training: dY rows to the owners)
   char** peer_dx_dev = nullptr;         // [R] every rank's dXsrc (training: dX rows back)
+  // dispatch overlapped with GEMM1 (CL_MOE_EP_OVERLAP=1): arrival counters of this rank's experts
+  // (mapped by the peers), the running targets, every rank's counter array, per global expert the
+  // owner's counter
+  uint32_t* arrive = nullptr;           // [n_local]
+  uint32_t* arrive_tgt = nullptr;       // [n_local]
+  char** peer_a_dev = nullptr;          // [R]
+  uint32_t** expert_arrive = nullptr;   // [N]
   void** expert_dst_dy = nullptr;       // [N] this rank's dY pieces in the owners' dYbuf
   void** row_ptr_dx = nullptr;          // [recv_cap] source address of every received row's dX
   bool ep_group = false;                // member of a single-process EP group (cl_moe_ep_group_*)
@@ -258,7 +265,7 @@ struct cl_moe {
                     (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,
                     (void*)row_ptr, (void*)bar_buf, (void*)peer_dy_dev, (void*)peer_dx_dev, (void*)expert_dst_dy,
-                    (void*)row_ptr_dx, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr, (void*)x16, (void*)sxr_dev, (void*)wrq,
+                    (void*)row_ptr_dx, (void*)arrive, (void*)arrive_tgt, (void*)peer_a_dev, (void*)expert_arrive, (void*)xd, (void*)actd, (void*)yd, (void*)rwd, (void*)invd, (void*)offd, (void*)route_ctr, (void*)x16, (void*)sxr_dev, (void*)wrq,
                     (void*)wsr, (void*)wr64q, (void*)xq8, (void*)cert_w8, (void*)cert_wn,
                     (void*)cert_w8q, (void*)cert_wnq, (void*)cert_count})
       if (p) cudaFree(p);

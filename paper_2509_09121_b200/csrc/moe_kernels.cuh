@@ -1067,6 +1067,21 @@ __global__ void decision_tiles_kernel(const int32_t* __restrict__ idx, int T, in
   if (threadIdx.x == 0) rb.tile_lse2[tile] = 0.0;
 }
 
+constexpr int kMaxArriveExperts = 128;
+// End of a dispatch CTA with arrival counters: every thread has fenced its own peer stores; after
+// the barrier one thread per expert publishes the CTA's piece count with a system-scope release.
+__device__ __forceinline__ void dispatch_arrive_tail(uint32_t* const* expert_arrive, int N, uint32_t* s_arr) {
+  __threadfence_system();
+  __syncthreads();
+  for (int g = threadIdx.x; g < N; g += blockDim.x) {
+    const uint32_t c = s_arr[g];
+    if (c && expert_arrive[g]) {
+      __threadfence_system();
+      red_release_sys_add(expert_arrive[g], c);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K3: fused permute/dispatch ("memcpy elimination"). One warp per token: the
 // token row is read once and written straight into each of its K expert-contiguous rows of the
@@ -1081,12 +1096,24 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
                                                        int32_t* __restrict__ perm, int32_t* __restrict__ inv,
                                                        float* __restrict__ row_w, const float* __restrict__ act_scale,
                                                        void* const* __restrict__ expert_dst = nullptr,
-                                                       float* const* __restrict__ expert_dst_w = nullptr) {
+                                                       float* const* __restrict__ expert_dst_w = nullptr,
+                                                       uint32_t* const* __restrict__ expert_arrive = nullptr) {
   // expert_dst (peer transport, ep.cuh): row r of expert e goes to expert_dst[e] + (r - offsets[e])
   // rows — the owner's receive buffer over NVLink — instead of xperm; null entries (overflow) skip.
+  // expert_arrive (dispatch overlapped with the owners' GEMM1): after its stores the CTA adds the
+  // number of (row, column-slice) pieces it wrote for each expert to the owner's arrival counter
+  // (system-scope release), which the owner's GEMM1 producer acquires before loading the rows.
+  __shared__ uint32_t s_arr[kMaxArriveExperts];
+  if (expert_arrive) {
+    for (int g = threadIdx.x; g < N; g += blockDim.x) s_arr[g] = 0;
+    __syncthreads();
+  }
   const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (j >= T) return;
+  if (j >= T) {
+    if (expert_arrive) dispatch_arrive_tail(expert_arrive, N, s_arr);
+    return;
+  }
   const int tile = j / tpc;
   int rows[8];
   float sc[8];
@@ -1110,6 +1137,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
       perm[r] = static_cast<int32_t>(s);
       row_w[r] = wts[s];
     }
+    if (expert_arrive && lane == 0 && dsts[k]) atomicAdd(&s_arr[e], 1u);
   }
   const int4* src = reinterpret_cast<const int4*>(x + (size_t)j * d);
   // gridDim.y column slices (small batches: more warps in flight than tokens)
@@ -1165,6 +1193,7 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
     }
   }
   if (expert_dst) __threadfence_system();  // peer stores visible before the exchange barrier
+  if (expert_arrive) dispatch_arrive_tail(expert_arrive, N, s_arr);
 }
 
 // ---------------------------------------------------------------------------------------
