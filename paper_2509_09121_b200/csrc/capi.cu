@@ -10,6 +10,7 @@
 // host_train.cuh (training), included below into this one translation unit.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>

@@ -170,6 +170,8 @@ struct cl_moe {
   std::vector<int> prof_kind;          // 0 forward (6 stages), 1 backward (7 stages)
   size_t prof_used = 0;
   std::vector<cudaEvent_t>* cur_ev = nullptr;
+  uint64_t nvtx_id = 0;                // open NVTX stage range (nvtxRangeStartA)
+  int nvtx_kind = 0;
 
   // expert parallelism (ep.cuh)
   NcclApi::Comm comm = nullptr;
@@ -323,8 +325,27 @@ cl_status guarded(cl_moe* h, Fn fn) {
 constexpr int kStages = 6;     // forward: router, plan, dispatch, gemm1, gemm2, combine
 constexpr int kBwdStages = 7;  // backward: combine-bwd, dgrad1, dgrad2, dispatch-bwd, transposes, wgrad-out, wgrad-in
 
+// NVTX: one range per stage of every call (host timeline of the launches; cheap without a tool),
+// named like the profile stages so an Nsight timeline reads like profile_read.
+const char* nvtx_stage_name(int kind, int stage) {
+  static const char* fwd[kStages] = {"moe.router", "moe.plan", "moe.dispatch", "moe.gemm1_swiglu", "moe.gemm2_weight",
+                                     "moe.combine"};
+  static const char* bwd[kBwdStages] = {"moe.bwd.combine", "moe.bwd.dgrad1_swiglu", "moe.bwd.dgrad2",
+                                        "moe.bwd.dispatch", "moe.bwd.transposes", "moe.bwd.wgrad_out",
+                                        "moe.bwd.wgrad_in"};
+  return kind == 1 ? bwd[stage] : fwd[stage];
+}
+void nvtx_next(cl_moe* h, int stage) {  // ends the open range; opens `stage`'s (if any)
+  if (h->nvtx_id) nvtxRangeEnd(h->nvtx_id);
+  h->nvtx_id = 0;
+  if (stage >= 0 && stage < (h->nvtx_kind == 1 ? kBwdStages : kStages))
+    h->nvtx_id = nvtxRangeStartA(nvtx_stage_name(h->nvtx_kind, stage));
+}
+
 void prof_begin(cl_moe* h, cudaStream_t st, int kind = 0) {
   h->cur_ev = nullptr;
+  h->nvtx_kind = kind;
+  nvtx_next(h, 0);
   if (!h->prof) return;
   if (h->prof_used == h->prof_sets.size()) {
     std::vector<cudaEvent_t> v(kBwdStages + 1);
@@ -337,6 +358,7 @@ void prof_begin(cl_moe* h, cudaStream_t st, int kind = 0) {
   CK(cudaEventRecord((*h->cur_ev)[0], st));
 }
 void prof_mark(cl_moe* h, int stage, cudaStream_t st) {
+  nvtx_next(h, stage + 1);
   if (h->cur_ev) CK(cudaEventRecord((*h->cur_ev)[stage + 1], st));
 }
 
