@@ -678,7 +678,7 @@ cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* o
     if (!exec) {
       if (!h->cap_stream) CK(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
       if (dense_ok(h, T)) ensure_dense(h);  // no allocation while capturing
-      cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);
+      if (cert_enabled()) cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);
       const bool prof = h->prof;
       h->prof = false;  // no timing events inside the graph
       CK(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -703,7 +703,8 @@ cl_status cl_moe_forward_graph(cl_moe* h, const void* hidden, int64_t T, void* o
       }
       h->graphs.push_back({hidden, out, T, h->precision, exec});
     }
-    cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);  // weights changed?
+    if (cert_enabled())  // the certified router's fp32 W_r copy follows weight updates
+      cert_prepare(h, h->precision == CL_MOE_FP8_E4M3 && h->router_fp8, (cudaStream_t)stream);
     CK(cudaGraphLaunch(exec, (cudaStream_t)stream));
   });
 }
