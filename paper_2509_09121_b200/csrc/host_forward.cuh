@@ -84,16 +84,7 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
       }
       break;
     case 2:  // big
-      if (big_tok == 64)  // experiment: 64-thread CTAs (CL_MOE_BIG_THREADS=64)
-        router_big_kernel<64, 3, 4, XT><<<n_tiles, 64, RouterBigSmem(N, 64, 3, 4, xb).total, st>>>(x, w64, (int)T, d,
-                                                                                                  N, K, h->rb, xs);
-      else if (big_tok == 128)  // experiment: 128-thread CTAs
-        router_big_kernel<128, 3, 4, XT><<<n_tiles, 128, RouterBigSmem(N, 128, 3, 4, xb).total, st>>>(x, w64, (int)T,
-                                                                                                     d, N, K, h->rb, xs);
-      else if (big_tok == 5)  // experiment: 4-deep ring
-        router_big_kernel<32, 4, 4, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 4, 4, xb).total, st>>>(x, w64, (int)T, d,
-                                                                                                  N, K, h->rb, xs);
-      else if (big_tok == 2)
+      if (big_tok == 2)
         router_big_kernel<32, 3, 2, XT><<<n_tiles, 32, RouterBigSmem(N, 32, 3, 2, xb).total, st>>>(x, w64, (int)T, d,
                                                                                                   N, K, h->rb, xs);
       else
@@ -179,16 +170,9 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
     return e ? std::atoi(e) : 0;
   }();
   const int tiles4 = (int)((T + RouterBigSmem(N, 32, 3, 4).tpc - 1) / RouterBigSmem(N, 32, 3, 4).tpc);
-  static const int big_thr_env = [] {
-    const char* e = std::getenv("CL_MOE_BIG_THREADS");  // experiment: 64 | 128 (4 x 4 per thread), 5 = 4-deep ring
-    return e ? std::atoi(e) : 0;
-  }();
-  int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
-  int big_thr = 32, big_st = 3;
-  if (big_tok == 4 && (big_thr_env == 64 || big_thr_env == 128)) big_thr = big_tok = big_thr_env;
-  if (big_tok == 4 && big_thr_env == 5) big_st = 4, big_tok = 5;
-  const int tpc_big = RouterBigSmem(N, big_thr, big_st, big_tok >= 4 ? 4 : 2).tpc;
-  const bool big_ok = RouterBigSmem(N, big_thr, big_st, big_tok >= 4 ? 4 : 2, xb).total <= 220 * 1024;
+  const int big_tok = big_tok_env == 2 || big_tok_env == 4 ? big_tok_env : (tiles4 >= 3 * h->num_sms ? 4 : 2);
+  const int tpc_big = RouterBigSmem(N, 32, 3, big_tok).tpc;
+  const bool big_ok = RouterBigSmem(N, 32, 3, big_tok, xb).total <= 220 * 1024;
   const bool big = big_ok && (force == 2 || (force == 0 && (T + tpc_big - 1) / tpc_big >= h->num_sms));
   // latency variant: chunk length by expert count (shared-memory budget), ring depth 3
   const int N4r = (N + 3) / 4 * 4;

@@ -469,14 +469,6 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-  for (const void* fn : {(const void*)router_big_kernel<64, 3, 4, __nv_bfloat16>,
-                         (const void*)router_big_kernel<128, 3, 4, __nv_bfloat16>,
-                         (const void*)router_big_kernel<32, 4, 4, __nv_bfloat16>,
-                         (const void*)router_big_kernel<64, 3, 4, float>, (const void*)router_big_kernel<128, 3, 4, float>,
-                         (const void*)router_big_kernel<32, 4, 4, float>, (const void*)router_big_kernel<64, 3, 4, uint8_t>,
-                         (const void*)router_big_kernel<128, 3, 4, uint8_t>,
-                         (const void*)router_big_kernel<32, 4, 4, uint8_t>})
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_lat_kernel<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
