@@ -58,7 +58,8 @@ struct GemmArgs {
   int64_t rp;               // padded-row capacity of aux_t
   const int32_t* poff;      // [n_experts+1] 64-aligned first padded row of each expert
   void* const* row_ptr;     // EPI_ROWSCALE peer transport: destination address of each row (nullable)
-  int32_t m_group;          // row-grouped tile order: m-tiles per group (0 = all), see decode_tile
+  int32_t m_group;          // row-grouped tile order: m-tiles per group (0 = all), see decode_tile;
+                            // kWgrad: the smallest group (the budget may allow more)
   int64_t group_bytes;      // kWgrad tile order: L2 budget of a resident A group (0 = m fastest)
   int32_t half_tail;        // 2-CTA, forward epilogues: an expert's last m-tile with <= 128 rows runs
                             // as an M=128 pair MMA (64 rows per CTA, half the tensor time)
@@ -68,6 +69,7 @@ struct GemmArgs {
   int32_t prefetch_kb;      // row-grouped: k-blocks of the NEXT tile prefetched into L2 (0 = off) ...
   int32_t prefetch_lead;    // ... issued this many k-blocks before the end of the current tile, where
                             // the producer also claims the next tile index
+  uint64_t a_hint, b_hint;  // TMA L2 cache hints of the A / B loads (0 = the kernel's default)
 };
 
 constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
@@ -164,8 +166,9 @@ __device__ __forceinline__ bool decode_tile_mc(int tile, const int* mp_prefix, c
 
 // K-grouped decode (weight gradients): every expert has m_tiles x n_tiles_n tiles; the K range
 // is the expert's padded row range, so its operand slabs grow with its row count. m-tiles go in
-// groups whose A slabs fit `group_bytes` of L2 (m fastest inside, sweeping every n-block), as in
-// decode_tile: a hot expert's A slab is then read once instead of once per n-block.
+// groups whose A slabs fit `group_bytes` of L2 but of at least m_group m-tiles (m fastest inside,
+// sweeping every n-block), as in decode_tile: a hot expert's A slab is then read once per group
+// instead of once per n-block, and its B slabs once per group instead of once per m-tile.
 __device__ __forceinline__ bool decode_tile_wgrad(int tile, const int* s_kb, const GemmArgs& a, int bm, TileInfo& ti) {
   const int per = a.m_tiles * a.n_tiles_n;
   if (tile >= a.n_experts * per) return false;
@@ -175,7 +178,7 @@ __device__ __forceinline__ bool decode_tile_wgrad(int tile, const int* s_kb, con
   int gm = a.m_tiles;
   if (a.group_bytes > 0 && nkb > 0) {
     const int64_t g = a.group_bytes / ((int64_t)bm * nkb * kBKBytes);
-    gm = (int)max((int64_t)1, min((int64_t)a.m_tiles, g));
+    gm = (int)min((int64_t)a.m_tiles, max((int64_t)max(1, a.m_group), g));
   }
   const int g = local / (gm * a.n_tiles_n);
   const int within = local - g * gm * a.n_tiles_n;
@@ -260,7 +263,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kElemBytes = kFp8 ? 1 : 2;
   constexpr int kBKElems = kBKBytes / kElemBytes;
   // Row-grouped: the A rows of an expert are re-read for every n-block -> keep them in L2.
-  constexpr uint64_t kAHint = kWgrad ? kEvictNormal : kEvictLast;
+  const uint64_t kAHint = args.a_hint ? args.a_hint : (kWgrad ? kEvictNormal : kEvictLast);
+  const uint64_t kBHint = args.b_hint ? args.b_hint : kEvictNormal;
 
   extern __shared__ uint8_t smem_raw[];
   // 1024-byte aligned by an offset from the shared array itself, so the compiler keeps the pointer
@@ -437,15 +441,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int c = 0; c < Cfg::kBRowsPerCta / 64; ++c) {
               if constexpr (kCtaGroup == 1)
-                tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64, kEvictNormal);
+                tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64, kBHint);
               else
-                tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64,
-                                 kEvictNormal);
+                tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB + c * 8192, b_row + c * 64, kb * 64, kBHint);
             }
           } else if constexpr (kCtaGroup == 1) {
             mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
             tma_load_2d(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
-            tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
+            tma_load_2d(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kBHint);
           } else if constexpr (kCM == 2) {
             // A: this CTA's rows of its pair's m-tile; B: one 64-row quarter of the n-block's
             // 256 rows (this CTA's half, the pair's share), multicast to the same-half CTA of
@@ -454,11 +457,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             if (active) tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint, pleader);
             tma_load_2d_pair_mc(&tmB, &full[s], sB + s * Cfg::kStageB + pair * (Cfg::kStageB / 2), kb * kBKElems,
                                 b_row + pair * (Cfg::kBRowsPerCta / 2), (uint16_t)((1u << cta_rank) | (4u << cta_rank)),
-                                kEvictNormal, pleader);
+                                kBHint, pleader);
           } else {
             if (cta_rank == 0) mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStageBytes);
             tma_load_2d_pair(&tmA, &full[s], sA + s * Cfg::kStageA, kb * kBKElems, a_row, kAHint);
-            tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kEvictNormal);
+            tma_load_2d_pair(&tmB, &full[s], sB + s * Cfg::kStageB, kb * kBKElems, b_row, kBHint);
           }
           if (++s == S) { s = 0; ph ^= 1; }
         }

@@ -13,7 +13,7 @@ int64_t l2_group_budget() {
   }();
   return budget;
 }
-// Next-tile L2 prefetch of the row-grouped GEMMs (GemmArgs::prefetch_kb / prefetch_lead).
+// Integer tuning knob from the environment (read once by the callers' statics).
 int gemm_env(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -30,8 +30,26 @@ void launch_gemm(cl_moe* h, const CUtensorMap& a, const CUtensorMap& b, const Ge
   if (!h->tile_counter) h->tile_counter = dalloc<int>(1);
   GemmArgs args = args_in;
   args.tile_counter = h->tile_counter;
-  if (!WG && args.m_group == 0) args.m_group = std::max(1, m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G) / CM);
+  // Smallest m-group of the tile orders (row-grouped and weight-gradient). When an expert's A
+  // slabs are too long for the L2 budget (dgrad2's K = 2f, the weight gradients of a hot expert),
+  // the budget alone gives groups of 1-2 m-tiles; with the dynamic scheduler the running tiles'
+  // start times spread over one tile duration, so an L2 line is reused only by tiles claimed
+  // within a few dozen of each other, and the slabs such a window touches (gm A + window/gm B) are
+  // fewest at a few m-tiles per group. Measured on C5 (tools/gemm_dram_sweep.sh, floors 1-16):
+  // dgrad2 DRAM reads 76 -> 55 GB at 4, dW_in 97 -> 41 GB and dW_out 35 -> 24 GB at 6, C5 step
+  // -5 %; a row-grouped floor of 6 slowed C2's GEMM2 (budget 4) by 1 %, so it stays at 4.
+  static const int gm_min = gemm_env("CL_MOE_GEMM_GROUP_MIN", 4), wg_gm_min = gemm_env("CL_MOE_WGRAD_GROUP_MIN", 6);
+  if (!WG && args.m_group == 0) {
+    const int g = m_group_for((int64_t)args.num_kb * kBKBytes, 128 * G);
+    args.m_group = g > 0 ? std::max(1, std::max(g, gm_min) / CM) : 0;
+  }
   if (WG && args.group_bytes == 0) args.group_bytes = l2_group_budget();
+  if (WG) args.m_group = wg_gm_min;
+  // (measurement knobs: L2 hints of the operand loads, 0 = default / 1 normal / 2 last / 3 first)
+  static const uint64_t hints[4] = {0, kEvictNormal, kEvictLast, kEvictFirst};
+  static const int a_hint = gemm_env("CL_MOE_GEMM_A_HINT", 0) & 3, b_hint = gemm_env("CL_MOE_GEMM_B_HINT", 0) & 3;
+  if (!args.a_hint) args.a_hint = hints[a_hint];
+  if (!args.b_hint) args.b_hint = hints[b_hint];
   static const int pf_kb = gemm_env("CL_MOE_GEMM_PREFETCH_KB", 0), pf_lead = gemm_env("CL_MOE_GEMM_PREFETCH_LEAD", 12);
   if (!WG) {
     args.prefetch_kb = pf_kb;

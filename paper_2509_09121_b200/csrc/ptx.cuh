@@ -398,6 +398,13 @@ __device__ __forceinline__ int4 ld_nc_v4(const void* p) {
                : "l"(p));
   return r;
 }
+// 256-bit read-once load (sm_100): no L1 allocation, L2 evict-first so it does not displace the
+// GEMM's operand tiles.
+__device__ __forceinline__ void ld_stream_v8(const void* p, uint32_t* v, uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "l"(p), "l"(pol));
+}
 __device__ __forceinline__ void st_na_v4(void* p, const int4& v) {
   asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)

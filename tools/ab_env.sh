@@ -1,7 +1,7 @@
 #!/bin/bash
 # Same-box A/B of environment settings on the bench (run on the GPU box from the repo root):
 #   tools/ab_env.sh "<bench args>" "<envA>" "<envB>" ... ; each setting runs ROUNDS times, interleaved.
-# Prints one line per run: setting, step ms, per-stage ms (router/dispatch/gemm1/gemm2/combine), SM clock.
+# Prints one line per run: setting, step ms, every per-stage ms the bench reports, SM clock.
 args="$1"; shift
 ROUNDS=${ROUNDS:-2}
 for r in $(seq $ROUNDS); do
@@ -15,8 +15,12 @@ try:
 except Exception:
     print(s, "FAILED", line[:200]); sys.exit()
 st = d["stages"]["ms"]
-print(f"{s:45s} step {d['ms_per_step']:.3f} ms  tok/s {d['value']/1e6:.3f}M  r {st['router']:.3f} d {st['dispatch']:.3f} "
-      f"g1 {st['gemm1']:.3f} g2 {st['gemm2']:.3f} c {st['combine']:.3f}  sm {d['clocks'].get('sm_mhz')} e2e {d['e2e']['value']/1e6:.3f}M")
+short = {"router": "r", "dispatch": "d", "gemm1": "g1", "gemm2": "g2", "combine": "c", "combine_bwd": "cb",
+         "dgrad1_swiglu_bwd": "dg1", "dgrad2": "dg2", "dispatch_bwd": "db", "transposes": "tr",
+         "wgrad_out": "wo", "wgrad_in": "wi"}
+stages = " ".join(f"{short.get(k, k)} {v:.3f}" for k, v in st.items() if k != "plan")
+print(f"{s:45s} step {d['ms_per_step']:.3f} ms  tok/s {d['value']/1e6:.3f}M  {stages}  "
+      f"sm {d['clocks'].get('sm_mhz')} e2e {d['e2e']['value']/1e6:.3f}M")
 PY
   done
 done
