@@ -159,7 +159,7 @@ __global__ void router_bwd_dz_kernel(const float* __restrict__ probs, const floa
   double mx = zr[0];
   for (int i = 1; i < N; ++i) mx = fmax(mx, static_cast<double>(zr[i]));
   double den = 0.0;
-  for (int i = 0; i < N; ++i) den += exp(static_cast<double>(zr[i]) - mx);
+  for (int i = 0; i < N; ++i) den += exp_glibc(static_cast<double>(zr[i]) - mx);
   const double lse = mx + log(den);
   // dp is sparse except for the dense aux term: dot = sum_i dp_i p_i computed on the fly
   double dot = 0.0;

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cuda_fp8.h>
 
+#include "glibc_exp.cuh"
 #include "ptx.cuh"
 
 namespace cmoe {
@@ -125,10 +126,10 @@ __device__ __forceinline__ void router_finish(int tile, int tok0, int tpc, int T
       double mx = zrow[0];
       for (int e = 1; e < N; ++e) mx = fmax(mx, static_cast<double>(zrow[e]));
       double denom = 0.0;
-      for (int e = 0; e < N; ++e) denom += exp(static_cast<double>(zrow[e]) - mx);
+      for (int e = 0; e < N; ++e) denom += exp_glibc(static_cast<double>(zrow[e]) - mx);
       float* p = rb.probs + (size_t)j * N;
       for (int e = 0; e < N; ++e) {
-        const float pe = static_cast<float>(exp(static_cast<double>(zrow[e]) - mx) / denom);
+        const float pe = static_cast<float>(exp_glibc(static_cast<double>(zrow[e]) - mx) / denom);
         p[e] = pe;
         zrow[e] = pe;  // the row now holds probs
       }
@@ -625,7 +626,7 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int e = q * 32 + lane;
-        if (q * 32 < N && e < N) ex[q] = exp(static_cast<double>(zrow[e]) - mx);
+        if (q * 32 < N && e < N) ex[q] = exp_glibc(static_cast<double>(zrow[e]) - mx);
       }
       // ascending-e sum: every lane adds the same shuffled terms in the same order
       double denom = 0.0;

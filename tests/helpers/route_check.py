@@ -36,7 +36,9 @@ def main(t, d, n, k, mode="random", dtype="bf16"):
         ref = Oracle("port").route(inp["x"], inp["w_router"], k)
     ok = (np.array_equal(dec.logits.cpu().numpy(), ref["logits"]) and
           np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), ref["topk_idx"]) and
-          np.array_equal(dec.counts.cpu().numpy(), ref["counts"]))
+          np.array_equal(dec.counts.cpu().numpy(), ref["counts"]) and
+          np.array_equal(dec.probs.cpu().numpy(), ref["probs"]) and
+          np.array_equal(dec.combine_weights.cpu().numpy(), ref["combine_weights"]))
     print("ok" if ok else "MISMATCH")
     return 0 if ok else 1
 

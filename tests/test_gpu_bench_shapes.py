@@ -1,7 +1,7 @@
 """GPU parity at the shapes bench.py measures (BASELINE.json configs[1..4] = C2..C5), through the C ABI.
 
 Every case runs the whole layer on the device at the benchmarked shape and checks:
-  * routing for ALL tokens bit-exact against the oracle (logits, top-K, counts; the oracle's router is
+  * routing for ALL tokens bit-exact against the oracle (logits, probs, top-K, weights, counts; the oracle's router is
     cheap on CPU) and the dispatch permutation / expert offsets bit-exact (oracle plan);
   * a sample of output rows against the oracle's per-token compute (orc_expert_ffn per expert, fp64
     accumulation), tolerance as tests/test_gpu_parity.py: rel-F <= 1e-2, max <= 3e-2 max|y| (bf16);
@@ -46,6 +46,8 @@ def _check_routing(o, lay, x, dec, k, n):
     assert np.array_equal(dec.logits.cpu().numpy(), ref["logits"])
     assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), ref["topk_idx"])
     assert np.array_equal(dec.counts.cpu().numpy(), ref["counts"])
+    assert np.array_equal(dec.probs.cpu().numpy(), ref["probs"])
+    assert np.array_equal(dec.combine_weights.cpu().numpy(), ref["combine_weights"])
     t = x.shape[0]
     offsets, perm, _ = o.plan(ref["topk_idx"], n)
     assert np.array_equal(lay.stage("offsets", (n + 1,), torch.int32).cpu().numpy(), offsets)
@@ -176,6 +178,7 @@ def test_fp8_decode_at_c2_layer_shape():
         rq, _ = router_fp8_sim(o, x, wr, k, s_r)
         assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"]), T
         assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"]), T
+        assert np.array_equal(dec.combine_weights.cpu().numpy(), rq["combine_weights"]), T
         rows = np.arange(T) if T <= 64 else _sample(rq["topk_idx"], n, per_expert=3, extra=16)
         cases.append((T, x, rq, rows, _host(out)[rows]))
     want = {T: np.zeros((len(rows), d), np.float64) for T, _, _, rows, _ in cases}

@@ -60,6 +60,8 @@ def test_fp8_layer_vs_qdq_oracle(gemm_ctas):
     assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"])
     assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"])
     assert np.array_equal(dec.counts.cpu().numpy(), rq["counts"])
+    assert np.array_equal(dec.probs.cpu().numpy(), rq["probs"])
+    assert np.array_equal(dec.combine_weights.cpu().numpy(), rq["combine_weights"])
     o32 = out.float().cpu().numpy().astype(np.float64)
     rel = np.linalg.norm(o32 - ref_out) / np.linalg.norm(ref_out)
     assert rel <= 2e-2, rel
