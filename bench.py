@@ -232,6 +232,21 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------------------------------
+def count_our_launches(step, sync):
+    """Kernels of this library launched by one step, counted by the CUDA profiler (CUPTI, through
+    torch.profiler) on one extra untimed step: kernels in the `cmoe` namespace. None when the
+    profiler is unavailable."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            sync()
+        n = sum(ev.count for ev in prof.key_averages() if "cmoe::" in ev.key)
+        return n if n > 0 else None
+    except Exception:  # noqa: BLE001 — the count is diagnostic; the timed run does not depend on it
+        return None
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -397,6 +412,9 @@ def run_ours(args, cfg):
         e2e_s = float(t.item())
     e2e_val = world * T * e2e_steps / e2e_s
 
+    # ---- our kernel launches per step, counted (CUPTI) on one extra untimed step ----
+    per_step_launches = count_our_launches(step, layer.sync)
+
     # ---- NVLink exchange accounting (N > 1): exact rows this rank sent to other ranks ----
     a2a = None
     if world > 1:
@@ -490,10 +508,13 @@ def run_ours(args, cfg):
                              "d_hidden, every step (copies double-buffered on two copy streams)" if train else
                              "host wall clock around `steps` pipelined cl_moe_forward_host_async calls (H2D of x "
                              "and D2H of out every call) + cl_moe_host_wait")),
-            # ours per step: router, plan, dispatch, GEMM1, GEMM2, combine (+ the EP peer layout
-            # kernel); training adds pad-plan and combine-bwd, dgrad x2, dispatch-bwd, transposes x2,
-            # zero-pad x2, wgrad x2 (NCCL kernels are not counted)
-            gpu_launches=((17 if train else 6) + (1 if (world > 1 and "peer" in transport) else 0)) * args.steps,
+            # ours per step, counted by CUPTI on an extra step (fallback: router, plan, dispatch,
+            # GEMM1, GEMM2, combine (+ the EP peer layout kernel); training adds pad-plan and
+            # combine-bwd, dgrad x2, dispatch-bwd, transposes x2, zero-pad x2, wgrad x2)
+            gpu_launches=(per_step_launches if per_step_launches else
+                          (17 if train else 6) + (1 if (world > 1 and "peer" in transport) else 0)) * args.steps,
+            gpu_launches_source="counted (torch.profiler / CUPTI, kernels in namespace cmoe, one extra step)"
+            if per_step_launches else "static per-step count",
             clocks=clocks,
         )
         if world > 1 and a2a is not None:

@@ -80,6 +80,29 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
   constexpr int xb = sizeof(XT);
   const int d = (int)h->d, K = (int)h->K;
   switch (variant) {
+    case 5: {  // dmma (fp64 tensor cores): ws_cons carries the warps per CTA (2 or 4; 8 tokens
+               // each); w64 points at the [d][N4] layout, the fragments follow. Then the finish.
+      const double* wf = w64 + router_wfrag_offset(d, N);
+      const size_t smem = RouterDmmaSmem(N, ws_cons, xb).total;
+      const int nt = dmma_n8(N) / 8;
+#define CL_MOE_DMMA_LAUNCH(NT, W) \
+  router_dmma_kernel<NT, W, XT><<<dm_tiles, W * 32, smem, st>>>(x, wf, (int)T, d, N, h->rb, xs)
+      const int dm_tiles = static_cast<int>((T + ws_cons * 8 - 1) / (ws_cons * 8));
+      if (ws_cons == 4) {
+        if (nt == 1) CL_MOE_DMMA_LAUNCH(1, 4);
+        else if (nt == 2) CL_MOE_DMMA_LAUNCH(2, 4);
+        else CL_MOE_DMMA_LAUNCH(4, 4);
+      } else {
+        if (nt == 1) CL_MOE_DMMA_LAUNCH(1, 2);
+        else if (nt == 2) CL_MOE_DMMA_LAUNCH(2, 2);
+        else CL_MOE_DMMA_LAUNCH(4, 2);
+      }
+#undef CL_MOE_DMMA_LAUNCH
+      CK(cudaGetLastError());
+      router_finish_kernel<<<n_tiles, kFinishTpc * 32, router_finish_smem(N, kFinishTpc), st>>>((int)T, N, K,
+                                                                                            kFinishTpc, h->rb);
+      break;
+    }
     case 4:  // ws
       if (ws_cons == 32)
         router_ws_kernel<32, XT><<<n_tiles, 32 + 64, RouterWsSmem(N, 32, xb).total, st>>>(x, w64, (int)T, d, N, K,
@@ -178,8 +201,8 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   // large batches: 4 tokens x 4 experts per thread (shared-memory traffic per DFMA / 3).
   // decode-size batches: one thread per (token, expert) chain (latency-bound: parallelism first).
   static const int force = [] {
-    const char* e = std::getenv("CL_MOE_ROUTER");  // bring-up / test override: "ws", "lat", "small" or "big"
-    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : e[0] == 'w' ? 4 : 0) : 0;
+    const char* e = std::getenv("CL_MOE_ROUTER");  // test override: "ws", "lat", "small", "big" or "dmma"
+    return e ? (e[0] == 'b' ? 2 : e[0] == 's' ? 1 : e[0] == 'l' ? 3 : e[0] == 'w' ? 4 : e[0] == 'd' ? 5 : 0) : 0;
   }();
   // large batches: 4 tokens x 4 experts per thread when that still gives >= 3 CTAs per SM, else
   // 2 x 4 (2x the CTAs, e.g. C3's 8192 tokens); CL_MOE_BIG_TOK=2|4 pins the choice (benchmarks)
@@ -213,10 +236,19 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   float* rwd = fuse ? h->rwd : nullptr;
   int32_t* invd = fuse ? h->invd : nullptr;
   const bool small = !big && !lat && !ws && router_smem_bytes(N, 32, 8, xb) <= 220 * 1024;
-  const int tpc = big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
-                                 : router_tokens_per_cta(N, small ? 32 : 128);
-  const int variant = ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
+  // batches beyond the decode sizes: the fp64 tensor-core router (router_dmma_kernel), when the
+  // device check passed and the experts fit its instantiations (N <= 32)
+  const int nt8 = dmma_n8(N) / 8;
+  // 4 warps (32 tokens) per CTA when that still leaves >= 2 CTAs per SM, else 2 (16 tokens)
+  const int dmma_g = (T + 31) / 32 >= 2 * h->num_sms ? 4 : 2;
+  const bool dmma_fit = h->dmma_ok && (nt8 == 1 || nt8 == 2 || nt8 == 4) &&
+                        RouterDmmaSmem(N, dmma_g, xb).total <= 220 * 1024;
+  // (the opt-in certified router takes precedence when enabled)
   const bool cert = big && !h->need_exact && !dense && N <= 32 && cert_enabled() && force == 0;
+  const bool dmma = dmma_fit && !cert && (force == 5 || (force == 0 && !lat_size && !dense));
+  const int tpc = dmma ? kFinishTpc : big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
+                                 : router_tokens_per_cta(N, small ? 32 : 128);
+  const int variant = dmma ? 5 : ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
   const int tpc_eff = cert ? cert_tpc(N, xb) : tpc;
   h->tpc_cur = tpc_eff;
   h->last_tokens = T;
@@ -235,17 +267,17 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
     if (cert)
       launch_router_cert<uint8_t>(h, h->xq8, h->sxr_dev, true, T, st);
     else
-      launch_router<uint8_t>(h, h->xq8, h->wr64q, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail, rwd, invd,
+      launch_router<uint8_t>(h, h->xq8, h->wr64q, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok, lat_chunk, tail, rwd, invd,
                              st, h->sxr_dev);
   } else if (cert && xf32) {
     launch_router_cert<float>(h, static_cast<const float*>(x), nullptr, false, T, st);
   } else if (cert) {
     launch_router_cert<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), nullptr, false, T, st);
   } else if (xf32)
-    launch_router<float>(h, static_cast<const float*>(x), h->wr64, T, N, n_tiles, variant, ws_cons, big_tok, lat_chunk, tail,
+    launch_router<float>(h, static_cast<const float*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok, lat_chunk, tail,
                          rwd, invd, st);
   else
-    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), h->wr64, T, N, n_tiles, variant, ws_cons, big_tok,
+    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok,
                                  lat_chunk, tail, rwd, invd, st);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
@@ -518,7 +550,7 @@ void ensure_fp8_storage(cl_moe* h) {
     h->sxr_dev = dalloc<float>(1);
     h->wrq = dalloc<float>(h->d * h->N);
     h->wsr = dalloc<float>(h->N);
-    h->wr64q = dalloc<double>(3 * h->d * ((h->N + 3) / 4 * 4));
+    h->wr64q = dalloc<double>(router_w64_size((int)h->d, (int)h->N));
     h->xq8 = dalloc<uint8_t>(h->cap * h->d);
   }
   if (h->win8) return;

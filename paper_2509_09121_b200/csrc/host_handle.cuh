@@ -162,6 +162,7 @@ struct cl_moe {
   int64_t last_rows = 0;
   bool last_dense = false;  // the last forward took the dense-decode path (stage view = dense buffers)
   int tpc_cur = 32;                    // router tile (tokens) of the last routing call
+  bool dmma_ok = false;                // the fp64 tensor-core router passed its device check (init)
   int64_t last_tokens = 0;             // T of the current call
 
   // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call
@@ -464,7 +465,29 @@ void init_handle(cl_moe* h, const cl_moe_config* c) {
   h->row_w = dalloc<float>(rows);
 
   h->wr = dalloc<float>(h->d * h->N);
-  h->wr64 = dalloc<double>(3 * h->d * ((h->N + 3) / 4 * 4));  // [d][N4] + the router_ws layout (<= 2x)
+  // [d][N4], the router_ws layout, the router_dmma fragment layout (widen_router_kernel)
+  h->wr64 = dalloc<double>(router_w64_size((int)h->d, (int)h->N));
+  for (const void* fn : {(const void*)router_dmma_kernel<1, 2>, (const void*)router_dmma_kernel<2, 2>,
+                         (const void*)router_dmma_kernel<4, 2>, (const void*)router_dmma_kernel<1, 4>,
+                         (const void*)router_dmma_kernel<2, 4>, (const void*)router_dmma_kernel<4, 4>,
+                         (const void*)router_dmma_kernel<1, 2, float>, (const void*)router_dmma_kernel<2, 2, float>,
+                         (const void*)router_dmma_kernel<4, 2, float>, (const void*)router_dmma_kernel<1, 4, float>,
+                         (const void*)router_dmma_kernel<2, 4, float>, (const void*)router_dmma_kernel<4, 4, float>,
+                         (const void*)router_dmma_kernel<1, 2, uint8_t>, (const void*)router_dmma_kernel<2, 2, uint8_t>,
+                         (const void*)router_dmma_kernel<4, 2, uint8_t>, (const void*)router_dmma_kernel<1, 4, uint8_t>,
+                         (const void*)router_dmma_kernel<2, 4, uint8_t>, (const void*)router_dmma_kernel<4, 4, uint8_t>})
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+  {  // the DMMA router is used only if the instruction accumulates as the sequential chain here
+    unsigned long long* bad = dalloc<unsigned long long>(1);
+    CK(cudaMemset(bad, 0, sizeof(unsigned long long)));
+    dmma_selftest_kernel<<<h->num_sms, 256>>>(64, bad);
+    CK(cudaGetLastError());
+    unsigned long long nb = 1;
+    CK(cudaMemcpy(&nb, bad, sizeof(nb), cudaMemcpyDeviceToHost));
+    CK(cudaFree(bad));
+    const char* e = std::getenv("CL_MOE_ROUTER_DMMA");  // "0": keep the DFMA variants (A/B)
+    h->dmma_ok = nb == 0 && !(e && e[0] == '0');
+  }
   CK(cudaFuncSetAttribute(router_kernel<128, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_kernel<32, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
   CK(cudaFuncSetAttribute(router_big_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

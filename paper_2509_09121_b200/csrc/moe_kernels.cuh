@@ -97,7 +97,7 @@ __host__ __device__ inline int router_ws_chunk(int N4) { return N4 <= 16 ? 256 :
 // doubles per row so a warp's experts hit distinct banks) — one contiguous bulk copy per ring
 // slot. Once per weight update.
 __global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, double* __restrict__ out) {
-  const int N4 = (N + 3) / 4 * 4;
+  const int N4 = (N + 3) / 4 * 4, N8 = (N + 7) / 8 * 8;
   const int chunk = router_ws_chunk(N4), pitch = chunk + 2;
   double* wt = out + (size_t)d * N4;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * N4; i += gridDim.x * blockDim.x) {
@@ -108,6 +108,14 @@ __global__ void widen_router_kernel(const float* __restrict__ wr, int d, int N, 
     double* row = wt + ((size_t)c * N4 + e) * pitch;
     row[j] = v;
     if (j == 0) row[chunk] = row[chunk + 1] = 0.0;
+  }
+  // router_dmma_kernel's B fragments: [d/4][N8/8][32], lane = (e % 8) * 4 + l % 4
+  // (router_wfrag_offset: after the two layouts above)
+  const size_t foff = (size_t)d * N4 + (size_t)(d / chunk) * N4 * pitch;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * N8; i += gridDim.x * blockDim.x) {
+    const int l = i / N8, e = i % N8;
+    const double v = e < N ? static_cast<double>(wr[(size_t)l * N + e]) : 0.0;
+    out[foff + ((size_t)(l / 4) * (N8 / 8) + e / 8) * 32 + (e % 8) * 4 + l % 4] = v;
   }
 }
 
@@ -718,16 +726,31 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
     if (lane == 0) slse[tl] = lse2;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+  // tile statistics, one warp per expert over 32-token slices: a token's rank among the tile's
+  // tokens routed to e is the popcount of the earlier lanes' ballot (each token picks e at most
+  // once); the prob sum adds the tokens in ascending order, as router_finish
+  for (int e = warp; e < N; e += nwarps) {
     int cnt = 0;
     double ps = 0.0;
-    for (int t = 0; t < ntok; ++t) {
-      ps += static_cast<double>(slog[t * N4 + e]);
-      for (int k = 0; k < K; ++k)
-        if (sidx[t * 8 + k] == e) rb.local_rank[(size_t)(tok0 + t) * K + k] = cnt++;
+    for (int t0 = 0; t0 < ntok; t0 += 32) {
+      const int t = t0 + lane;
+      int kk = -1;
+      double p = 0.0;
+      if (t < ntok) {
+        for (int k = 0; k < K; ++k)
+          if (sidx[t * 8 + k] == e) kk = k;
+        p = static_cast<double>(slog[t * N4 + e]);
+      }
+      const unsigned m = __ballot_sync(kAll, kk >= 0);
+      if (kk >= 0) rb.local_rank[(size_t)(tok0 + t) * K + kk] = cnt + __popc(m & ((1u << lane) - 1u));
+      cnt += __popc(m);
+      const int n = min(32, ntok - t0);
+      for (int i = 0; i < n; ++i) ps += __shfl_sync(kAll, p, i);
     }
-    rb.tile_cnt[(size_t)tile * N + e] = cnt;
-    rb.tile_psum[(size_t)tile * N + e] = ps;
+    if (lane == 0) {
+      rb.tile_cnt[(size_t)tile * N + e] = cnt;
+      rb.tile_psum[(size_t)tile * N + e] = ps;
+    }
   }
   if (threadIdx.x == 0) {
     double a = 0.0;
@@ -1042,6 +1065,191 @@ __global__ void __launch_bounds__(kThreads, 1) router_big_kernel(const XT* __res
 // K2: dispatch plan. Exclusive scan of the per-tile expert counts (tile-major within each
 // expert) -> each tile's base row inside its expert segment; expert offsets; agg_prob, aux-loss
 // and Z-loss reductions in a fixed order. One CTA; deterministic (no atomics).
+// ---------------------------------------------------------------------------------------
+// K1, fp64 tensor-core variant (large and mid-size batches). DMMA (mma.sync.m8n8k4.f64) computes
+// D = C + A B over k = 0..3 as the sequential FMA chain fma(a3,b3, fma(a2,b2, fma(a1,b1,
+// fma(a0,b0,c)))) — measured on this B200 (tools/dmma_probe.cu): bit-identical to the ascending-k
+// chain on 1.5e9 outputs of bf16 x fp32 operands with a 2^40 exponent spread, where the
+// descending chain or products-summed-first differ on 12-15 % of them. One DMMA is therefore four
+// steps of the reference's ascending-l chain (tensor.cpp:157-173) for an 8-token x 8-expert block,
+// with the accumulator carried across k-steps in registers: logits stay bit-identical by
+// construction of the instruction's arithmetic, 256 FMAs per warp instruction instead of 32. The
+// handle checks the instruction on the device before first use (dmma_selftest_kernel) and keeps
+// the DFMA variants otherwise.
+//   Warp: one 8-token tile x every 8-expert tile (kNT accumulator chains; C fragment: lane
+//   holds C[lane/4][2(lane%4) + {0,1}]), so each x value is widened once per warp and feeds kNT
+//   DMMAs. A DMMA occupies its sub-partition's FP64 pipe for 16 cycles and has a 26-cycle
+//   dependent latency (tools/dmma_probe.cu), so CTAs are small (kW warps) and many. A fragment
+//   (x, one value per lane: row lane/4, k = lane%4) is read from a row-padded smem copy of the x
+//   chunk (rows 16 B apart in banks: conflict-free) and widened in registers; B fragments (W_r)
+//   come pre-arranged in fragment order (widen_router_kernel's third layout: [d/4][N8/8][32]
+//   fp64), one 8-byte load per lane. x and W chunks of kDmmaChunk steps stream through a
+//   cp.async ring. The kernel writes logits only: the per-token softmax / top-K / tile statistics
+//   run in router_finish_kernel with one warp per token (inside this kernel they would be a
+//   serial tail of every CTA, ~30 us at C2).
+constexpr int kDmmaChunk = 64;
+constexpr int kDmmaStages = 4;
+__host__ __device__ inline int dmma_n8(int N) { return (N + 7) / 8 * 8; }
+// W_r fragment layout: after the [d][N4] copy and the router_ws layout inside the wr64 buffer
+__host__ __device__ inline size_t router_wfrag_offset(int d, int N) {
+  const int N4 = (N + 3) / 4 * 4, chunk = router_ws_chunk(N4);
+  return (size_t)d * N4 + (size_t)(d / chunk) * N4 * (chunk + 2);
+}
+__host__ __device__ inline size_t router_w64_size(int d, int N) {  // doubles of the whole wr64 buffer
+  return router_wfrag_offset(d, N) + (size_t)d * dmma_n8(N);
+}
+struct RouterDmmaSmem {
+  int tpc, NT, xpitch;
+  size_t sx, sw, total;
+  __host__ __device__ RouterDmmaSmem(int n_experts, int warps, int xb) {
+    NT = dmma_n8(n_experts) / 8;
+    tpc = warps * 8;
+    xpitch = kDmmaChunk * xb + 16;  // bytes per token row; +16: consecutive rows 4 banks apart
+    sx = 0;                                                              // [stages][tpc][xpitch]
+    sw = sx + (size_t)kDmmaStages * tpc * xpitch;                        // [stages][chunk/4][NT][32]
+    total = sw + (size_t)kDmmaStages * (kDmmaChunk / 4) * NT * 32 * 8;
+  }
+};
+
+__device__ __forceinline__ void dmma_f64(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int kNT, int kW, typename XT = __nv_bfloat16>
+__global__ void __launch_bounds__(kW * 32) router_dmma_kernel(const XT* __restrict__ x,
+                                                            const double* __restrict__ wfrag, int T, int d, int N,
+                                                            RouteBufs rb, const float* __restrict__ xscale = nullptr) {
+  constexpr int kXB = sizeof(XT), kThreads = kW * 32;
+  const float xsc = router_xscale(xscale);
+  const RouterDmmaSmem L(N, kW, kXB);
+  const int tpc = L.tpc, xpitch = L.xpitch;
+  const int tok0 = blockIdx.x * tpc;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* sx = smem_raw + L.sx;
+  double* sw = reinterpret_cast<double*>(smem_raw + L.sw);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  const int nchunks = d / kDmmaChunk;
+  constexpr int kRowPieces = kDmmaChunk * kXB / 16;          // 16-byte pieces of one token's x chunk
+  constexpr int kWPieces = (kDmmaChunk / 4) * kNT * 32 / 2;  // 16-byte pieces of one W chunk
+  auto issue = [&](int c, int buf) {
+    const int c0 = c * kDmmaChunk;
+    uint8_t* xdst = sx + (size_t)buf * tpc * xpitch;
+    for (int i = threadIdx.x; i < tpc * kRowPieces; i += kThreads) {
+      const int r = i / kRowPieces, q = i % kRowPieces;
+      const bool ok = tok0 + r < T;
+      const XT* src = x + (size_t)(ok ? tok0 + r : 0) * d + c0 + q * (16 / kXB);
+      cp_async16(xdst + r * xpitch + q * 16, src, ok);
+    }
+    const double* wsrc = wfrag + (size_t)(c0 / 4) * kNT * 32;
+    double* wdst = sw + (size_t)buf * (kDmmaChunk / 4) * kNT * 32;
+    for (int i = threadIdx.x; i < kWPieces; i += kThreads) cp_async16(wdst + 2 * i, wsrc + 2 * i, true);
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int c = 0; c < kDmmaStages - 1; ++c) {
+    if (c < nchunks) issue(c, c);
+    else cp_async_commit();
+  }
+  double acc[kNT][2];
+#pragma unroll
+  for (int g = 0; g < kNT; ++g) acc[g][0] = acc[g][1] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c % kDmmaStages;
+    cp_async_wait<kDmmaStages - 2>();
+    __syncthreads();
+    if (c + kDmmaStages - 1 < nchunks) issue(c + kDmmaStages - 1, (c + kDmmaStages - 1) % kDmmaStages);
+    else cp_async_commit();
+    const uint8_t* xs = sx + (size_t)buf * tpc * xpitch + (size_t)(warp * 8 + lane / 4) * xpitch + (lane % 4) * kXB;
+    const double* ws = sw + (size_t)buf * (kDmmaChunk / 4) * kNT * 32 + lane;
+#pragma unroll 8
+    for (int j = 0; j < kDmmaChunk / 4; ++j) {
+      const double a = x_to_f64<XT>(*reinterpret_cast<const XT*>(xs + j * 4 * kXB), xsc);
+#pragma unroll
+      for (int g = 0; g < kNT; ++g) dmma_f64(acc[g][0], acc[g][1], a, ws[(j * kNT + g) * 32]);
+    }
+  }
+  // logits: C fragment row lane/4 of this warp's token tile, columns 2(lane%4) + {0,1} of tile g
+  const int tok = tok0 + warp * 8 + lane / 4;
+  if (tok < T) {
+#pragma unroll
+    for (int g = 0; g < kNT; ++g)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = g * 8 + 2 * (lane % 4) + h;
+        if (e < N) {
+          const float z = static_cast<float>(acc[g][h]);
+          rb.logits[(size_t)tok * N + e] = z;
+          if (!isfinite(z)) atomicOr(rb.finite_flag, 1);
+        }
+      }
+  }
+}
+
+// Softmax / top-K / combine weights / tile statistics of router tiles whose logits are already in
+// rb.logits (router_dmma_kernel): one CTA per tile of tpc <= 32 tokens, one warp per token.
+constexpr int kFinishTpc = 16;  // tokens per finish tile (the plan's router tile on this path)
+__global__ void __launch_bounds__(kFinishTpc * 32) router_finish_kernel(int T, int N, int K, int tpc, RouteBufs rb) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const int N4 = (N + 3) / 4 * 4;
+  float* slog = reinterpret_cast<float*>(smem_raw);                                  // [tpc][N4]
+  int* sidx = reinterpret_cast<int*>(smem_raw + sizeof(float) * tpc * N4);          // [tpc][8]
+  double* slse = reinterpret_cast<double*>(smem_raw + ((sizeof(float) * tpc * N4 + sizeof(int) * tpc * 8 + 7) / 8 * 8));
+  const int tok0 = blockIdx.x * tpc;
+  const int ntok = min(tpc, T - tok0);
+  for (int i = threadIdx.x; i < tpc * N4; i += blockDim.x) {
+    const int t = i / N4, e = i % N4;
+    slog[i] = (t < ntok && e < N) ? rb.logits[(size_t)(tok0 + t) * N + e] : 0.0f;
+  }
+  __syncthreads();
+  router_finish_warps(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
+}
+__host__ __device__ inline size_t router_finish_smem(int N, int tpc) {
+  const int N4 = (N + 3) / 4 * 4;
+  return (sizeof(float) * tpc * N4 + sizeof(int) * tpc * 8 + 7) / 8 * 8 + sizeof(double) * tpc;
+}
+
+// Device check of the DMMA accumulation order, run once per handle before router_dmma_kernel is
+// used: random bf16 x fp32 operands (exponents over 2^+-20) through one m8n8k4 DMMA per trial vs
+// the sequential FMA chain; *bad counts mismatching outputs.
+__global__ void dmma_selftest_kernel(int trials, unsigned long long* bad) {
+  const int lane = threadIdx.x % 32;
+  unsigned long long nb = 0;
+  uint64_t st = 0x243f6a8885a308d3ull ^ ((uint64_t)(blockIdx.x * blockDim.x + threadIdx.x - lane) << 17);
+  auto next = [&]() {
+    st += 0x9e3779b97f4a7c15ull;
+    uint64_t z = st;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  for (int it = 0; it < trials; ++it) {
+    const uint64_t ra = next(), rb = next(), rc = next(), rd = next();
+    // per-lane values from the warp-common stream, mixed with the lane id
+    const uint64_t ua = ra * (2 * lane + 1) + (rb >> 7), ub = rb * (2 * lane + 3) + (rc >> 9);
+    const uint64_t uc = rc * (2 * lane + 5) + (rd >> 5), ud = rd * (2 * lane + 7) + (ra >> 3);
+    const float fa = ldexpf(1.0f + (float)((ua >> 8) & 0xff) / 256.0f, (int)(ua % 41) - 20) * ((ua >> 40) & 1 ? -1.f : 1.f);
+    const double a = static_cast<double>(__uint_as_float(__float_as_uint(fa) & 0xffff0000u));  // bf16 value
+    const double b = static_cast<double>(ldexpf(1.0f + (float)((ub >> 8) & 0xffffff) / 16777216.0f,
+                                                (int)(ub % 41) - 20) * ((ub >> 40) & 1 ? -1.f : 1.f));
+    double c0 = static_cast<double>(ldexpf(1.0f + (float)((uc >> 8) & 0xffffff) / 16777216.0f, (int)(uc % 41) - 20));
+    double c1 = -static_cast<double>(ldexpf(1.0f + (float)((ud >> 8) & 0xffffff) / 16777216.0f, (int)(ud % 41) - 20));
+    double s0 = c0, s1 = c1;
+    const int row = lane / 4, col = 2 * (lane % 4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double ak = __shfl_sync(0xffffffffu, a, row * 4 + k);
+      s0 = __fma_rn(ak, __shfl_sync(0xffffffffu, b, col * 4 + k), s0);
+      s1 = __fma_rn(ak, __shfl_sync(0xffffffffu, b, (col + 1) * 4 + k), s1);
+    }
+    dmma_f64(c0, c1, a, b);
+    nb += (__double_as_longlong(c0) != __double_as_longlong(s0)) + (__double_as_longlong(c1) != __double_as_longlong(s1));
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 template <int kThreads>
 __global__ void __launch_bounds__(kThreads) plan_kernel(int n_tiles, int T, int N, int K, RouteBufs rb) {
   plan_body<kThreads>(n_tiles, T, N, K, rb);

@@ -32,7 +32,7 @@ def test_exp_table_matches_generator():
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import gen_exp_table
     src = open(os.path.join(CSRC, "glibc_exp.cuh")).read()
-    block = src[src.index("kExpTab[256] = {", src.index("#else")):]
-    block = block[:block.index("};")]
+    block = src[src.index("#define CMOE_EXP_TABLE {"):]
+    block = block[:block.index("}")]
     vals = [int(v, 16) for v in re.findall(r"0x([0-9a-f]{16})ull", block)]
     assert vals == gen_exp_table.table()

@@ -1,10 +1,12 @@
-"""Every K1 router variant (ws and lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4), forced through
+"""Every K1 router variant (ws and lat 1x1 chains, small 1x4 with a deep prefetch ring, big 2x4 / 4x4, dmma on the
+fp64 tensor cores), forced through
 CL_MOE_ROUTER in a fresh process, gives bit-exact logits / top-k / counts against the oracle,
 including ragged last tiles, shapes where the automatic choice would pick another variant, and exact
 ties (duplicated router columns, all-zero tokens: the lowest expert index must win). Each case runs
 three times: bf16 tokens; unrounded fp32 tokens through the fp32 router input; and the router of the
 FP8 scheme (E4M3 codes of x / s_x widened in K1, qdq'd W_r) against router_fp8_sim. The "lat"
-variant is bf16-only; forced with another input it runs ws."""
+variant is bf16-only; forced with another input it runs ws. "dmma" (N <= 32) falls back to the automatic choice for
+more experts."""
 import os
 import subprocess
 import sys
@@ -16,7 +18,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("variant", ["small", "big2", "big4", "lat", "ws"])
+@pytest.mark.parametrize("variant", ["small", "big2", "big4", "lat", "ws", "dmma"])
 @pytest.mark.parametrize("t,d,n,k,mode", [(333, 256, 16, 2, "random"), (1000, 512, 8, 2, "random"),
                                           (257, 256, 32, 4, "random"), (70, 1024, 4, 1, "random"),
                                           (5, 256, 128, 8, "random"), (300, 256, 16, 4, "ties"),
