@@ -192,13 +192,20 @@ cl_status cl_moe_host_wait(cl_moe* h);
  * output (the reference's check_finite, proj/src/tensor.cpp:35-41) -> CL_ERR_RUN. */
 cl_status cl_moe_sync(cl_moe* h, void* stream);
 
-/* Large-batch routing in the fused forward (no decision export) is certified (DESIGN.md §4 K1):
- * fp32 logits with a rigorous error bound decide every token whose top-K order is unambiguous, the
- * others are recomputed with the reference's exact fp64 chains; routing indices, counts and the
- * permutation are bit-exact either way. cert_calls = certified routing calls so far,
- * last_recomputed = tokens recomputed exactly in the last one. Synchronous.
- * Environment: CL_MOE_ROUTER_CERT=0 routes every call with the exact kernels. */
+/* Opt-in certified large-batch routing in the fused forward (no decision export; environment
+ * CL_MOE_ROUTER_CERT=1, DESIGN.md §4 K1): fp32 logits with a rigorous error bound decide every token
+ * whose top-K order is unambiguous, the others are recomputed with the reference's exact fp64
+ * chains; routing indices, counts and the permutation are bit-exact either way. cert_calls =
+ * certified routing calls so far, last_recomputed = tokens recomputed exactly in the last one.
+ * Synchronous. */
 cl_status cl_moe_router_stats(cl_moe* h, int64_t* cert_calls, int64_t* last_recomputed);
+
+/* Which router kernel (K1) the last routing call ran, for diagnostics and tests: 0 = 128-thread 1x4
+ * blocked, 1 = 32-thread 1x4 with a deep ring, 2 = 4x4 / 2x4 blocked, 3 = latency 1x1, 4 = warp-
+ * specialised 1x1 chains (decode), 5 = fp64 tensor cores (DMMA), 6 = certified. dmma_ok = 1 when
+ * the handle's device check found DMMA accumulating as the sequential fp64 chain (variant 5 is
+ * then used for batches beyond the decode sizes; environment CL_MOE_ROUTER_DMMA=0 disables it). */
+cl_status cl_moe_router_variant(cl_moe* h, int32_t* variant, int32_t* dmma_ok);
 
 /* Stage buffers of the last call (valid until the next call on the handle). After a dense-decode
  * forward (single GPU, T <= 128) they are the dense buffers: rows = N*T, row e*T + t = token t for

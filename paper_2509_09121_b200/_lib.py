@@ -127,6 +127,7 @@ _PROTOS = {
     "cl_moe_save_fp8_scheme": (C.c_int, [C.c_void_p, C.c_char_p]),
     "cl_moe_get_weights": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "cl_moe_router_stats": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "cl_moe_router_variant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "cl_moe_load_fp8_scheme": (C.c_int, [C.c_void_p, C.c_char_p]),
     "cl_moe_get_router_fp8": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
 }

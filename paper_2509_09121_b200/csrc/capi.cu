@@ -1189,6 +1189,13 @@ cl_status cl_moe_router_stats(cl_moe* h, int64_t* cert_calls, int64_t* last_reco
   });
 }
 
+cl_status cl_moe_router_variant(cl_moe* h, int32_t* variant, int32_t* dmma_ok) {
+  return guarded(h, [&] {
+    if (variant) *variant = h->last_router_variant;
+    if (dmma_ok) *dmma_ok = h->dmma_ok ? 1 : 0;
+  });
+}
+
 cl_status cl_moe_set_router_fp8(cl_moe* h, int32_t enable, float act_scale) {
   return guarded(h, [&] {
     if (enable != 0 && enable != 1) throw ConfigErr("enable must be 0 or 1");

@@ -251,6 +251,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   const int variant = dmma ? 5 : ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
   const int tpc_eff = cert ? cert_tpc(N, xb) : tpc;
   h->tpc_cur = tpc_eff;
+  h->last_router_variant = cert ? 6 : variant;
   h->last_tokens = T;
   const int n_tiles = static_cast<int>((T + tpc_eff - 1) / tpc_eff);
   if (own_prof) prof_begin(h, st);

@@ -163,6 +163,7 @@ struct cl_moe {
   bool last_dense = false;  // the last forward took the dense-decode path (stage view = dense buffers)
   int tpc_cur = 32;                    // router tile (tokens) of the last routing call
   bool dmma_ok = false;                // the fp64 tensor-core router passed its device check (init)
+  int last_router_variant = -1;        // K1 kernel of the last routing call (cl_moe_router_variant)
   int64_t last_tokens = 0;             // T of the current call
 
   // per-stage CUDA-event timing (cl_moe_profile): one event set per profiled call

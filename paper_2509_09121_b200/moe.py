@@ -216,6 +216,12 @@ class MoELayer:
         self._check(self.L.cl_moe_router_stats(self.h, C.byref(a), C.byref(b)), "router_stats")
         return a.value, b.value
 
+    def router_variant(self):
+        """(K1 kernel of the last routing call — 0..6, see compass_moe.h —, DMMA device check passed)."""
+        a, b = C.c_int32(), C.c_int32()
+        self._check(self.L.cl_moe_router_variant(self.h, C.byref(a), C.byref(b)), "router_variant")
+        return a.value, bool(b.value)
+
     def router_weights(self) -> np.ndarray:
         """Host copy of W_r [d x N] (fp32) as the layer holds it."""
         w = np.empty((self.cfg.d_model, self.cfg.n_experts), np.float32)
