@@ -641,11 +641,9 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (q * 32 >= N) break;
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const double v = __shfl_sync(kAll, ex[q], i);
-          if (q * 32 + i < N) denom += v;
-        }
+        const int nq = min(32, N - q * 32);
+#pragma unroll 8
+        for (int i = 0; i < nq; ++i) denom += __shfl_sync(kAll, ex[q], i);
       }
       float pv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
       bool nan = false;
