@@ -23,7 +23,7 @@ def _layer(inp, t, k):
 
 @pytest.mark.parametrize("t,d,n,k,bf16", [(4096, 1024, 8, 2, True), (16384, 4096, 16, 2, True),
                                           (16384, 4096, 16, 2, False), (9000, 512, 32, 4, True),
-                                          (5000, 256, 4, 1, False)])
+                                          (5000, 256, 4, 1, False), (7000, 512, 12, 3, True)])
 def test_dmma_router_bit_exact(t, d, n, k, bf16):
     o = Oracle("port")
     inp = make_inputs(t, d, n, 128, experts=False, bf16=bf16)
@@ -42,6 +42,23 @@ def test_dmma_router_bit_exact(t, d, n, k, bf16):
     assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), ref["topk_idx"])
     assert np.array_equal(dec.combine_weights.cpu().numpy(), ref["combine_weights"])
     assert np.array_equal(dec.counts.cpu().numpy(), ref["counts"])
+    lay.close()
+
+
+def test_expert_counts_beyond_the_dmma_tiles_fall_back():
+    """N = 20 (three 8-expert tiles: not instantiated) routes with the DFMA kernels, still exact."""
+    t, d, n, k = 6000, 256, 20, 2
+    o = Oracle("port")
+    inp = make_inputs(t, d, n, 128, experts=False)
+    inp["w_in"] = np.zeros((n, d, 256), np.float32)
+    inp["w_out"] = np.zeros((n, 128, d), np.float32)
+    ref = o.route(inp["x"], inp["w_router"], k)
+    lay = _layer(inp, t, k)
+    dec = lay.route_tokens(torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16))
+    lay.sync()
+    assert lay.router_variant()[0] != 5
+    assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), ref["topk_idx"])
+    assert np.array_equal(dec.probs.cpu().numpy(), ref["probs"])
     lay.close()
 
 
