@@ -99,8 +99,8 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
       }
 #undef CL_MOE_DMMA_LAUNCH
       CK(cudaGetLastError());
-      router_finish_kernel<<<n_tiles, kFinishTpc * 32, router_finish_smem(N, kFinishTpc), st>>>((int)T, N, K,
-                                                                                            kFinishTpc, h->rb);
+      router_finish_kernel<<<n_tiles, router_finish_threads(N), router_finish_smem(N, kFinishTpc), st>>>(
+          (int)T, N, K, kFinishTpc, h->rb);
       break;
     }
     case 4:  // ws

@@ -611,6 +611,45 @@ __device__ __forceinline__ void ws_step_ld(double& acc, double xx, double ww, do
       : "memory");
 }
 
+// Per-tile statistics of a router tile whose rows of slog now hold probs and sidx the top-K
+// picks: one warp per expert over 32-token slices; a token's rank among the tile's tokens routed
+// to e is the popcount of the earlier lanes' ballot (each token picks e at most once); the prob sum
+// adds the tokens in ascending order, as router_finish. Called by all threads after a barrier.
+__device__ __forceinline__ void router_tile_stats(int tile, int tok0, int ntok, int N, int N4, int K,
+                                                  const float* slog, const int* sidx, const double* slse,
+                                                  const RouteBufs& rb) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  constexpr unsigned kAll = 0xffffffffu;
+  for (int e = warp; e < N; e += nwarps) {
+    int cnt = 0;
+    double ps = 0.0;
+    for (int t0 = 0; t0 < ntok; t0 += 32) {
+      const int t = t0 + lane;
+      int kk = -1;
+      double p = 0.0;
+      if (t < ntok) {
+        for (int k = 0; k < K; ++k)
+          if (sidx[t * 8 + k] == e) kk = k;
+        p = static_cast<double>(slog[t * N4 + e]);
+      }
+      const unsigned m = __ballot_sync(kAll, kk >= 0);
+      if (kk >= 0) rb.local_rank[(size_t)(tok0 + t) * K + kk] = cnt + __popc(m & ((1u << lane) - 1u));
+      cnt += __popc(m);
+      const int n = min(32, ntok - t0);
+      for (int i = 0; i < n; ++i) ps += __shfl_sync(kAll, p, i);
+    }
+    if (lane == 0) {
+      rb.tile_cnt[(size_t)tile * N + e] = cnt;
+      rb.tile_psum[(size_t)tile * N + e] = ps;
+    }
+  }
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < ntok; ++t) a += slse[t];
+    rb.tile_lse2[tile] = a;
+  }
+}
+
 // Per-token softmax / top-K / combine weights with one warp per token (lanes own experts), then the
 // per-tile statistics. Same arithmetic as router_finish: the max is order-free, the fp64 softmax
 // denominator and the top-K weight sum are accumulated in ascending order (every lane runs the same
@@ -724,37 +763,7 @@ __device__ __forceinline__ void router_finish_warps(int tile, int tok0, int tpc,
     if (lane == 0) slse[tl] = lse2;
   }
   __syncthreads();
-  // tile statistics, one warp per expert over 32-token slices: a token's rank among the tile's
-  // tokens routed to e is the popcount of the earlier lanes' ballot (each token picks e at most
-  // once); the prob sum adds the tokens in ascending order, as router_finish
-  for (int e = warp; e < N; e += nwarps) {
-    int cnt = 0;
-    double ps = 0.0;
-    for (int t0 = 0; t0 < ntok; t0 += 32) {
-      const int t = t0 + lane;
-      int kk = -1;
-      double p = 0.0;
-      if (t < ntok) {
-        for (int k = 0; k < K; ++k)
-          if (sidx[t * 8 + k] == e) kk = k;
-        p = static_cast<double>(slog[t * N4 + e]);
-      }
-      const unsigned m = __ballot_sync(kAll, kk >= 0);
-      if (kk >= 0) rb.local_rank[(size_t)(tok0 + t) * K + kk] = cnt + __popc(m & ((1u << lane) - 1u));
-      cnt += __popc(m);
-      const int n = min(32, ntok - t0);
-      for (int i = 0; i < n; ++i) ps += __shfl_sync(kAll, p, i);
-    }
-    if (lane == 0) {
-      rb.tile_cnt[(size_t)tile * N + e] = cnt;
-      rb.tile_psum[(size_t)tile * N + e] = ps;
-    }
-  }
-  if (threadIdx.x == 0) {
-    double a = 0.0;
-    for (int t = 0; t < ntok; ++t) a += slse[t];
-    rb.tile_lse2[tile] = a;
-  }
+  router_tile_stats(tile, tok0, ntok, N, N4, K, slog, sidx, slse, rb);
 }
 
 // tail_ctr (dense decode, nullable): the last CTA to finish also runs the plan (plan_body<128>)
@@ -1186,9 +1195,111 @@ __global__ void __launch_bounds__(kW * 32) router_dmma_kernel(const XT* __restri
   }
 }
 
+// router_finish_warps for N <= 16 with two tokens per warp (one per 16-lane half; lane = expert):
+// the same operations in the same order — max (fmax, NaN-ignoring, from the row's first logit),
+// exp_glibc, ascending-e fp64 denominator, one division per probability, K argmax rounds with the
+// lowest index winning ties (here a half-warp butterfly on (bits, index)), the winners' sum in
+// round order — so the results are bit-identical; half the warp instructions per token. tpc even.
+__device__ __forceinline__ void router_finish_half(int tile, int tok0, int tpc, int T, int N, int N4, int K,
+                                                   float* slog, int* sidx, double* slse, const RouteBufs& rb) {
+  const int ntok = min(tpc, T - tok0);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
+  const int seg = lane >> 4, sl = lane & 15;
+  constexpr unsigned kAll = 0xffffffffu;
+  for (int tb = warp * 2; tb < tpc; tb += nwarps * 2) {
+    const int tl = tb + seg;
+    const bool tv = tl < ntok;   // uniform within the half
+    const bool ev = tv && sl < N;
+    const int j = tok0 + tl;
+    float* zrow = slog + tl * N4;
+    const float z = ev ? zrow[sl] : 0.0f;
+    double mx = tv ? static_cast<double>(zrow[0]) : 0.0;
+    if (ev) mx = fmax(mx, static_cast<double>(z));
+#pragma unroll
+    for (int o = 8; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kAll, mx, o));
+    const double ex = ev ? exp_glibc(static_cast<double>(z) - mx) : 0.0;
+    double denom = 0.0;
+    for (int i = 0; i < N; ++i) denom += __shfl_sync(kAll, ex, (seg << 4) + i);
+    __syncwarp();  // every lane has read zrow (logits) before it is overwritten with probs
+    float pv = 0.0f;
+    bool nan = false;
+    if (ev) {
+      pv = static_cast<float>(ex / denom);
+      rb.probs[(size_t)j * N + sl] = pv;
+      zrow[sl] = pv;
+      nan = isnan(pv);
+    }
+    const double lse = mx + log(denom);
+    const double lse2 = tv ? lse * lse : 0.0;
+    const bool segnan = ((__ballot_sync(kAll, nan) >> (seg << 4)) & 0xffffu) != 0;
+    __syncwarp();
+    if (!segnan) {
+      bool taken = false;
+      float myv = 0.0f;
+      int myi = 0;
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k >= K) break;
+        unsigned key = (ev && !taken) ? __float_as_uint(pv) : 0u;
+        int idx = (ev && !taken) ? sl : 0x7fffffff;
+#pragma unroll
+        for (int o = 8; o; o >>= 1) {
+          const unsigned ok = __shfl_xor_sync(kAll, key, o);
+          const int oi = __shfl_xor_sync(kAll, idx, o);
+          if (ok > key || (ok == key && oi < idx)) {
+            key = ok;
+            idx = oi;
+          }
+        }
+        if (idx == sl) taken = true;
+        const float bv = __uint_as_float(key);
+        if (sl == k) {
+          myv = bv;
+          myi = idx;
+        }
+        sum += static_cast<double>(bv);
+      }
+      if (tv && sl < K) {
+        rb.topk_idx[(size_t)j * K + sl] = myi;
+        rb.combine_w[(size_t)j * K + sl] = static_cast<float>(static_cast<double>(myv) / sum);
+        sidx[tl * 8 + sl] = myi;
+      }
+    } else if (tv && sl == 0) {  // sequential reference order (rows with a NaN probability)
+      float vals[8];
+      int ids[8];
+      unsigned taken_bits = 0;
+      for (int k = 0; k < K; ++k) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < N; ++e) {
+          if ((taken_bits >> e) & 1u) continue;
+          const float v = zrow[e];
+          if (best < 0 || v > bv) { best = e; bv = v; }
+        }
+        taken_bits |= 1u << best;
+        vals[k] = bv;
+        ids[k] = best;
+      }
+      double sum = 0.0;
+      for (int k = 0; k < K; ++k) sum += static_cast<double>(vals[k]);
+      for (int k = 0; k < K; ++k) {
+        rb.topk_idx[(size_t)j * K + k] = ids[k];
+        rb.combine_w[(size_t)j * K + k] = static_cast<float>(static_cast<double>(vals[k]) / sum);
+        sidx[tl * 8 + k] = ids[k];
+      }
+    }
+    if (sl == 0) slse[tl] = lse2;
+  }
+  __syncthreads();
+  router_tile_stats(tile, tok0, ntok, N, N4, K, slog, sidx, slse, rb);
+}
+
 // Softmax / top-K / combine weights / tile statistics of router tiles whose logits are already in
-// rb.logits (router_dmma_kernel): one CTA per tile of tpc <= 32 tokens, one warp per token.
+// rb.logits (router_dmma_kernel): one CTA per tile of tpc <= 32 tokens, one warp per token (two for
+// N <= 16, router_finish_half).
 constexpr int kFinishTpc = 16;  // tokens per finish tile (the plan's router tile on this path)
+__host__ __device__ inline int router_finish_threads(int N) { return N <= 16 ? kFinishTpc * 16 : kFinishTpc * 32; }
 __global__ void __launch_bounds__(kFinishTpc * 32) router_finish_kernel(int T, int N, int K, int tpc, RouteBufs rb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int N4 = (N + 3) / 4 * 4;
@@ -1202,7 +1313,8 @@ __global__ void __launch_bounds__(kFinishTpc * 32) router_finish_kernel(int T, i
     slog[i] = (t < ntok && e < N) ? rb.logits[(size_t)(tok0 + t) * N + e] : 0.0f;
   }
   __syncthreads();
-  router_finish_warps(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
+  if (N <= 16) router_finish_half(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
+  else router_finish_warps(blockIdx.x, tok0, tpc, T, N, N4, K, slog, sidx, slse, rb);
 }
 __host__ __device__ inline size_t router_finish_smem(int N, int tpc) {
   const int N4 = (N + 3) / 4 * 4;
