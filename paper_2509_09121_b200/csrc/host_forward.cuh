@@ -99,8 +99,8 @@ void launch_router(cl_moe* h, const XT* x, const double* w64, int64_t T, int N, 
       }
 #undef CL_MOE_DMMA_LAUNCH
       CK(cudaGetLastError());
-      router_finish_kernel<<<n_tiles, router_finish_threads(N), router_finish_smem(N, kFinishTpc), st>>>(
-          (int)T, N, K, kFinishTpc, h->rb);
+      router_finish_kernel<<<n_tiles, router_finish_threads(N), router_finish_smem(N, router_finish_tpc(N)), st>>>(
+          (int)T, N, K, router_finish_tpc(N), h->rb);
       break;
     }
     case 4:  // ws
@@ -246,7 +246,7 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   // (the opt-in certified router takes precedence when enabled)
   const bool cert = big && !h->need_exact && !dense && N <= 32 && cert_enabled() && force == 0;
   const bool dmma = dmma_fit && !cert && (force == 5 || (force == 0 && !lat_size && !dense));
-  const int tpc = dmma ? kFinishTpc : big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
+  const int tpc = dmma ? router_finish_tpc(N) : big ? tpc_big : ws ? RouterWsSmem(N, ws_cons, xb).tpc : lat ? tpc_lat
                                  : router_tokens_per_cta(N, small ? 32 : 128);
   const int variant = dmma ? 5 : ws ? 4 : lat ? 3 : big ? 2 : small ? 1 : 0;
   const int tpc_eff = cert ? cert_tpc(N, xb) : tpc;

@@ -1296,11 +1296,14 @@ __device__ __forceinline__ void router_finish_half(int tile, int tok0, int tpc, 
 }
 
 // Softmax / top-K / combine weights / tile statistics of router tiles whose logits are already in
-// rb.logits (router_dmma_kernel): one CTA per tile of tpc <= 32 tokens, one warp per token (two for
-// N <= 16, router_finish_half).
-constexpr int kFinishTpc = 16;  // tokens per finish tile (the plan's router tile on this path)
-__host__ __device__ inline int router_finish_threads(int N) { return N <= 16 ? kFinishTpc * 16 : kFinishTpc * 32; }
-__global__ void __launch_bounds__(kFinishTpc * 32) router_finish_kernel(int T, int N, int K, int tpc, RouteBufs rb) {
+// rb.logits (router_dmma_kernel): one CTA per tile of router_finish_tpc(N) tokens, one warp per
+// token (two for N <= 16, router_finish_half).
+// tokens per finish tile (the plan's router tile on this path) and threads: 32 tokens on 16 warps
+// (two per warp) for N <= 16, else 16 tokens on 16 warps; fewer, larger tiles keep the plan's
+// serial scan short
+__host__ __device__ inline int router_finish_tpc(int N) { return N <= 16 ? 32 : 16; }
+__host__ __device__ inline int router_finish_threads(int) { return 512; }
+__global__ void __launch_bounds__(512) router_finish_kernel(int T, int N, int K, int tpc, RouteBufs rb) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const int N4 = (N + 3) / 4 * 4;
   float* slog = reinterpret_cast<float*>(smem_raw);                                  // [tpc][N4]
