@@ -70,6 +70,8 @@ struct GemmArgs {
   int32_t prefetch_lead;    // ... issued this many k-blocks before the end of the current tile, where
                             // the producer also claims the next tile index
   uint64_t a_hint, b_hint;  // TMA L2 cache hints of the A / B loads (0 = the kernel's default)
+  const int32_t* a_poff;    // row-grouped, nullable: A rows come from the padded row layout (expert e
+                            // from a_poff[e]); output rows, masks and row scales stay in the row layout
 };
 
 constexpr int kGemmThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / idle; warps 4-11: epilogue
@@ -411,7 +413,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           ready_e = ti.e;
         }
         const bool half_t = kCtaGroup == 2 && ti.half;
-        const int a_row = ti.a_row + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
+        const int a_src = (!kWgrad && args.a_poff) ? __ldg(args.a_poff + ti.e) + (ti.a_row - s_off[ti.e]) : ti.a_row;
+        const int a_row = a_src + cta_rank * (half_t ? 64 : Cfg::kRowsPerCta);
         const int b_row = ti.b_row + cta_rank * Cfg::kBRowsPerCta;
         int next = -1;
         const int claim_kb = pf ? ti.kb0 + max(0, ti.nkb - args.prefetch_lead) : 1 << 30;
@@ -419,7 +422,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (kb == claim_kb) {
             next = claim(i + 1);
             if (next < total_tiles && decode(next, tn, nactive)) {
-              const int na = tn.a_row + cta_rank * Cfg::kRowsPerCta, nb = tn.b_row + cta_rank * Cfg::kBRowsPerCta;
+              const int na_src = args.a_poff ? __ldg(args.a_poff + tn.e) + (tn.a_row - s_off[tn.e]) : tn.a_row;
+              const int na = na_src + cta_rank * Cfg::kRowsPerCta, nb = tn.b_row + cta_rank * Cfg::kBRowsPerCta;
               for (int k = tn.kb0; k < tn.kb0 + min(tn.nkb, args.prefetch_kb); ++k) {
                 tma_prefetch_2d(&tmA, k * kBKElems, na);
                 tma_prefetch_2d(&tmB, k * kBKElems, nb);
@@ -725,9 +729,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               du[i] = da * (g[i] * s);
               dg[i] = da * u[i] * (s * (1.0f + g[i] * (1.0f - s)));
             }
-            __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * (2 * args.ffn);
-            store_bf16x32(drow + col, dg);
-            store_bf16x32(drow + args.ffn + col, du);
+            if (args.out) {  // (training: null — dgrad-2 reads dH from the padded copy below)
+              __nv_bfloat16* drow = reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * (2 * args.ffn);
+              store_bf16x32(drow + col, dg);
+              store_bf16x32(drow + args.ffn + col, du);
+            }
             if (args.aux_t) {  // dH in the padded row layout (dW_in gradient operand)
               __nv_bfloat16* t = reinterpret_cast<__nv_bfloat16*>(args.aux_t) + (size_t)prow * (2 * args.ffn);
               store_bf16x32(t + col, dg);

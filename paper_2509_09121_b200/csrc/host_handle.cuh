@@ -225,7 +225,6 @@ struct cl_moe {
   __nv_bfloat16* wout_ref = nullptr;    // [NL][f][d]  reference layout (dgrad-1 B operand)
   __nv_bfloat16* Hbuf = nullptr;        // [cap*K][2f] pre-activations [G | U]
   __nv_bfloat16* dYbuf = nullptr;       // [cap*K][d]
-  __nv_bfloat16* dHbuf = nullptr;       // [cap*K][2f]
   __nv_bfloat16* dXbuf = nullptr;       // [cap*K][d]
   // weight-gradient operands in the padded row layout [rp_cap][C] (expert e's rows from poff[e],
   // zero padding rows): X, A (= SwiGLU output), dY, dH
@@ -236,7 +235,8 @@ struct cl_moe {
   float* rpart = nullptr;               // dW_r partials [chunks][d][N]
   float* dcw_scratch = nullptr;         // d(combine weights) [cap][K] when the caller does not want them
   int32_t* kb_off = nullptr;            // [NL+1]
-  CUtensorMap mAdg1[2], mBdg1[2], mAdg2[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
+  CUtensorMap mAdg1[2], mBdg1[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
+  CUtensorMap mAdg2T[2];  // dgrad-2's A = dH in the padded row layout (GemmArgs::a_poff)
 
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps
@@ -264,7 +264,7 @@ struct cl_moe {
     for (void* p : ptrs)
       if (p) cudaFree(p);
     for (void* p : {(void*)x_recv, (void*)act_recv, (void*)y_recv, (void*)ep_counts_dev, (void*)ep_off_dev,
-                    (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dHbuf, (void*)dXbuf, (void*)XT,
+                    (void*)win_ref, (void*)wout_ref, (void*)Hbuf, (void*)dYbuf, (void*)dXbuf, (void*)XT,
                     (void*)AT, (void*)dYT, (void*)dHT, (void*)poff, (void*)kb_off, (void*)rdz, (void*)rpart,
                     (void*)dcw_scratch, (void*)dYsrc, (void*)dXsrc, (void*)tile_counter, (void*)peer_x_dev,
                     (void*)peer_y_dev, (void*)peer_w_dev, (void*)w_recv, (void*)expert_dst, (void*)expert_dst_w,

@@ -23,7 +23,6 @@ void ensure_training(cl_moe* h) {
     h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
     h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
     if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
-    h->dHbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
     h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
     h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
     h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
@@ -35,7 +34,7 @@ void ensure_training(cl_moe* h) {
       const uint32_t brow = v == 0 ? 256 : 128;
       h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
       h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
-      h->mAdg2[v] = make_map(h->dHbuf, false, 2 * f, rows, 128);
+      h->mAdg2T[v] = make_map(h->dHT, false, 2 * f, h->rp_cap, 128);  // dH, padded row layout
       h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
       // weight-gradient operands, MN-major: boxes of 64 columns x 64 padded rows
       h->mAwo[v] = make_map(h->AT, false, f, h->rp_cap, 64);
@@ -144,7 +143,8 @@ void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   a1.n_tiles_n = static_cast<int>(f / kBN);
   a1.num_kb = static_cast<int>(d * 2 / kBKBytes);
   a1.b_rows_per_expert = static_cast<int>(f);
-  a1.out = h->dHbuf;
+  // dH is written once, in the padded row layout both dW_in and dgrad-2 read (a2.a_poff)
+  a1.out = nullptr;
   a1.aux = h->Hbuf;
   a1.ffn = static_cast<int>(f);
   a1.aux_t = h->dHT;  // dH^T straight from the epilogue (dW_in GEMM operand)
@@ -160,14 +160,15 @@ void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   a2.out = h->dXbuf;
   a2.ldo = static_cast<int>(d);
   a2.row_ptr = peer ? h->row_ptr_dx : nullptr;
+  a2.a_poff = h->poff;
   if (v) {
     launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
     prof_mark(h, 1, st);
-    launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
+    launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2T[v], h->mBdg2[v], a2, st);
   } else {
     launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
     prof_mark(h, 1, st);
-    launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2[v], h->mBdg2[v], a2, st);
+    launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2T[v], h->mBdg2[v], a2, st);
   }
   if (ep && !peer) ep_exchange(h, h->dXbuf, dX_src, false, st);  // dX rows back to their tokens' ranks
   prof_mark(h, 2, st);
