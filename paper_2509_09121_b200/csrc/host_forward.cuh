@@ -240,9 +240,9 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
   // device check passed and the experts fit its instantiations (N <= 32)
   const int nt8 = dmma_n8(N) / 8;
   // 4 warps (32 tokens) per CTA when that still leaves >= 2 CTAs per SM, else 2 (16 tokens)
-  const int dmma_g = (T + 31) / 32 >= 2 * h->num_sms ? 4 : 2;
+  const int dmma_w = (T + 31) / 32 >= 2 * h->num_sms ? 4 : 2;
   const bool dmma_fit = h->dmma_ok && (nt8 == 1 || nt8 == 2 || nt8 == 4) &&
-                        RouterDmmaSmem(N, dmma_g, xb).total <= 220 * 1024;
+                        RouterDmmaSmem(N, dmma_w, xb).total <= 220 * 1024;
   // (the opt-in certified router takes precedence when enabled)
   const bool cert = big && !h->need_exact && !dense && N <= 32 && cert_enabled() && force == 0;
   const bool dmma = dmma_fit && !cert && (force == 5 || (force == 0 && !lat_size && !dense));
@@ -268,17 +268,17 @@ bool run_router(cl_moe* h, const void* x, int64_t T, cudaStream_t st, bool own_p
     if (cert)
       launch_router_cert<uint8_t>(h, h->xq8, h->sxr_dev, true, T, st);
     else
-      launch_router<uint8_t>(h, h->xq8, h->wr64q, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok, lat_chunk, tail, rwd, invd,
+      launch_router<uint8_t>(h, h->xq8, h->wr64q, T, N, n_tiles, variant, dmma ? dmma_w : ws_cons, big_tok, lat_chunk, tail, rwd, invd,
                              st, h->sxr_dev);
   } else if (cert && xf32) {
     launch_router_cert<float>(h, static_cast<const float*>(x), nullptr, false, T, st);
   } else if (cert) {
     launch_router_cert<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), nullptr, false, T, st);
   } else if (xf32)
-    launch_router<float>(h, static_cast<const float*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok, lat_chunk, tail,
+    launch_router<float>(h, static_cast<const float*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_w : ws_cons, big_tok, lat_chunk, tail,
                          rwd, invd, st);
   else
-    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_g : ws_cons, big_tok,
+    launch_router<__nv_bfloat16>(h, static_cast<const __nv_bfloat16*>(x), h->wr64, T, N, n_tiles, variant, dmma ? dmma_w : ws_cons, big_tok,
                                  lat_chunk, tail, rwd, invd, st);
   CK(cudaGetLastError());
   prof_mark(h, 0, st);
