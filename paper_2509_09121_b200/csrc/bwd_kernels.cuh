@@ -19,9 +19,11 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ dy, float* __restrict__ d_cw,
                                                           void* const* __restrict__ expert_dst = nullptr,
                                                           const int32_t* __restrict__ idx = nullptr,
-                                                          const int32_t* __restrict__ offsets = nullptr) {
+                                                          const int32_t* __restrict__ offsets = nullptr,
+                                                          const int32_t* __restrict__ dst_poff = nullptr) {
   // expert_dst (EP peer transport): the dY row of expert g goes straight into the owner's dYbuf at
-  // expert_dst[g] + (r - offsets[g]) rows instead of dy[r].
+  // expert_dst[g] + (r - offsets[g]) rows instead of dy[r]. dst_poff (single GPU): dy is the padded
+  // row layout, expert g's rows from dst_poff[g] (dgrad-1 and dW_out read it there).
   const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -31,7 +33,10 @@ __global__ void __launch_bounds__(256) combine_bwd_kernel(const __nv_bfloat16* _
   const int4* g = reinterpret_cast<const int4*>(d_out + (size_t)j * d);
   const int4* yr = reinterpret_cast<const int4*>(y + (size_t)r * d);
   int4* o = reinterpret_cast<int4*>(dy + (size_t)r * d);
-  if (expert_dst) {
+  if (dst_poff) {
+    const int e = idx[s];
+    o = reinterpret_cast<int4*>(dy + (size_t)(dst_poff[e] + (r - offsets[e])) * d);
+  } else if (expert_dst) {
     const int e = idx[s];
     char* b = static_cast<char*>(expert_dst[e]);
     o = b ? reinterpret_cast<int4*>(b + (size_t)(r - offsets[e]) * d * 2) : nullptr;

@@ -214,6 +214,7 @@ void run_ep(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, cudaSt
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
   h->last_dense = false;
+  h->last_xperm_padded = false;
   if (train) {
     h->train_T = T;
     h->cur_x = x;
@@ -319,6 +320,7 @@ void ep_peer_combine(cl_moe* h, const void* x, int64_t T, void* out, bool out_f3
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
   h->last_dense = false;
+  h->last_xperm_padded = false;
 }
 
 // Multi-process forward over NVLink peer memory. NCCL carries only the R x N counts and two

@@ -312,7 +312,7 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
                cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr,
                cudaEvent_t g2_wait = nullptr, const uint32_t* g1_arrive = nullptr,
-               const uint32_t* g1_arrive_tgt = nullptr) {
+               const uint32_t* g1_arrive_tgt = nullptr, const int32_t* a1_poff = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
@@ -331,6 +331,7 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g1.b_rows_per_expert = static_cast<int>(2 * h->f);
   g1.out = act;
   g1.ldo = static_cast<int>(h->f);
+  g1.a_poff = a1_poff;  // single-GPU training: the dispatched rows sit in the padded layout
   g1.act_scale = h->sx_in;
   g1.w_scale = h->ws_in;
   g1.out_scale = h->sx_mid;
@@ -435,6 +436,7 @@ void run_experts(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
   h->last_dense = false;
+  h->last_xperm_padded = false;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -527,6 +529,7 @@ void run_forward(cl_moe* h, const void* x, int64_t T, void* out, bool out_f32, c
   h->cur_ev = nullptr;
   h->last_rows = N * T;  // dense layout: row e*T + t = token t for expert e
   h->last_dense = true;
+  h->last_xperm_padded = false;
 }
 
 void export_decision(cl_moe* h, int64_t T, const cl_moe_decision* o, cudaStream_t st) {

@@ -237,6 +237,8 @@ struct cl_moe {
   int32_t* kb_off = nullptr;            // [NL+1]
   CUtensorMap mAdg1[2], mBdg1[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
   CUtensorMap mAdg2T[2];  // dgrad-2's A = dH in the padded row layout (GemmArgs::a_poff)
+  CUtensorMap mA1T[2], mAdg1T[2];  // single-GPU training: GEMM1's A = X, dgrad-1's A = dY, padded
+  bool last_xperm_padded = false;  // the last call (single-GPU forward_train) left x_perm padded
 
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps

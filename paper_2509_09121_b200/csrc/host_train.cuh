@@ -35,6 +35,8 @@ void ensure_training(cl_moe* h) {
       h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
       h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
       h->mAdg2T[v] = make_map(h->dHT, false, 2 * f, h->rp_cap, 128);  // dH, padded row layout
+      h->mA1T[v] = make_map(h->XT, false, d, h->rp_cap, 128);          // X (single-GPU training)
+      h->mAdg1T[v] = make_map(h->dYT, false, d, h->rp_cap, 128);       // dY (single-GPU training)
       h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
       // weight-gradient operands, MN-major: boxes of 64 columns x 64 padded rows
       h->mAwo[v] = make_map(h->AT, false, f, h->rp_cap, 64);
@@ -68,14 +70,16 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   }
   const int N = static_cast<int>(h->N);
   const int tpc = h->tpc_cur;
-  const int blocks = static_cast<int>((T + 7) / 8);
-  dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
-                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->xperm, h->perm,
-                                                 h->inv, h->row_w, nullptr);
+  // the dispatched rows go straight into the padded row layout the dW_in GEMM reads; GEMM1 reads
+  // them there too (GemmArgs::a_poff), so no row-layout copy and no pad pass
   pad_plan_kernel<<<1, 32, 0, st>>>(h->rb.offsets, h->n_local, h->poff, h->kb_off);
+  dispatch_kernel<false><<<token_grid(T), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), (int)T, (int)h->d, N, (int)h->K,
+                                                 tpc, h->rb, h->rb.topk_idx, h->rb.combine_w, h->XT, h->perm,
+                                                 h->inv, h->row_w, nullptr, nullptr, nullptr, nullptr, h->poff);
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
-  run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf);
+  run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1T, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf, nullptr,
+            nullptr, nullptr, nullptr, h->poff);
   prof_mark(h, 4, st);
   launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
                                 h->rb.finite_flag, st, h->rb.combine_w);
@@ -84,6 +88,7 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   h->cur_ev = nullptr;
   h->last_rows = T * h->K;
   h->last_dense = false;
+  h->last_xperm_padded = true;
   h->train_T = T;
   h->cur_x = x;
 }
@@ -120,10 +125,12 @@ void bwd_phase_a(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   __nv_bfloat16* dY_src = ep ? h->dYsrc : h->dYbuf;
   prof_begin(h, st, 1);
   // 1. combine backward: dY = w * dOut[token], d_combine_w = <dOut[token], Y>
+  // single GPU: dY rows straight into the padded layout dgrad-1 and dW_out read
   combine_bwd_kernel<<<(int)((rows + 7) / 8), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(a.d_out), h->y, h->perm,
-                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K, dY_src,
-                                                           a.d_cw, peer ? h->expert_dst_dy : nullptr, h->rb.topk_idx,
-                                                           h->rb.offsets);
+                                                           h->rb.combine_w, (int)rows, (int)d, (int)h->K,
+                                                           ep ? dY_src : h->dYT, a.d_cw,
+                                                           peer ? h->expert_dst_dy : nullptr, h->rb.topk_idx,
+                                                           h->rb.offsets, ep ? nullptr : h->poff);
   CK(cudaGetLastError());
   if (ep && !peer) ep_exchange(h, dY_src, h->dYbuf, true, st);  // dY rows to the experts' owners
   prof_mark(h, 0, st);
@@ -161,12 +168,15 @@ void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   a2.ldo = static_cast<int>(d);
   a2.row_ptr = peer ? h->row_ptr_dx : nullptr;
   a2.a_poff = h->poff;
+  // dY: padded on a single GPU (combine-bwd wrote it there), the receive layout under EP
+  const CUtensorMap* mA_dg1 = ep ? h->mAdg1 : h->mAdg1T;
+  if (!ep) a1.a_poff = h->poff;
   if (v) {
-    launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    launch_gemm<2, EPI_SWIGLU_BWD, false, false>(h, mA_dg1[v], h->mBdg1[v], a1, st);
     prof_mark(h, 1, st);
     launch_gemm<2, EPI_ROWSCALE, false, false>(h, h->mAdg2T[v], h->mBdg2[v], a2, st);
   } else {
-    launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, h->mAdg1[v], h->mBdg1[v], a1, st);
+    launch_gemm<1, EPI_SWIGLU_BWD, false, false>(h, mA_dg1[v], h->mBdg1[v], a1, st);
     prof_mark(h, 1, st);
     launch_gemm<1, EPI_ROWSCALE, false, false>(h, h->mAdg2T[v], h->mBdg2[v], a2, st);
   }
@@ -223,8 +233,13 @@ void bwd_phase_d(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   // padded row-major operands of the weight gradients: X and dY copied into the padded row
   // layout; A and dH were written there by the GEMM1 / dgrad-1 epilogues (zero their padding)
   const unsigned pr = static_cast<unsigned>(h->rp_cap / 8);
-  pad_rows_kernel<<<pr, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d, es_off, h->poff, NL, h->XT);
-  pad_rows_kernel<<<pr, 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT);
+  if (ep) {  // expert parallel: X and dY arrived in the receive layout
+    pad_rows_kernel<<<pr, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(es_x), (int)d, es_off, h->poff, NL, h->XT);
+    pad_rows_kernel<<<pr, 256, 0, st>>>(h->dYbuf, (int)d, es_off, h->poff, NL, h->dYT);
+  } else {   // single GPU: dispatch and combine-bwd wrote them padded; zero the padding rows only
+    zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->XT, (int)d, es_off, h->poff);
+    zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->dYT, (int)d, es_off, h->poff);
+  }
   zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->AT, (int)f, es_off, h->poff);
   zero_pad_rows_kernel<<<dim3(8, (unsigned)NL), 256, 0, st>>>(h->dHT, (int)(2 * f), es_off, h->poff);
   CK(cudaGetLastError());

@@ -1419,12 +1419,16 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
                                                        float* __restrict__ row_w, const float* __restrict__ act_scale,
                                                        void* const* __restrict__ expert_dst = nullptr,
                                                        float* const* __restrict__ expert_dst_w = nullptr,
-                                                       uint32_t* const* __restrict__ expert_arrive = nullptr) {
+                                                       uint32_t* const* __restrict__ expert_arrive = nullptr,
+                                                       const int32_t* __restrict__ dst_poff = nullptr) {
   // expert_dst (peer transport, ep.cuh): row r of expert e goes to expert_dst[e] + (r - offsets[e])
   // rows — the owner's receive buffer over NVLink — instead of xperm; null entries (overflow) skip.
   // expert_arrive (dispatch overlapped with the owners' GEMM1): after its stores the CTA adds the
   // number of (row, column-slice) pieces it wrote for each expert to the owner's arrival counter
   // (system-scope release), which the owner's GEMM1 producer acquires before loading the rows.
+  // dst_poff (training, single GPU): xperm is the padded row layout, expert e's rows from
+  // dst_poff[e] (the weight-gradient operand, read by GEMM1 through GemmArgs::a_poff); perm / inv /
+  // row_w stay in the row layout.
   __shared__ uint32_t s_arr[kMaxArriveExperts];
   if (expert_arrive) {
     for (int g = threadIdx.x; g < N; g += blockDim.x) s_arr[g] = 0;
@@ -1451,7 +1455,8 @@ __global__ void __launch_bounds__(256) dispatch_kernel(const __nv_bfloat16* __re
       dsts[k] = b ? b + (size_t)(r - rb.offsets[e]) * d * kRowElemBytes : nullptr;
       if (lane == 0 && b && blockIdx.y == 0) expert_dst_w[e][r - rb.offsets[e]] = wts[s];
     } else {
-      dsts[k] = static_cast<char*>(xperm) + (size_t)r * d * kRowElemBytes;
+      const size_t pr = dst_poff ? (size_t)(dst_poff[e] + (r - rb.offsets[e])) : (size_t)r;
+      dsts[k] = static_cast<char*>(xperm) + pr * d * kRowElemBytes;
     }
     if constexpr (kFp8) sc[k] = act_scale[e];
     if (lane == 0 && blockIdx.y == 0) {

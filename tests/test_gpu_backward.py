@@ -89,3 +89,25 @@ def test_full_backward_with_router_vs_oracle(t, d, n, k, f, ga, gz):
     assert _rel(dwi.cpu().numpy(), rdwi) <= 2e-2
     assert _rel(dwo.cpu().numpy(), rdwo) <= 2e-2
     lay.close()
+
+
+def test_training_forward_keeps_dispatched_rows_padded():
+    """A single-GPU forward_train writes the dispatched rows only into the padded layout the
+    weight gradients (and GEMM1) read: the x_perm stage is then refused (stage contract,
+    compass_moe.h), and an inference forward afterwards materialises it again."""
+    from paper_2509_09121_b200.moe import MoEConfig, MoEError, MoELayer
+    t, d, n, k, f = 300, 256, 4, 2, 256
+    inp = make_inputs(t, d, n, f)
+    lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t), inp["w_router"],
+                   inp["w_in"], inp["w_out"])
+    x = torch.from_numpy(inp["x"]).cuda().to(torch.bfloat16).contiguous()
+    lay.forward_train(x)
+    lay.sync()
+    with pytest.raises(MoEError):
+        lay.stage("x_perm", (t * k, d), torch.bfloat16)
+    lay.forward(x)
+    lay.sync()
+    xp = lay.stage("x_perm", (t * k, d), torch.bfloat16)
+    perm = lay.stage("perm", (t * k,), torch.int32).long()
+    assert torch.equal(xp, x[perm // k])
+    lay.close()
