@@ -239,6 +239,7 @@ struct cl_moe {
   CUtensorMap mAdg2T[2];  // dgrad-2's A = dH in the padded row layout (GemmArgs::a_poff)
   CUtensorMap mA1T[2], mAdg1T[2];  // single-GPU training: GEMM1's A = X, dgrad-1's A = dY, padded
   bool last_xperm_padded = false;  // the last call (single-GPU forward_train) left x_perm padded
+  bool mAdg1_ready = false;        // dgrad-1's receive-layout dY map exists (expert parallel)
 
   CUtensorMap mA1[2], mB1[2], mA2[2], mB2[2];      // [variant: 0 = 1-CTA, 1 = 2-CTA]
   CUtensorMap mA1q[2], mB1q[2], mA2q[2], mB2q[2];  // e4m3 maps

@@ -22,7 +22,7 @@ void ensure_training(cl_moe* h) {
     h->win_ref = dalloc<__nv_bfloat16>((size_t)NL * d * 2 * f);
     h->wout_ref = dalloc<__nv_bfloat16>((size_t)NL * f * d);
     h->Hbuf = dalloc<__nv_bfloat16>(rows * 2 * f);
-    if (!h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(rows * d);
+    if (ep && !h->dYbuf) h->dYbuf = dalloc<__nv_bfloat16>(rows * d);  // (single GPU: dY lives in dYT)
     h->dXbuf = dalloc<__nv_bfloat16>(rows * d);
     h->XT = dalloc<__nv_bfloat16>(d * h->rp_cap);
     h->AT = dalloc<__nv_bfloat16>(f * h->rp_cap);
@@ -32,7 +32,8 @@ void ensure_training(cl_moe* h) {
     h->kb_off = dalloc<int32_t>(NL + 1);
     for (int v = 0; v < 2; ++v) {
       const uint32_t brow = v == 0 ? 256 : 128;
-      h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
+      if (ep) h->mAdg1[v] = make_map(h->dYbuf, false, d, rows, 128);
+      h->mAdg1_ready = ep;
       h->mBdg1[v] = make_map(h->wout_ref, false, d, (uint64_t)NL * f, brow);
       h->mAdg2T[v] = make_map(h->dHT, false, 2 * f, h->rp_cap, 128);  // dH, padded row layout
       h->mA1T[v] = make_map(h->XT, false, d, h->rp_cap, 128);          // X (single-GPU training)
@@ -169,6 +170,8 @@ void bwd_phase_b(cl_moe* h, const BwdArgs& a, cudaStream_t st) {
   a2.row_ptr = peer ? h->row_ptr_dx : nullptr;
   a2.a_poff = h->poff;
   // dY: padded on a single GPU (combine-bwd wrote it there), the receive layout under EP
+  if (ep && !h->mAdg1_ready)  // training buffers are laid out once, for the mode of the first call
+    throw ConfigErr("expert-parallel training needs cl_moe_ep_init before the handle's first forward_train");
   const CUtensorMap* mA_dg1 = ep ? h->mAdg1 : h->mAdg1T;
   if (!ep) a1.a_poff = h->poff;
   if (v) {
