@@ -212,8 +212,8 @@ cl_status cl_moe_router_variant(cl_moe* h, int32_t* variant, int32_t* dmma_ok);
  * expert e (offsets[e] = e*T), row_weight = the combine weight of (t, e) or 0 when e is not among
  * t's top-K, inv[t*K + k] = the row of token t's k-th expert; perm = NULL (copy_stage(1) ->
  * CL_ERR_RUN): no permutation is materialised. After a single-GPU cl_moe_forward_train the
- * dispatched rows live only in the padded layout the weight gradients read: x_perm = NULL
- * (copy_stage(4) -> CL_ERR_RUN). */
+ * dispatched rows and the SwiGLU output live only in the padded layouts the weight gradients
+ * read: x_perm = act = NULL (copy_stage(4) / copy_stage(5) -> CL_ERR_RUN). */
 cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* view);
 
 /* Copies stage buffer `which` (0 offsets, 1 perm, 2 inv, 3 row_weight, 4 x_perm, 5 act, 6 y)

@@ -807,7 +807,7 @@ cl_status cl_moe_stage_buffers(cl_moe* h, cl_moe_stage_view* v) {
       v->inv = h->inv;
       v->row_weight = h->row_w;
       v->x_perm = h->last_xperm_padded ? nullptr : h->xperm;  // (single-GPU training: padded)
-      v->act = h->act;
+      v->act = h->last_xperm_padded ? nullptr : h->act;
       v->y = h->y;
     }
     v->rows = h->last_rows;
@@ -831,7 +831,11 @@ cl_status cl_moe_copy_stage(cl_moe* h, int32_t which, void* dst, int64_t bytes, 
           throw RunErr("x_perm is kept in the padded row layout after a single-GPU training forward");
         src = dn ? (const void*)h->xd : h->xperm;
         break;
-      case 5: src = dn ? (const void*)h->actd : h->act; break;
+      case 5:
+        if (h->last_xperm_padded)
+          throw RunErr("act is kept in the padded row layout after a single-GPU training forward");
+        src = dn ? (const void*)h->actd : h->act;
+        break;
       case 6: src = dn ? (const void*)h->yd : h->y; break;
       default: throw ConfigErr("unknown stage buffer");
     }

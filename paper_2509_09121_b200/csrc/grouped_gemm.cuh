@@ -570,7 +570,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             st_global_v8(reinterpret_cast<uint8_t*>(args.out) + (size_t)row * args.ldo + col, p);
           } else {
-            store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
+            if (args.out)  // (single-GPU training: null — A lives only in the padded copy below)
+              store_bf16x32(reinterpret_cast<__nv_bfloat16*>(args.out) + (size_t)row * args.ldo + col, v);
             if (args.aux) {  // training: keep H = [G | U] for the SwiGLU backward
               __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(args.aux) + (size_t)row * (2 * args.ffn);
               store_bf16x32(hrow + col, gv);

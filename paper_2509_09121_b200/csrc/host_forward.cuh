@@ -312,7 +312,8 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
                const CUtensorMap* mA1, const CUtensorMap* mA2, const CUtensorMap* mA1q, const CUtensorMap* mA2q,
                cudaStream_t st, __nv_bfloat16* h_save = nullptr, void* const* row_ptr = nullptr,
                cudaEvent_t g2_wait = nullptr, const uint32_t* g1_arrive = nullptr,
-               const uint32_t* g1_arrive_tgt = nullptr, const int32_t* a1_poff = nullptr) {
+               const uint32_t* g1_arrive_tgt = nullptr, const int32_t* a1_poff = nullptr,
+               const CUtensorMap* mA2_padded = nullptr) {
   const bool fp8 = h->precision == CL_MOE_FP8_E4M3;
   GemmArgs g1{};
   g1.offsets = offsets;
@@ -332,6 +333,7 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g1.out = act;
   g1.ldo = static_cast<int>(h->f);
   g1.a_poff = a1_poff;  // single-GPU training: the dispatched rows sit in the padded layout
+  if (mA2_padded) g1.out = nullptr;  // ... and A is written only there (aux_t), GEMM2 reads it there
   g1.act_scale = h->sx_in;
   g1.w_scale = h->ws_in;
   g1.out_scale = h->sx_mid;
@@ -355,6 +357,10 @@ void run_gemms(cl_moe* h, const int32_t* offsets, void* act, __nv_bfloat16* y, c
   g1.half_tail = g2.half_tail = 1;  // 2-CTA: tail m-tiles of <= 128 rows as M=128 pair MMAs
   g2.act_scale = h->sx_mid;
   g2.w_scale = h->ws_out;
+  if (mA2_padded) {
+    g2.a_poff = h->poff;
+    mA2 = mA2_padded;
+  }
   const int v = h->gemm_ctas == 2 ? 1 : 0;
   // clusters of two CTA pairs sharing the B tile by TMA multicast (CL_MOE_GEMM_MC=1)
   static const bool mc_env = [] {

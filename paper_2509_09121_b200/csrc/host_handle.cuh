@@ -238,6 +238,7 @@ struct cl_moe {
   CUtensorMap mAdg1[2], mBdg1[2], mBdg2[2], mAwo[2], mBwo[2], mAwi[2], mBwi[2];
   CUtensorMap mAdg2T[2];  // dgrad-2's A = dH in the padded row layout (GemmArgs::a_poff)
   CUtensorMap mA1T[2], mAdg1T[2];  // single-GPU training: GEMM1's A = X, dgrad-1's A = dY, padded
+  CUtensorMap mA2T[2];             // single-GPU training: GEMM2's A = SwiGLU output, padded
   bool last_xperm_padded = false;  // the last call (single-GPU forward_train) left x_perm padded
   bool mAdg1_ready = false;        // dgrad-1's receive-layout dY map exists (expert parallel)
 

@@ -38,6 +38,7 @@ void ensure_training(cl_moe* h) {
       h->mAdg2T[v] = make_map(h->dHT, false, 2 * f, h->rp_cap, 128);  // dH, padded row layout
       h->mA1T[v] = make_map(h->XT, false, d, h->rp_cap, 128);          // X (single-GPU training)
       h->mAdg1T[v] = make_map(h->dYT, false, d, h->rp_cap, 128);       // dY (single-GPU training)
+      h->mA2T[v] = make_map(h->AT, false, f, h->rp_cap, 128);          // A (single-GPU training)
       h->mBdg2[v] = make_map(h->win_ref, false, 2 * f, (uint64_t)NL * d, brow);
       // weight-gradient operands, MN-major: boxes of 64 columns x 64 padded rows
       h->mAwo[v] = make_map(h->AT, false, f, h->rp_cap, 64);
@@ -80,7 +81,7 @@ void run_forward_train(cl_moe* h, const void* x, int64_t T, void* out, cudaStrea
   CK(cudaGetLastError());
   prof_mark(h, 2, st);
   run_gemms(h, h->rb.offsets, h->act, h->y, nullptr, h->mA1T, h->mA2, h->mA1q, h->mA2q, st, h->Hbuf, nullptr,
-            nullptr, nullptr, nullptr, h->poff);
+            nullptr, nullptr, nullptr, h->poff, h->mA2T);
   prof_mark(h, 4, st);
   launch_combine<__nv_bfloat16>(h->y, h->inv, (int)T, (int)h->d, (int)h->K, static_cast<__nv_bfloat16*>(out),
                                 h->rb.finite_flag, st, h->rb.combine_w);

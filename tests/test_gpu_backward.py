@@ -92,9 +92,10 @@ def test_full_backward_with_router_vs_oracle(t, d, n, k, f, ga, gz):
 
 
 def test_training_forward_keeps_dispatched_rows_padded():
-    """A single-GPU forward_train writes the dispatched rows only into the padded layout the
-    weight gradients (and GEMM1) read: the x_perm stage is then refused (stage contract,
-    compass_moe.h), and an inference forward afterwards materialises it again."""
+    """A single-GPU forward_train writes the dispatched rows and the SwiGLU output only into the
+    padded layouts the weight gradients (and GEMM1 / GEMM2) read: the x_perm and act stages are
+    then refused (stage contract, compass_moe.h), and an inference forward afterwards materialises
+    them again."""
     from paper_2509_09121_b200.moe import MoEConfig, MoEError, MoELayer
     t, d, n, k, f = 300, 256, 4, 2, 256
     inp = make_inputs(t, d, n, f)
@@ -105,6 +106,8 @@ def test_training_forward_keeps_dispatched_rows_padded():
     lay.sync()
     with pytest.raises(MoEError):
         lay.stage("x_perm", (t * k, d), torch.bfloat16)
+    with pytest.raises(MoEError):
+        lay.stage("act", (t * k, f), torch.bfloat16)
     lay.forward(x)
     lay.sync()
     xp = lay.stage("x_perm", (t * k, d), torch.bfloat16)
