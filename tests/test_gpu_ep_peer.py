@@ -24,9 +24,11 @@ def _dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda().to(torch.bfloat16).contiguous()
 
 
+# (the last two: per-rank batches large enough for the fp64 tensor-core router and its finish tiles)
 @pytest.mark.parametrize("R,n,k,ts,gemm_ctas", [(2, 8, 2, (300, 517), 1), (2, 8, 2, (1024, 900), 2),
                                                  (4, 16, 4, (300, 1, 517, 64), 1), (4, 16, 2, (640, 640, 3, 700), 2),
-                                                 (8, 16, 2, (128,) * 8, 1)])
+                                                 (8, 16, 2, (128,) * 8, 1), (2, 8, 2, (4096, 3000), 2),
+                                                 (4, 16, 2, (5000, 3100, 2500, 4000), 2)])
 def test_group_forward_bit_identical_to_single_gpu(R, n, k, ts, gemm_ctas):
     from paper_2509_09121_b200.moe import MoEConfig, MoELayer, ep_group_forward
     d, f = 512, 256
@@ -170,7 +172,7 @@ def test_ep_fp8_calibration_single_rank_nccl(peer):
         assert dl <= 2e-2 * want.float().abs().max().item()
 
 
-@pytest.mark.parametrize("R,n,k,t", [(2, 8, 2, 300), (4, 16, 2, 200)])
+@pytest.mark.parametrize("R,n,k,t", [(2, 8, 2, 300), (4, 16, 2, 200), (2, 8, 2, 3000)])
 def test_group_train_step_bit_identical_to_single_gpu(R, n, k, t):
     """EP training over the peer transport (emulated group): forward_train + expert-FFN backward.
     Ranks hold consecutive token slices, so each expert's receive layout is the single-GPU row
