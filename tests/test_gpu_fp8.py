@@ -25,10 +25,11 @@ def _win_col_of_packed_row(p, f):
     return b * 128 + i if i < 128 else f + b * 128 + (i - 128)
 
 
-@pytest.mark.parametrize("gemm_ctas", [1, 2])
-def test_fp8_layer_vs_qdq_oracle(gemm_ctas):
+# t = 4096: a batch that routes on the fp64 tensor cores (E4M3-code input of router_dmma_kernel)
+@pytest.mark.parametrize("gemm_ctas,t", [(1, 640), (2, 640), (2, 4096)])
+def test_fp8_layer_vs_qdq_oracle(gemm_ctas, t):
     from paper_2509_09121_b200.moe import MoEConfig, MoELayer
-    t, d, n, k, f = 640, 512, 8, 2, 256
+    d, n, k, f = 512, 8, 2, 256
     o = Oracle("port")
     inp = make_inputs(t, d, n, f)
     lay = MoELayer(MoEConfig(d_model=d, n_experts=n, top_k=k, d_ff=f, max_tokens=t, gemm_ctas=gemm_ctas),
@@ -57,6 +58,8 @@ def test_fp8_layer_vs_qdq_oracle(gemm_ctas):
     assert np.array_equal(ws_out, ws_out_ref)
     out, dec = lay.forward(x, want_decision=True)
     lay.sync()
+    if t >= 4096:
+        assert lay.router_variant() == (5, True)
     assert np.array_equal(dec.logits.cpu().numpy(), rq["logits"])
     assert np.array_equal(dec.topk_idx.cpu().numpy().astype(np.int64), rq["topk_idx"])
     assert np.array_equal(dec.counts.cpu().numpy(), rq["counts"])
